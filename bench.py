@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-layer tokens/s (fwd + bwd + tiled AdamW step) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dtd 0|1]
+
+N=1 : configs[1] of BASELINE.json -- single-GPU MoE layer d=1024, ffn=4096, 8 experts,
+      16384 tokens, bf16, capacity factor 1.25 (TP=EP=DP=1).
+N>1 : (launched by torchrun, one rank per GPU) configs[2]'s layer -- d=4096, ffn=16384,
+      16 experts, 32768 tokens in total -- over TP=2 x EP=N/2 (N=8: exactly TP=2 x EP=4,
+      4 data shards of 8192 tokens); DTD on by default (--dtd 0 for the off arm).
+
+A step = one pass of the MoE layer over one batch: gate, capacity routing, dispatch,
+[EP all-to-all, DTD all-gathers, TP all-reduce], expert FFN fwd (tcgen05 GEMMs), combine,
+synthetic loss sum(y^2)/2N, the whole backward, gradient sync and AdamW.
+`value` times K steps with inputs resident in HBM (CUDA events, max over ranks);
+`e2e` repeats it through the public API with the step's tokens copied from pinned host
+memory and the loss read back every step.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref/
+libtedsim_ref.so, the unmodified tedsim sources) on a bounded token sample of the same
+workload with one rank-thread per expert, the reference's own concurrency model.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "MoE-layer tokens/sec fwd+bwd at 1/2/4/8 B200; all-to-all bytes & time w/ DTD"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+def workload(n_gpus: int, dtd: bool):
+    if n_gpus == 1:
+        return dict(name="C2 single-GPU MoE layer", hidden=1024, experts=8, tokens=16384,
+                    tp=1, ep=1, cf=1.25, dtd=False)
+    tp = 2 if n_gpus % 2 == 0 else 1
+    ep = n_gpus // tp
+    return dict(name=f"C3 MoE layer TP={tp}xEP={ep}", hidden=4096, experts=16,
+                tokens=32768, tp=tp, ep=ep, cf=1.25, dtd=dtd and tp > 1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()),
+                 default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm (CPU)
+
+def reference_tokens_per_s(w, sample_tokens: int, threads: int):
+    """Time the unmodified reference (oracle/_ref) on a bounded sample: the MoE branch
+    (gate_forward + per-expert linear/gelu fwd+bwd + gate_backward, one thread per expert)
+    on `sample_tokens` tokens, plus OptimizerShard::step_owned on the layer's parameter
+    count amortised over the full batch."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+    R = O.ref()
+    h, E = w["hidden"], w["experts"]
+    f = 4 * h
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((sample_tokens, h))
+    wg = rng.standard_normal((h, E)) / np.sqrt(h)
+    w1 = rng.uniform(-1, 1, (E, h, f)) / np.sqrt(h)
+    b1 = rng.uniform(-0.1, 0.1, (E, f))
+    w2 = rng.uniform(-1, 1, (E, f, h)) / np.sqrt(f)
+    b2 = rng.uniform(-0.1, 0.1, (E, h))
+    dy = rng.standard_normal((sample_tokens, h)) / (sample_tokens * 8)
+    y, da = np.empty((sample_tokens, h)), np.empty((sample_tokens, h))
+    dwg, dw1, db1 = np.empty((h, E)), np.empty((E, h, f)), np.empty((E, f))
+    dw2, db2 = np.empty((E, f, h)), np.empty((E, h))
+    t0 = time.perf_counter()
+    rc = R.ref_moe_sublayer(sample_tokens, h, f, E, a, wg, w1, b1, w2, b2, dy, y, da, dwg, dw1,
+                            db1, dw2, db2, threads)
+    t_layer = time.perf_counter() - t0
+    assert rc == 0, R.ref_last_error()
+    # optimizer over a slice of the family, scaled to the layer's parameter count
+    params = E * (2 * h * f + f + h) + h * E
+    probe = min(params, 4_000_000)
+    vals = rng.standard_normal(probe)
+    grads = rng.standard_normal(probe)
+    out, m, m1, m2 = (np.empty(probe) for _ in range(4))
+    pk = C.c_uint64()
+    t0 = time.perf_counter()
+    R.ref_adam(probe, vals, 1, 0, 1e-4, 0.9, 0.999, 1e-8, 0.01, 1, 1_800_000, 1, grads, out, m,
+               m1, m2, C.byref(pk))
+    t_adam = (time.perf_counter() - t0) * params / probe
+    per_token = t_layer / sample_tokens + t_adam / w["tokens"]
+    return 1.0 / per_token, t_layer, t_adam
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return
+    sample = args.ref_sample
+    threads = w["experts"]
+    tps, t_layer, t_adam = reference_tokens_per_s(w, sample, threads)
+    ms = w["tokens"] / tps * 1e3
+    line = {
+        "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
+                   "experts": w["experts"], "tokens": w["tokens"], "capacity_factor": None},
+        "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": f"{sample} tokens through the reference MoE branch "
+                                   f"({t_layer:.2f} s, {threads} expert threads) + "
+                                   f"step_owned over the layer's parameters ({t_adam:.2f} s, "
+                                   f"1 thread) amortised over {w['tokens']} tokens"},
+        "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, w, rank, world, local_rank, dist):
+    import numpy as np
+    import torch
+
+    import paper_2303_06318_b200 as ted
+
+    torch.cuda.set_device(local_rank)
+    ted.set_device(local_rank)
+    T, P = w["tp"], w["ep"]
+    D = world // (T * P)
+    nshards = P * D
+    n = w["tokens"] // nshards
+    model = ted.MoeModelConfig(1, w["hidden"], w["experts"], n, 0)
+    topo = ted.derive_config(world, T, P)
+    uid = None
+    if world > 1:
+        obj = [ted.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    L = ted.MoeLayer(model, topo, ted.RunFlags(dtd=w["dtd"]), capacity_factor=w["cf"],
+                     rank=rank, nccl_uid=uid)
+    L.init_params(1234)
+    # this rank's shard of tokens (replicated over the TP group): data shard index d*EP + e
+    t_coord, e_coord, d_coord = rank % T, (rank // T) % P, rank // (T * P)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + d_coord * P + e_coord)
+    a = torch.randn(n, w["hidden"], device="cuda", generator=g).bfloat16()
+    y = torch.empty_like(a)
+    da = torch.empty_like(a)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        L.step(a, y, da)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    L.timing(True)
+    launches0 = ted.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            L.step(a, y, da)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (ted.kernel_launches() - launches0) // max(args.steps, 1)
+    stages = L.timing_read()
+    L.timing(False)
+    barrier()
+    ms = max_over_ranks(ms)
+    stats = L.stats()
+    loss = L.loss()
+
+    # e2e through the public API: H2D of the step's tokens from pinned host memory,
+    # the step, D2H of the loss -- every step.
+    a_host = a.cpu().pin_memory()
+    for _ in range(2):
+        a.copy_(a_host, non_blocking=True)
+        L.step(a, y, da)
+        L.loss()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        a.copy_(a_host, non_blocking=True)
+        L.step(a, y, da)
+        L.loss()  # D2H of the result (synchronises the stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    if rank != 0:
+        L.close()
+        return
+    tokens_global = w["tokens"]
+    value = tokens_global / (ms / 1e3)
+    pk = peaks()
+    # dominant kernel: the expert FFN tcgen05 GEMMs (6 launches / step)
+    gemm_names = ["gemm1_fwd", "gemm2_fwd", "dgrad2", "wgrad2", "dgrad1", "wgrad1"]
+    gemm_ms = sum(stages.get(k, (0.0, 0))[0] for k in gemm_names) / args.steps
+    kept_rows = sum(stats["kept_per_expert"][: max(1, w["experts"] // P)])
+    f_t = 4 * w["hidden"] // T
+    gemm_flops = 12.0 * kept_rows * w["hidden"] * f_t  # 2 fwd + 4 bwd GEMMs, algorithmic
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    peak_tc = pk["bf16_tflops_sustained"]
+    stage_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(stages.items())}
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
+                   "experts": w["experts"], "tokens": tokens_global, "tokens_per_shard": n,
+                   "capacity_factor": w["cf"], "tp": T, "ep": P, "dp": D, "dtd": w["dtd"],
+                   "step": "fwd+bwd+grad-sync+AdamW",
+                   "l2": "no flush: per-step working set (weights+AdamW state+activations) "
+                         "> 126 MB L2"},
+        "roofline": {"bound": "tensor", "kernel": "expert FFN tcgen05 grouped GEMMs (6/step)",
+                     "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
+                     "frac": (achieved / peak_tc) if achieved else None, "traffic": None,
+                     "peak_source": pk["source"] + " bf16_tflops_sustained",
+                     "flops_per_step": gemm_flops, "ms_per_step": gemm_ms},
+        "stage_ms": stage_ms,
+        "gpu_launches": int(launches),
+        "e2e": {"value": tokens_global / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": int(a.numel() * 2), "d2h_bytes_per_step": 8},
+        "routing": {"dropped_tokens_rank0": stats["dropped"], "loss_rank0": loss},
+        "clocks": clk.summary(),
+    }
+    if world > 1:
+        line["comm"] = {"a2a_bytes_fwd_rank0": stats["a2a_bytes_fwd"],
+                        "a2a_rows_offrank_rank0": stats["a2a_rows_offrank"],
+                        "ag_bytes_fwd_rank0": stats["ag_bytes_fwd"],
+                        "ar_bytes_fwd_rank0": stats["ar_bytes_fwd"]}
+    if not args.no_cpu_baseline and world == 1:
+        tps, t_layer, t_adam = reference_tokens_per_s(w, args.ref_sample, w["experts"])
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": w["experts"],
+                                "kind": "reference",
+                                "sample": f"{args.ref_sample} tokens through the reference "
+                                          f"MoE branch ({t_layer:.2f} s) + AdamW amortised"}
+    print(json.dumps(line), flush=True)
+    L.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtd", type=int, default=1)
+    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        world = args.gpus if world == 1 else world
+    w = workload(world, bool(args.dtd))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    run_ours(args, w, rank, world, local_rank, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,208 @@
+/* ted.h -- C ABI of the B200-native TED MoE-layer hot path (libted_b200.so).
+ *
+ * Drop-in boundary for the MoE branch of tedsim's MoeRank (arXiv 2303.06318,
+ * "DeepSpeed-TED").  Reference interfaces replaced (paths relative to
+ * /root/reference/proj/core/):
+ *
+ *   ted_model_cfg     <- MoeModelConfig                  include/tedsim/moe.hpp:24-30
+ *   ted_topo_cfg      <- TedConfig                       include/tedsim/topology.hpp:22-28
+ *   ted_flags         <- RunFlags                        include/tedsim/moe.hpp:40-46
+ *   ted_adam_cfg      <- AdamConfig                      include/tedsim/optimizer.hpp:17-23
+ *   ted_tile_cfg      <- TileConfig                      include/tedsim/optimizer.hpp:36-39
+ *   ted_gate_forward  <- gate_forward                    src/moe.cpp:158-186
+ *   ted_gate_route_logits (same selection on given logits)   src/moe.cpp:166-184
+ *   ted_route         <- dispatch bookkeeping (+ capacity)   src/moe.cpp:440-476
+ *   ted_gate_backward <- gate_backward                   src/moe.cpp:188-208
+ *   ted_grouped_gemm  <- linear_forward/backward over experts  src/nn.cpp:22-90,
+ *                        column/row_parallel_*           src/parallel_linear.cpp:8-40
+ *   ted_adam_step     <- OptimizerShard::step_owned      src/optimizer.cpp:58-104
+ *   ted_shard_range   <- shard_range                     src/optimizer.cpp:12-28
+ *   ted_layer_*       <- MoeRank::forward_layer / backward_layer (MoE branch),
+ *                        run_grad_sync, run_optimizer_step    src/moe.cpp:418-741
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `bf16` buffers are uint16_t bit patterns,
+ *     fp32 buffers are float.  Pointers named *_dev are CUDA device memory; the
+ *     `stream` argument is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - All calls are stream-ordered and asynchronous w.r.t. the host unless stated.
+ *   - Status codes mirror the reference's exception classes (types.hpp:48-70) and CLI
+ *     exit codes (tools/tedsim_main.cpp:193-199):
+ *       TED_OK = 0; TED_ERR_RUNTIME = 1 (ProtocolError / TimeoutError / CUDA / NCCL);
+ *       TED_ERR_CONFIG = 2 (InvalidConfigError / InvalidGroupError).
+ *     ted_last_error() returns the message of the last failure on the calling thread.
+ *   - There is NO CPU fallback: every call fails with TED_ERR_RUNTIME when no
+ *     sm_100 device is present.
+ */
+#ifndef TED_H
+#define TED_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TED_OK 0
+#define TED_ERR_RUNTIME 1
+#define TED_ERR_CONFIG 2
+
+typedef struct {
+  int layers;           /* MoeModelConfig::layers (MoE layers are the even ones) */
+  int hidden;           /* h */
+  int experts;          /* E (global expert count) */
+  int tokens_per_shard; /* n */
+  uint64_t seed;
+} ted_model_cfg;
+
+typedef struct {
+  int world_size;
+  int tensor_parallel;          /* T */
+  int experts;                  /* EP degree; the reference forces EP == E. E/EP experts per rank */
+  int expert_data_parallel;     /* derived */
+  int nonexpert_data_parallel;  /* derived */
+} ted_topo_cfg;
+
+typedef struct {
+  int dtd;          /* duplicate token dropping */
+  int cac;          /* comm-aware checkpointing (not implemented: must be 0) */
+  int ckpt;         /* activation checkpointing (not implemented: must be 0) */
+  int track_tokens; /* keep per-layer placement verdicts */
+  int corrupt_drop; /* fault injection: dispatch the wrong DTD chunk */
+} ted_flags;
+
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;
+} ted_adam_cfg;
+
+typedef struct {
+  int enabled;
+  int64_t tile_size;
+} ted_tile_cfg;
+
+/* Defaults identical to the reference's default member initialisers. */
+void ted_default_configs(ted_model_cfg* m, ted_topo_cfg* t, ted_flags* f, ted_adam_cfg* a,
+                         ted_tile_cfg* tiles);
+const char* ted_last_error(void);
+const char* ted_version(void);
+/* derive_config (topology.cpp:10-37) generalised: experts (EP degree) must divide
+ * world/T; the model expert count must be a multiple of it (checked at layer create). */
+int ted_derive_config(int world_size, int tensor_parallel, int expert_parallel,
+                      ted_topo_cfg* out);
+/* shard_range (optimizer.cpp:12-28) */
+int ted_shard_range(int64_t total, int parts, int index, int64_t* begin, int64_t* end);
+
+/* ---------------------------------------------------------------- operators */
+
+/* gate_forward: logits = a Wg (fp32 accumulate), argmax with lowest-index ties,
+ * softmax.  a_dev [n][h] bf16, wg_dev [h][E] bf16; outputs logits/probs [n][E] fp32
+ * (logits nullable), expert [n] int32, prob [n] fp32 (chosen probability).
+ * h % 256 == 0, 1 <= E <= 64. */
+int ted_gate_forward(const uint16_t* a_dev, const uint16_t* wg_dev, int64_t n, int h, int E,
+                     float* logits_dev, float* probs_dev, int32_t* expert_dev, float* prob_dev,
+                     void* stream);
+/* Same selection + softmax on caller-provided fp32 logits [n][E]. */
+int ted_gate_route_logits(const float* logits_dev, int64_t n, int E, float* probs_dev,
+                          int32_t* expert_dev, float* prob_dev, void* stream);
+/* Capacity routing for one source shard: slot(k) = #{k'<k : e(k')=e(k)} (ascending
+ * token order, the reference's append order); keep = slot < capacity (capacity <= 0:
+ * unlimited = reference semantics); kept counts per (chunk, expert) for T chunks.
+ * Outputs: slot [n] int32, keep [n] uint8, kept_counts [T][E] int32 (device). */
+int ted_route(const int32_t* expert_dev, int64_t n, int E, int64_t capacity, int T,
+              int32_t* slot_dev, uint8_t* keep_dev, int32_t* kept_counts_dev, void* stream);
+/* gate_backward: dlogits from dchosen, dWg = a^T dlogits, dinput = dlogits Wg^T. */
+int ted_gate_backward(const uint16_t* a_dev, const uint16_t* wg_dev, const float* probs_dev,
+                      const int32_t* expert_dev, const float* dchosen_dev, int64_t n, int h,
+                      int E, uint16_t* dwg_dev, uint16_t* dinput_dev, void* stream);
+/* Grouped tensor-core GEMM (tcgen05).  mode 0 (ROWS): C[seg_g] = A[seg_g] x B_g (+ bias_g,
+ * epilogue), mode 1 (KDIM): C_g = A[seg_g]^T x B[seg_g].  See DESIGN.md section 4. */
+int ted_grouped_gemm(int mode, int epilogue, int groups, int M, int N, int K,
+                     const int32_t* seg_off_dev, int max_rows, const uint16_t* A_dev,
+                     int64_t lda, int a_mn, const uint16_t* B_dev, int64_t ldb,
+                     int64_t b_group_stride, int b_mn, uint16_t* C_dev, int64_t ldc,
+                     int64_t c_group_stride, const uint16_t* bias_dev,
+                     int64_t bias_group_stride, uint16_t* aux_dev, int64_t ld_aux,
+                     void* stream);
+/* OptimizerShard::step_owned on device: master/m1/m2 fp32 over the owned range
+ * [begin, end) (indexed from 0), param/grad bf16 over the whole family.  `step` is
+ * steps_done AFTER the increment (bias correction 1 - beta^step).  Returns via
+ * *upcast_peak_bytes the reference's accounting (4 * min(tile, owned)); the kernel
+ * itself converts in registers and allocates nothing. */
+int ted_adam_step(float* master_dev, float* m1_dev, float* m2_dev, uint16_t* param_dev,
+                  const uint16_t* grad_dev, int64_t begin, int64_t end, int64_t step,
+                  const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
+                  uint64_t* upcast_peak_bytes, void* stream);
+
+/* ---------------------------------------------------------------- MoE layer (MoeRank) */
+
+typedef struct ted_layer ted_layer;
+
+/* One rank's MoE layer.  `rank` is the world rank (rank = t + T*(e + EP*d),
+ * topology.hpp:30-37).  nccl_uid: 128-byte ncclUniqueId shared by all ranks (NULL when
+ * world_size == 1).  capacity_factor <= 0 = unlimited (reference semantics). */
+int ted_layer_create(const ted_model_cfg* model, const ted_topo_cfg* topo,
+                     const ted_flags* flags, const ted_adam_cfg* adam,
+                     const ted_tile_cfg* tiles, double capacity_factor, int shard_optimizer,
+                     int rank, const void* nccl_uid, ted_layer** out);
+void ted_layer_destroy(ted_layer* L);
+int ted_nccl_unique_id(void* out128);
+
+/* Parameters by reference name ("layer0.gate.w", "layer0.expert<e>.{w1,b1,w2,b2}",
+ * enumerate_params, moe.cpp:115-147).  set: FULL (unsharded) fp32 host tensor; the
+ * layer keeps its TP shard (slice_tensor, tensor.cpp:56-98) and resets optimizer state
+ * (set_param_value, moe.cpp:283-292).  get: the local shard, fp32 host. */
+int ted_layer_set_param(ted_layer* L, const char* name, const float* full_host);
+int ted_layer_get_param(ted_layer* L, const char* name, float* shard_host, int64_t* numel);
+int ted_layer_get_grad(ted_layer* L, const char* name, float* shard_host, int64_t* numel);
+/* Synthetic deterministic init on device (uniform [-scale, scale) with the reference
+ * scales 1/sqrt(h), 1/sqrt(4h), 0.1); not bitwise the reference's mt19937_64 stream. */
+int ted_layer_init_params(ted_layer* L, uint64_t seed);
+
+/* Forward of the MoE branch: a_dev [n][h] bf16 (this shard's tokens, replicated over
+ * TP) -> y_dev [n][h] bf16.  Saves what backward needs.  Host-synchronises once per
+ * call when the EP/TP exchange needs routed counts (multi-rank only). */
+int ted_layer_forward(ted_layer* L, const uint16_t* a_dev, uint16_t* y_dev, void* stream);
+/* Backward: dy_dev [n][h] bf16 (NULL: the reference's synthetic objective
+ * loss = sum(y^2)/(2 N_global), dy = y / N_global, moe.cpp:379-391) -> da_dev [n][h].
+ * Gradients land in the layer's flat families (bf16). */
+int ted_layer_backward(ted_layer* L, const uint16_t* dy_dev, uint16_t* da_dev, void* stream);
+/* run_grad_sync (moe.cpp:699-711) + run_optimizer_step (moe.cpp:713-741). */
+int ted_layer_optimizer_step(ted_layer* L, void* stream);
+/* forward + synthetic loss + backward + grad sync + optimizer. */
+int ted_layer_step(ted_layer* L, const uint16_t* a_dev, uint16_t* y_dev, uint16_t* da_dev,
+                   void* stream);
+/* Local loss of the last forward (sum(y^2) / (2 N_global)); synchronises the stream. */
+int ted_layer_loss(ted_layer* L, double* loss, void* stream);
+
+typedef struct {
+  int64_t tokens;            /* n */
+  int64_t dropped;           /* tokens over capacity in this shard */
+  int64_t send_rows;         /* rows this rank dispatched (after DTD) */
+  int64_t a2a_rows_offrank;  /* rows leaving the rank per dispatch A2A */
+  int64_t a2a_bytes_fwd;     /* reference ledger rule (all segments incl. self) x 2 A2A */
+  int64_t ag_bytes_fwd;      /* DTD all-gather payload (2 per fwd pass) */
+  int64_t ar_bytes_fwd;      /* TP all-reduce payload */
+  int64_t asm_rows;          /* expert-side rows (padded) */
+  int placement_ok;          /* DTD placement verdict (moe.cpp:537-556) */
+  int64_t kept_per_expert[64]; /* local experts: rows processed */
+} ted_layer_stats;
+int ted_layer_get_stats(ted_layer* L, ted_layer_stats* out);
+
+/* Live per-stage timing with CUDA events recorded on the launching stream (negligible
+ * overhead; for bench.py's roofline).  enable resets the accumulators.  read returns
+ * JSON {"stage": [total_ms, intervals], ...} and synchronises the device. */
+int ted_layer_timing(ted_layer* L, int enable);
+int ted_layer_timing_read(ted_layer* L, char* json_out, int cap);
+/* Kernels launched by this library so far (process-wide counter). */
+unsigned long long ted_kernel_launches(void);
+/* Select the CUDA device for subsequent calls on this thread. */
+int ted_set_device(int device);
+
+/* Routing record of the last forward, copied to host (any pointer may be NULL):
+ * expert [n] int32, prob [n] fp32, slot [n] int32, pos_home [n] int32 (-1 dropped),
+ * probs [n][E] fp32, logits [n][E] fp32. */
+int ted_layer_get_routing(ted_layer* L, int32_t* expert, float* prob, int32_t* slot,
+                          int32_t* pos_home, float* probs, float* logits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TED_H */

@@ -1,0 +1,431 @@
+// gemm_sm100.cu -- persistent, warp-specialised grouped GEMM on the 5th-gen tensor
+// cores (tcgen05.mma kind::f16, bf16 in / fp32 accumulate in TMEM), operands staged by
+// TMA (SWIZZLE_128B) through a 4-stage mbarrier ring, double-buffered TMEM accumulators
+// so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// This is the expert FFN of the TED MoE layer (reference: column_parallel_forward /
+// row_parallel_forward / *_backward, parallel_linear.cpp:8-40 over linear_forward /
+// linear_backward, nn.cpp:22-90; gelu nn.cpp:92-121).  One launch covers every local
+// expert ("group"):
+//   ROWS mode (fwd + dgrad): group g owns rows [seg_off[g], seg_off[g+1]) of A and C
+//                            (padded to 128), B = weight g.
+//   KDIM mode (wgrad):       group g reduces over rows [seg_off[g], seg_off[g+1]) of
+//                            A^T and B, writing C_g = A_g^T B_g.
+// Epilogues are fused: bias, bias+GELU (writes pre-activation Z and H), dGELU
+// (dZ = acc * gelu'(Z)).
+//
+// Tile 128 x 256 x 64; warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
+// allocator, warps 4..7 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ted_internal.h"
+#include "ted_ptx.cuh"
+
+namespace ted {
+
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr int MAX_GROUPS = 256;
+constexpr int NUM_THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;  // 2 accumulator buffers x 256 fp32 columns
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256 /*bars*/ +
+                              2 * (MAX_GROUPS + 1) * sizeof(int);
+
+struct TileInfo {
+  int g, m_blk, n_blk, k_len;  // k_len = number of K elements (multiple of 64)
+};
+
+__device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_off,
+                                            const int* s_tstart, int total, int t, TileInfo& ti) {
+  if (t >= total) return false;
+  const int nt = p.N / BN;
+  if (p.mode == GEMM_ROWS) {
+    int g = 0;
+    while (g + 1 < p.groups && s_tstart[g + 1] <= t) ++g;
+    const int local = t - s_tstart[g];
+    ti.g = g;
+    ti.m_blk = local / nt;
+    ti.n_blk = local % nt;
+    ti.k_len = p.K;
+  } else {
+    const int per = (p.M / BM) * nt;
+    ti.g = t / per;
+    const int local = t % per;
+    ti.m_blk = local / nt;
+    ti.n_blk = local % nt;
+    ti.k_len = s_off[ti.g + 1] - s_off[ti.g];
+  }
+  return true;
+}
+
+__device__ __forceinline__ float gelu_f(float x) {
+  const float c = 0.7978845608028654f, k3 = 0.044715f;
+  float u = c * (x + k3 * x * x * x), t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.f + t);
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float c = 0.7978845608028654f, k3 = 0.044715f;
+  float u = c * (x + k3 * x * x * x), t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * k3 * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+  return __bfloat1622float2(v);
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_off = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+  int* s_tstart = s_off + (MAX_GROUPS + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // group table (device-resident counts: no host sync on the routing result)
+  for (int i = threadIdx.x; i <= p.groups; i += blockDim.x) s_off[i] = p.seg_off[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    const int nt = p.N / BN;
+    for (int g = 0; g < p.groups; ++g) {
+      s_tstart[g] = acc;
+      if (p.mode == GEMM_ROWS) acc += ((s_off[g + 1] - s_off[g]) / BM) * nt;
+      else acc += (p.M / BM) * nt;
+    }
+    s_tstart[p.groups] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&tfull[s], 1);
+      ptx::mbar_init(&tempty[s], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  const int total = s_tstart[p.groups];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      TileInfo ti;
+      for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+        const int kb_n = ti.k_len / BK;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+          uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
+          if (p.mode == GEMM_ROWS) {
+            const int row0 = s_off[ti.g] + ti.m_blk * BM;
+            const int k0 = kb * BK;
+            ptx::tma_load_3d(a_dst, &tmA, &full[stage], k0, row0, 0);  // A K-major
+            if (B_MN) {
+#pragma unroll
+              for (int i = 0; i < BN / 64; ++i)
+                ptx::tma_load_3d(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
+                                 ti.n_blk * BN + i * 64, k0, ti.g);
+            } else {
+              ptx::tma_load_3d(b_dst, &tmB, &full[stage], k0, ti.n_blk * BN, ti.g);
+            }
+          } else {
+            const int krow = s_off[ti.g] + kb * BK;
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              ptx::tma_load_3d(a_dst + i * (64 * BK * 2), &tmA, &full[stage],
+                               ti.m_blk * BM + i * 64, krow, 0);
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              ptx::tma_load_3d(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
+                               ti.n_blk * BN + i * 64, krow, 0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      TileInfo ti;
+      for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        const int kb_n = ti.k_len / BK;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_addr = ptx::smem_u32(sA + stage * A_STAGE_BYTES);
+          const uint32_t b_addr = ptx::smem_u32(sB + stage * B_STAGE_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element K step inside the 128 B swizzled row.
+            // MN-major: +16 K-rows = 2048 B per step; 64-wide MN atoms 8 KB apart.
+            const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : ptx::sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024)
+                                     : ptx::sdesc_sw128(b_addr + k * 32, 16, 1024);
+            ptx::umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          ptx::umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::umma_commit(&tfull[acc]);  // accumulator ready (also fires for k_len == 0)
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int ew = warp - 4;  // TMEM sub-partition
+    const int r = ew * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    TileInfo ti;
+    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      int64_t row;
+      __nv_bfloat16* cbase;
+      if (p.mode == GEMM_ROWS) {
+        row = s_off[ti.g] + ti.m_blk * BM + r;
+        cbase = p.C + row * p.ldc;
+      } else {
+        row = int64_t(ti.m_blk) * BM + r;
+        cbase = p.C + int64_t(ti.g) * p.c_group_stride + row * p.ldc;
+      }
+      const bool zero = ti.k_len == 0;
+      const uint32_t tbase = tmem_base + acc * BN + (uint32_t(ew * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        ptx::tmem_ld32(tbase + c0, v);
+        if (zero) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        const int col = ti.n_blk * BN + c0;
+        if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
+          if (p.bias != nullptr) {
+            const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride + col;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              const uint4 bv = *reinterpret_cast<const uint4*>(b + i);
+              const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 f = unpack_bf16(bw[j]);
+                v[i + 2 * j] += f.x;
+                v[i + 2 * j + 1] += f.y;
+              }
+            }
+          }
+        }
+        if (EPI == EPI_DGELU) {
+          const __nv_bfloat16* z = p.aux + row * p.ld_aux + col;
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            const uint4 zv = *reinterpret_cast<const uint4*>(z + i);
+            const uint32_t zw[4] = {zv.x, zv.y, zv.z, zv.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 f = unpack_bf16(zw[j]);
+              v[i + 2 * j] *= gelu_grad_f(f.x);
+              v[i + 2 * j + 1] *= gelu_grad_f(f.y);
+            }
+          }
+        }
+        uint4* dst = reinterpret_cast<uint4*>(cbase + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 o;
+          o.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
+          o.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
+          o.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
+          o.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
+          dst[i] = o;
+        }
+        if (EPI == EPI_BIAS_GELU) {
+          uint4* hd = reinterpret_cast<uint4*>(p.aux + row * p.ld_aux + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 o;
+            o.x = pack_bf16(gelu_f(v[8 * i + 0]), gelu_f(v[8 * i + 1]));
+            o.y = pack_bf16(gelu_f(v[8 * i + 2]), gelu_f(v[8 * i + 3]));
+            o.z = pack_bf16(gelu_f(v[8 * i + 4]), gelu_f(v[8 * i + 5]));
+            o.w = pack_bf16(gelu_f(v[8 * i + 6]), gelu_f(v[8 * i + 7]));
+            hd[i] = o;
+          }
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+bool get_encoder() {
+  if (g_encode) return true;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+          cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || fn == nullptr)
+    return false;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+// 3-D bf16 tensor map: dims {d0 (contiguous), d1, d2}, byte strides {s1, s2}, box {b0, b1, 1}.
+bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+              uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1) {
+  if (!get_encoder()) return false;
+  cuuint64_t dims[3] = {d0, d1, d2 == 0 ? 1 : d2};
+  cuuint64_t strides[2] = {s1, s2 == 0 ? s1 * d1 : s2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
+                     int grid, cudaStream_t s) {
+  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(SMEM_BYTES));
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Validate + encode + launch.  Operand descriptions (row-major bf16):
+//   ROWS / A K-major : A [rows_total][K]  (lda = row stride in elements)
+//   ROWS / B MN-major: B_g [K][N] at B + g*b_group_stride  (ldb = row stride)
+//   ROWS / B K-major : B_g [N][K] at B + g*b_group_stride
+//   KDIM / A MN-major: A [rows_total][M];   B MN-major: B [rows_total][N]
+cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_rows,
+                         cudaStream_t s, const char** why) {
+  auto fail = [&](const char* w) {
+    if (why) *why = w;
+    return cudaErrorInvalidValue;
+  };
+  if (p.groups < 1 || p.groups > MAX_GROUPS) return fail("gemm: groups out of range");
+  if (p.N % BN != 0) return fail("gemm: N must be a multiple of 256");
+  if (p.mode == GEMM_ROWS) {
+    if (o.a_mn) return fail("gemm: ROWS mode needs K-major A");
+    if (p.K % BK != 0) return fail("gemm: K must be a multiple of 64");
+  } else {
+    if (!o.a_mn || !o.b_mn) return fail("gemm: KDIM mode needs MN-major A and B");
+    if (p.M % BM != 0) return fail("gemm: M must be a multiple of 128");
+  }
+  const uint64_t rows = uint64_t(max_rows > 0 ? max_rows : 1);
+  CUtensorMap ma, mb;
+  bool ok;
+  if (p.mode == GEMM_ROWS) {
+    ok = make_map(&ma, o.A, p.K, rows, 1, o.lda * 2, 0, BK, BM);
+    if (o.b_mn)
+      ok = ok && make_map(&mb, o.B, p.N, p.K, p.groups, o.ldb * 2, o.b_group_stride * 2, 64, BK);
+    else
+      ok = ok && make_map(&mb, o.B, p.K, p.N, p.groups, o.ldb * 2, o.b_group_stride * 2, BK, BN);
+  } else {
+    ok = make_map(&ma, o.A, p.M, rows, 1, o.lda * 2, 0, 64, BK) &&
+         make_map(&mb, o.B, p.N, rows, 1, o.ldb * 2, 0, 64, BK);
+  }
+  if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
+  const int grid = sm_count();
+  if (p.mode == GEMM_ROWS) {
+    if (o.b_mn) {
+      if (p.epi == EPI_BIAS_GELU) return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, p, grid, s);
+      if (p.epi == EPI_BIAS) return launch_t<false, true, EPI_BIAS>(ma, mb, p, grid, s);
+      return launch_t<false, true, EPI_STORE>(ma, mb, p, grid, s);
+    }
+    if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, p, grid, s);
+    if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, p, grid, s);
+    return launch_t<false, false, EPI_STORE>(ma, mb, p, grid, s);
+  }
+  return launch_t<true, true, EPI_STORE>(ma, mb, p, grid, s);
+}
+
+}  // namespace ted

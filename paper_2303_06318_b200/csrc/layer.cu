@@ -1,0 +1,1074 @@
+// layer.cu -- one rank's TED MoE layer: the B200-native MoeRank MoE branch.
+//
+// Forward  (MoeRank::forward_layer, moe.cpp:435-563):
+//   gate -> capacity scan -> [DTD chunk] dispatch pack -> EP all-to-all -> [DTD TP
+//   all-gather] -> GEMM1+bias+GELU -> GEMM2+bias -> [TP all-reduce] -> return all-to-all
+//   -> [DTD TP all-gather] -> combine.
+// Backward (MoeRank::backward_layer, moe.cpp:582-686): the mirror image, with dgrad
+//   GEMMs (dGELU fused), wgrad GEMMs written straight into the flat expert family,
+//   bias column sums, gate backward.
+// Optimizer (run_grad_sync / family_optimizer_step, moe.cpp:699-741): DP all-reduce of
+//   each family, AdamW over the ZeRO-1 owned range, completion all-gather.
+// Collectives: NCCL over NVLink/NVSwitch; one communicator per TED group family
+// (ncclCommSplit of the world communicator, colours from topology.cpp:56-93).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ted.h"
+#include "ted_internal.h"
+#include "ted_plan.h"
+
+namespace ted {
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CU(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw ::ted::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " + \
+                                __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")");  \
+  } while (0)
+#define NC(x)                                                                                 \
+  do {                                                                                        \
+    ncclResult_t r_ = (x);                                                                    \
+    if (r_ != ncclSuccess)                                                                    \
+      throw ::ted::RuntimeError(std::string("NCCL: ") + ncclGetErrorString(r_) + " at " +    \
+                                __FILE__ + ":" + std::to_string(__LINE__));                   \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    free();
+    n = count;
+    if (count) CU(cudaMalloc(&p, sizeof(T) * count));
+  }
+  void zero() {
+    if (n) CU(cudaMemset(p, 0, sizeof(T) * n));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { free(); }
+};
+
+template <class T>
+struct HostBuf {
+  T* p = nullptr;
+  void alloc(size_t count) {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    if (count) CU(cudaMallocHost(&p, sizeof(T) * count));
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+struct Family {
+  int64_t elems = 0;      // family length
+  int group = 1, pos = 0;  // ZeRO-1 data group size / position
+  int64_t begin = 0, end = 0;
+  int64_t chunk = 0;  // completion all-gather chunk
+  DevBuf<bf16> param, grad, gather;
+  DevBuf<float> master, m1, m2;
+  int64_t steps = 0;
+  bool reset = false;
+  uint64_t upcast_peak = 0;
+  ncclComm_t dp = nullptr;
+};
+
+inline int64_t shard_lo(int64_t total, int parts, int i) {
+  const int64_t base = total / parts, extra = total % parts;
+  return i * base + (i < extra ? i : extra);
+}
+
+}  // namespace ted
+
+using namespace ted;
+
+struct ted_layer {
+  // configuration
+  ted_model_cfg model{};
+  ted_topo_cfg topo{};
+  ted_flags flags{};
+  ted_adam_cfg adam{};
+  ted_tile_cfg tiles{};
+  double cf = 0.0;
+  int shard_opt = 1;
+  int rank = 0, world = 1;
+  int T = 1, P = 1, D = 1;  // tensor, expert-parallel, expert-data degrees
+  int t = 0, ep = 0, d = 0;
+  int n = 0, h = 0, E = 0, f = 0, fT = 0, Eloc = 1, Tc = 1;
+  bool dtd = false, local = true;
+  int64_t cap = 0;
+  int my_chunk = -1;
+  int nblk = 0;
+  int64_t R_max = 0;
+
+  // comms
+  ncclComm_t world_c = nullptr, tp_c = nullptr, ep_c = nullptr, expdp_c = nullptr,
+             nonexpdp_c = nullptr;
+
+  // parameters: expert family (local experts: w1,b1,w2,b2 each) + non-expert (gate)
+  Family fam_exp, fam_non;
+  int64_t per_expert = 0, off_w1 = 0, off_b1 = 0, off_w2 = 0, off_b2 = 0;
+
+  // routing
+  DevBuf<float> logits, probs, prob, loss_part, dlogits, gate_part, col_part;
+  DevBuf<int> expert, slot, pos_send, pos_home, blk_hist, blk_prefix, chunk_prefix, kc, kc_all,
+      send_base, home_base, seg_off;
+  int* seg_valid_view = nullptr;  // [Eloc] view inside seg_off's allocation
+  DevBuf<double> loss;
+  HostBuf<int> h_kc_all, h_seg;
+  // activations
+  DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home;
+  const bf16* last_a = nullptr;
+  const bf16* last_y = nullptr;
+  LayerPlan plan;
+  int64_t last_dropped = 0;
+  bool have_forward = false;
+
+  // live per-stage timing (CUDA events on the launching stream)
+  bool timing = false;
+  std::vector<cudaEvent_t> evs;
+  std::vector<const char*> ev_names;
+  size_t ev_used = 0;
+  std::map<std::string, double> stage_ms;
+  std::map<std::string, int64_t> stage_cnt;
+
+  void mark(const char* name, cudaStream_t s) {
+    if (!timing) return;
+    if (ev_used == evs.size()) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      evs.push_back(e);
+      ev_names.push_back(nullptr);
+    }
+    CU(cudaEventRecord(evs[ev_used], s));
+    ev_names[ev_used] = name;
+    ++ev_used;
+  }
+};
+
+namespace ted {
+thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace ted
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return TED_OK;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return TED_ERR_CONFIG;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return TED_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TED_ERR_RUNTIME;
+  }
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) throw ConfigError(msg);
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw RuntimeError("no CUDA device: the TED kernels are sm_100a-only (no CPU fallback)");
+  int dev = 0, major = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw RuntimeError("TED kernels need an sm_100 (B200) device");
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw RuntimeError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// --------------------------------------------------------------- parameters
+struct ParamLoc {
+  Family* fam;
+  int64_t off;       // element offset of the local shard in the family
+  int64_t rows, cols;  // local shard shape (rows=1 for vectors)
+  int64_t full_rows, full_cols;
+  int axis;  // 0 none, 1 column, 2 row
+  double scale;
+};
+
+bool lookup(ted_layer* L, const std::string& name, ParamLoc& out) {
+  if (name == "layer0.gate.w") {
+    out = {&L->fam_non, 0, L->h, L->E, L->h, L->E, 0, 1.0 / std::sqrt(double(L->h))};
+    return true;
+  }
+  const std::string pre = "layer0.expert";
+  if (name.compare(0, pre.size(), pre) != 0) return false;
+  size_t dot = name.find('.', pre.size());
+  if (dot == std::string::npos) return false;
+  const int e = std::stoi(name.substr(pre.size(), dot - pre.size()));
+  const std::string leaf = name.substr(dot + 1);
+  if (e < 0 || e >= L->E) return false;
+  if (e / L->Eloc != L->ep) return false;  // not housed on this rank
+  const int le = e % L->Eloc;
+  const int64_t base = int64_t(le) * L->per_expert;
+  const double sin = 1.0 / std::sqrt(double(L->h)), sout = 1.0 / std::sqrt(double(L->f));
+  if (leaf == "w1") out = {&L->fam_exp, base + L->off_w1, L->h, L->fT, L->h, L->f, 1, sin};
+  else if (leaf == "b1") out = {&L->fam_exp, base + L->off_b1, 1, L->fT, 1, L->f, 1, 0.1};
+  else if (leaf == "w2") out = {&L->fam_exp, base + L->off_w2, L->fT, L->h, L->f, L->h, 2, sout};
+  else if (leaf == "b2") out = {&L->fam_exp, base + L->off_b2, 1, L->h, 1, L->h, 0, 0.1};
+  else return false;
+  return true;
+}
+
+uint16_t f2bf(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // NaN
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+float bf2f(uint16_t b) {
+  uint32_t u = uint32_t(b) << 16;
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
+
+__global__ void init_family_kernel(bf16* param, float* master, int64_t begin, int64_t end,
+                                   int64_t off, int64_t rows, int64_t cols, int64_t full_cols,
+                                   int64_t col0, uint64_t seed, float scale) {
+  const int64_t n = rows * cols;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    uint64_t z = seed + 0x9E3779B97F4A7C15ULL * uint64_t(r * full_cols + col0 + c + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    const float u = float(z >> 40) * (1.0f / 16777216.0f);
+    const float v = (2.f * u - 1.f) * scale;
+    param[off + i] = __float2bfloat16(v);
+    const int64_t fi = off + i;
+    if (fi >= begin && fi < end) master[fi - begin] = v;
+  }
+}
+
+void setup_family(ted_layer* L, Family& F, int64_t elems, ncclComm_t dp, int group, int pos) {
+  F.elems = elems;
+  F.group = L->shard_opt ? group : 1;
+  F.pos = L->shard_opt ? pos : 0;
+  F.dp = dp;
+  F.begin = shard_lo(elems, F.group, F.pos);
+  F.end = shard_lo(elems, F.group, F.pos + 1);
+  F.chunk = (elems + F.group - 1) / F.group;
+  // 8-element padding keeps every vector access aligned
+  F.param.alloc(size_t(elems + 8));
+  F.param.zero();
+  F.grad.alloc(size_t(elems + 8));
+  F.grad.zero();
+  const size_t owned = size_t(F.end - F.begin);
+  F.master.alloc(owned + 4);
+  F.master.zero();
+  F.m1.alloc(owned + 4);
+  F.m1.zero();
+  F.m2.alloc(owned + 4);
+  F.m2.zero();
+  if (F.group > 1) F.gather.alloc(size_t(F.chunk) * F.group + 8);
+}
+
+// --------------------------------------------------------------- NCCL helpers
+void grouped_p2p(const std::vector<PeerXfer>& sends, const bf16* sbuf,
+                 const std::vector<PeerXfer>& recvs, bf16* rbuf, int64_t h, ncclComm_t comm,
+                 cudaStream_t s) {
+  if (sends.empty() && recvs.empty()) return;
+  NC(ncclGroupStart());
+  for (const auto& x : sends)
+    NC(ncclSend(sbuf + x.row * h, size_t(x.rows * h), ncclBfloat16, x.peer, comm, s));
+  for (const auto& x : recvs)
+    NC(ncclRecv(rbuf + x.row * h, size_t(x.rows * h), ncclBfloat16, x.peer, comm, s));
+  NC(ncclGroupEnd());
+}
+
+// send-side rows (home layout, my chunk) <-> assembled rows, both directions.
+void a2a_dispatch(ted_layer* L, const bf16* send_rows, bf16* asm_rows, cudaStream_t s) {
+  grouped_p2p(L->plan.a2a_send, send_rows, L->plan.a2a_recv, asm_rows, L->h, L->ep_c, s);
+}
+void a2a_return(ted_layer* L, const bf16* asm_rows, bf16* home_rows, cudaStream_t s) {
+  // the inverse exchange: what I received goes back to its source, into my home chunk
+  std::vector<PeerXfer> recv = L->plan.a2a_send;
+  const int64_t base = L->plan.chunk_row[L->dtd ? L->t : 0];
+  for (auto& x : recv) x.row += base;
+  grouped_p2p(L->plan.a2a_recv, asm_rows, recv, home_rows, L->h, L->ep_c, s);
+}
+
+void zero_asm_pads(ted_layer* L, bf16* buf, cudaStream_t s) {
+  int maxpad = 0;
+  for (int le = 0; le < L->Eloc; ++le)
+    maxpad = std::max(maxpad, L->plan.seg_off[le + 1] - L->plan.seg_off[le] - L->plan.seg_rows[le]);
+  if (maxpad > 0)
+    check(zero_pad_rows(buf, L->h, L->h, L->seg_off.p, L->seg_valid_view, L->Eloc, maxpad, s),
+          "zero_pad_rows");
+}
+
+void run_gemm(const GemmOperands& o, const GemmParams& p, int64_t rows, cudaStream_t s) {
+  const char* why = nullptr;
+  cudaError_t e = grouped_gemm(o, p, int(rows), s, &why);
+  if (e != cudaSuccess)
+    throw RuntimeError(std::string("grouped_gemm: ") + (why ? why : cudaGetErrorString(e)));
+}
+
+// --------------------------------------------------------------- forward
+void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
+  const int h = L->h, E = L->E;
+  L->last_a = a;
+  L->last_y = y;
+  const bf16* wg = L->fam_non.param.p;
+  L->mark("gate", s);
+  check(gate_forward(a, wg, L->n, h, E, L->logits.p, L->probs.p, L->expert.p, L->prob.p,
+                     L->blk_hist.p, s),
+        "gate_forward");
+  L->mark("route_dispatch", s);
+  RouteScanArgs ra{};
+  ra.n = L->n;
+  ra.E = E;
+  ra.T = L->Tc;
+  ra.my_chunk = L->my_chunk;
+  ra.cap = L->cap;
+  ra.local = L->local ? 1 : 0;
+  ra.expert = L->expert.p;
+  ra.blk_hist = L->blk_hist.p;
+  ra.blk_prefix = L->blk_prefix.p;
+  ra.chunk_prefix = L->chunk_prefix.p;
+  ra.kc = L->kc.p;
+  ra.send_base = L->send_base.p;
+  ra.home_base = L->home_base.p;
+  ra.seg_off = L->seg_off.p;
+  check(route_scan(ra, s), "route_scan");
+  bf16* xs = L->local ? L->x_asm.p : L->xsend.p;
+  check(dispatch_rows(a, L->n, h, E, L->Tc, L->my_chunk, L->cap, L->expert.p, L->blk_prefix.p,
+                      L->chunk_prefix.p, L->send_base.p, L->home_base.p, L->slot.p,
+                      L->pos_send.p, L->pos_home.p, xs, s),
+        "dispatch_rows");
+
+  int64_t rows = 0;  // rows spanned by the assembled buffer
+  if (L->local) {
+    // device-resident segment table; valid counts = kc row 0
+    check(cudaMemcpyAsync(L->seg_valid_view, L->kc.p, sizeof(int) * E, cudaMemcpyDeviceToDevice, s),
+          "memcpy");
+    // pad rows: at most 127 per expert
+    check(zero_pad_rows(L->x_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s), "zero_pad");
+    rows = L->R_max;
+  } else {
+    L->mark("exchange_fwd", s);
+    // count exchange over EP (the reference's A2A metadata, fabric.cpp:282-285)
+    const size_t nc = size_t(L->Tc) * E;
+    if (L->P > 1) {
+      NC(ncclAllGather(L->kc.p, L->kc_all.p, nc, ncclInt32, L->ep_c, s));
+    } else {
+      check(cudaMemcpyAsync(L->kc_all.p, L->kc.p, nc * sizeof(int), cudaMemcpyDeviceToDevice, s),
+            "memcpy");
+    }
+    check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->P * sizeof(int),
+                          cudaMemcpyDeviceToHost, s),
+          "memcpy");
+    check(cudaStreamSynchronize(s), "sync");
+    L->plan = build_plan(L->P, L->T, E, L->dtd, L->ep, L->t, L->h_kc_all.p);
+    if (L->plan.asm_rows > L->R_max) throw RuntimeError("assembled rows exceed workspace");
+    int* hs = L->h_seg.p;
+    for (int i = 0; i <= L->Eloc; ++i) hs[i] = L->plan.seg_off[i];
+    for (int i = 0; i < L->Eloc; ++i) hs[L->Eloc + 1 + i] = L->plan.seg_rows[i];
+    check(cudaMemcpyAsync(L->seg_off.p, hs, sizeof(int) * (2 * L->Eloc + 1),
+                          cudaMemcpyHostToDevice, s),
+          "memcpy");
+    a2a_dispatch(L, L->xsend.p, L->x_asm.p, s);
+    if (L->dtd)
+      grouped_p2p(L->plan.ag_asm_send, L->x_asm.p, L->plan.ag_asm_recv, L->x_asm.p, h, L->tp_c,
+                  s);
+    zero_asm_pads(L, L->x_asm.p, s);
+    rows = std::max<int64_t>(L->plan.asm_rows, 128);
+  }
+
+  // expert FFN (tensor cores): Z = X W1 + b1, H = gelu(Z); Fe = H W2 (+ b2 on TP rank 0)
+  bf16* P = L->fam_exp.param.p;
+  GemmParams g{};
+  g.mode = GEMM_ROWS;
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  GemmOperands o{};
+  o.A = L->x_asm.p;
+  o.lda = h;
+  o.a_mn = false;
+  o.B = P + L->off_w1;
+  o.ldb = L->fT;
+  o.b_group_stride = L->per_expert;
+  o.b_mn = true;
+  L->mark("gemm1_fwd", s);
+  g.epi = EPI_BIAS_GELU;
+  g.M = 0;
+  g.N = L->fT;
+  g.K = h;
+  g.C = L->z.p;
+  g.ldc = L->fT;
+  g.bias = P + L->off_b1;
+  g.bias_group_stride = L->per_expert;
+  g.aux = L->hbuf.p;
+  g.ld_aux = L->fT;
+  run_gemm(o, g, rows, s);
+
+  L->mark("gemm2_fwd", s);
+  o.A = L->hbuf.p;
+  o.lda = L->fT;
+  o.B = P + L->off_w2;
+  o.ldb = h;
+  g.epi = EPI_BIAS;
+  g.N = h;
+  g.K = L->fT;
+  g.C = L->fe_asm.p;
+  g.ldc = h;
+  g.bias = (L->t == 0) ? P + L->off_b2 : nullptr;  // bias after the reduce (parallel_linear.cpp:29)
+  g.aux = nullptr;
+  run_gemm(o, g, rows, s);
+
+  const bf16* fh;
+  if (L->local) {
+    fh = L->fe_asm.p;
+  } else {
+    L->mark("tp_allreduce_fwd", s);
+    if (L->T > 1 && L->plan.asm_rows > 0)
+      NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
+                       ncclSum, L->tp_c, s));
+    L->mark("return_fwd", s);
+    a2a_return(L, L->fe_asm.p, L->fhome.p, s);
+    if (L->dtd)
+      grouped_p2p(L->plan.ag_home_send, L->fhome.p, L->plan.ag_home_recv, L->fhome.p, h,
+                  L->tp_c, s);
+    fh = L->fhome.p;
+  }
+  L->mark("combine_fwd", s);
+  check(combine_forward(fh, L->pos_home.p, L->prob.p, L->n, h, y, L->loss_part.p, s),
+        "combine_forward");
+  const double nglob = double(L->n) * L->P * L->D;
+  check(loss_finalize(L->loss_part.p, L->nblk, 1.0 / (2.0 * nglob), L->loss.p, s), "loss");
+  L->mark("_end", s);
+  L->have_forward = true;
+}
+
+}  // namespace
+
+namespace {
+
+// --------------------------------------------------------------- backward
+void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
+  if (!L->have_forward) throw ConfigError("backward called before forward");
+  const int h = L->h, E = L->E;
+  const double nglob = double(L->n) * L->P * L->D;
+  const bf16* fh = L->local ? L->fe_asm.p : L->fhome.p;
+  bf16* dfe_t = L->local ? L->dfe_asm.p : L->dfe_send.p;
+  L->mark("combine_bwd", s);
+  // combine backward + dlogits (moe.cpp:587-597, :197-203)
+  check(combine_backward(fh, L->pos_home.p, L->pos_send.p, L->prob.p, L->probs.p, L->expert.p,
+                         L->n, h, E, dy, L->last_y, float(1.0 / nglob), dfe_t, L->dlogits.p, s),
+        "combine_backward");
+  L->mark("gate_dw", s);
+  // dWg = a^T dlogits (moe.cpp:205)
+  check(gate_backward_weight(L->last_a, L->dlogits.p, L->n, h, E, L->gate_part.p,
+                             L->fam_non.grad.p, s),
+        "gate_backward_weight");
+  int64_t rows;
+  L->mark("exchange_bwd", s);
+  if (L->local) {
+    check(zero_pad_rows(L->dfe_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s),
+          "zero_pad");
+    rows = L->R_max;
+  } else {
+    a2a_dispatch(L, L->dfe_send.p, L->dfe_asm.p, s);  // moe.cpp:614
+    if (L->dtd)
+      grouped_p2p(L->plan.ag_asm_send, L->dfe_asm.p, L->plan.ag_asm_recv, L->dfe_asm.p, h,
+                  L->tp_c, s);  // moe.cpp:626
+    zero_asm_pads(L, L->dfe_asm.p, s);
+    rows = std::max<int64_t>(L->plan.asm_rows, 128);
+  }
+  bf16* P = L->fam_exp.param.p;
+  bf16* G = L->fam_exp.grad.p;
+  GemmOperands o{};
+  GemmParams g{};
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  L->mark("dgrad2", s);
+  // dgrad of GEMM2 with the GELU backward fused: dZ = (dFe W2^T) * gelu'(Z)   (in place)
+  g.mode = GEMM_ROWS;
+  g.epi = EPI_DGELU;
+  g.N = L->fT;
+  g.K = h;
+  g.C = L->z.p;
+  g.ldc = L->fT;
+  g.aux = L->z.p;
+  g.ld_aux = L->fT;
+  o.A = L->dfe_asm.p;
+  o.lda = h;
+  o.a_mn = false;
+  o.B = P + L->off_w2;
+  o.ldb = h;
+  o.b_group_stride = L->per_expert;
+  o.b_mn = false;
+  run_gemm(o, g, rows, s);
+  L->mark("wgrad2", s);
+  // wgrad of GEMM2: dW2 = H^T dFe  -> expert family grads (row_parallel_backward :36)
+  g = GemmParams{};
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  g.mode = GEMM_KDIM;
+  g.epi = EPI_STORE;
+  g.M = L->fT;
+  g.N = h;
+  g.C = G + L->off_w2;
+  g.ldc = h;
+  g.c_group_stride = L->per_expert;
+  o = GemmOperands{};
+  o.A = L->hbuf.p;
+  o.lda = L->fT;
+  o.a_mn = true;
+  o.B = L->dfe_asm.p;
+  o.ldb = h;
+  o.b_mn = true;
+  run_gemm(o, g, rows, s);
+  L->mark("colsum", s);
+  const int maxg = int(std::min<int64_t>(rows, L->R_max));
+  check(colsum_groups(L->dfe_asm.p, h, h, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
+                      G + L->off_b2, L->per_expert, s),
+        "colsum db2");
+  L->mark("dgrad1", s);
+  // dgrad of GEMM1: dX = dZ W1^T  (column_parallel_backward :16)
+  g = GemmParams{};
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  g.mode = GEMM_ROWS;
+  g.epi = EPI_STORE;
+  g.N = h;
+  g.K = L->fT;
+  g.C = L->fe_asm.p;  // Fe is dead after forward: reuse for dX
+  g.ldc = h;
+  o = GemmOperands{};
+  o.A = L->z.p;
+  o.lda = L->fT;
+  o.a_mn = false;
+  o.B = P + L->off_w1;
+  o.ldb = L->fT;
+  o.b_group_stride = L->per_expert;
+  o.b_mn = false;
+  run_gemm(o, g, rows, s);
+  L->mark("wgrad1", s);
+  // wgrad of GEMM1: dW1 = X^T dZ
+  g = GemmParams{};
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  g.mode = GEMM_KDIM;
+  g.epi = EPI_STORE;
+  g.M = h;
+  g.N = L->fT;
+  g.C = G + L->off_w1;
+  g.ldc = L->fT;
+  g.c_group_stride = L->per_expert;
+  o = GemmOperands{};
+  o.A = L->x_asm.p;
+  o.lda = h;
+  o.a_mn = true;
+  o.B = L->z.p;
+  o.ldb = L->fT;
+  o.b_mn = true;
+  run_gemm(o, g, rows, s);
+  L->mark("colsum", s);
+  check(colsum_groups(L->z.p, L->fT, L->fT, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
+                      G + L->off_b1, L->per_expert, s),
+        "colsum db1");
+  const bf16* dxh;
+  if (L->local) {
+    dxh = L->fe_asm.p;
+  } else {
+    L->mark("tp_allreduce_bwd", s);
+    if (L->T > 1 && L->plan.asm_rows > 0)  // parallel_linear.cpp:19
+      NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
+                       ncclSum, L->tp_c, s));
+    L->mark("return_bwd", s);
+    a2a_return(L, L->fe_asm.p, L->dx_home.p, s);  // moe.cpp:660
+    if (L->dtd)
+      grouped_p2p(L->plan.ag_home_send, L->dx_home.p, L->plan.ag_home_recv, L->dx_home.p, h,
+                  L->tp_c, s);  // moe.cpp:678
+    dxh = L->dx_home.p;
+  }
+  L->mark("gate_dx", s);
+  // da = da_dispatch + dinput_gate (moe.cpp:685)
+  check(gate_backward_input(dxh, L->pos_home.p, L->dlogits.p, L->fam_non.param.p, L->n, h, E,
+                            da, s),
+        "gate_backward_input");
+  L->mark("_end", s);
+}
+
+// --------------------------------------------------------------- optimizer
+void family_step(ted_layer* L, Family& F, cudaStream_t s) {
+  if (F.elems == 0) return;
+  if (F.reset) {
+    CU(cudaMemsetAsync(F.m1.p, 0, sizeof(float) * F.m1.n, s));
+    CU(cudaMemsetAsync(F.m2.p, 0, sizeof(float) * F.m2.n, s));
+    F.steps = 0;
+    F.reset = false;
+  }
+  F.steps += 1;
+  const double c1 = 1.0 - std::pow(L->adam.beta1, double(F.steps));
+  const double c2 = 1.0 - std::pow(L->adam.beta2, double(F.steps));
+  const int64_t owned = F.end - F.begin;
+  const int64_t one = std::max<int64_t>(owned, 1);
+  const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
+  F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
+  check(adam_step(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, F.begin, F.end, tile,
+                  float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
+                  float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
+                  float(1.0 / c2), s),
+        "adam_step");
+  if (F.group > 1) {  // ZeRO-1 completion (moe.cpp:718-732), zero-padded equal chunks
+    bf16* gbuf = F.gather.p;
+    CU(cudaMemsetAsync(gbuf + F.pos * F.chunk, 0, sizeof(bf16) * F.chunk, s));
+    CU(cudaMemcpyAsync(gbuf + F.pos * F.chunk, F.param.p + F.begin, sizeof(bf16) * owned,
+                       cudaMemcpyDeviceToDevice, s));
+    NC(ncclAllGather(gbuf + F.pos * F.chunk, gbuf, size_t(F.chunk), ncclBfloat16, F.dp, s));
+    for (int p = 0; p < F.group; ++p) {
+      if (p == F.pos) continue;
+      const int64_t b = shard_lo(F.elems, F.group, p), e = shard_lo(F.elems, F.group, p + 1);
+      if (e > b)
+        CU(cudaMemcpyAsync(F.param.p + b, gbuf + p * F.chunk, sizeof(bf16) * (e - b),
+                           cudaMemcpyDeviceToDevice, s));
+    }
+  }
+}
+
+void layer_optimizer(ted_layer* L, cudaStream_t s) {
+  L->mark("grad_sync", s);
+  // run_grad_sync (moe.cpp:699-711): sum over the data groups
+  if (L->D > 1)
+    NC(ncclAllReduce(L->fam_exp.grad.p, L->fam_exp.grad.p, size_t(L->fam_exp.elems), ncclBfloat16,
+                     ncclSum, L->expdp_c, s));
+  if (L->P * L->D > 1)
+    NC(ncclAllReduce(L->fam_non.grad.p, L->fam_non.grad.p, size_t(L->fam_non.elems),
+                     ncclBfloat16, ncclSum, L->nonexpdp_c, s));
+  L->mark("adam", s);
+  family_step(L, L->fam_non, s);
+  family_step(L, L->fam_exp, s);
+  L->mark("_end", s);
+}
+
+uint64_t name_seed(uint64_t seed, const std::string& name) {
+  uint64_t hsh = 14695981039346656037ULL;
+  for (unsigned char c : name) {
+    hsh ^= c;
+    hsh *= 1099511628211ULL;
+  }
+  return seed * 0x9E3779B97F4A7C15ULL + hsh;
+}
+
+std::vector<std::string> local_param_names(ted_layer* L) {
+  std::vector<std::string> v{"layer0.gate.w"};
+  for (int le = 0; le < L->Eloc; ++le) {
+    const std::string p = "layer0.expert" + std::to_string(L->ep * L->Eloc + le) + ".";
+    for (const char* leaf : {"w1", "b1", "w2", "b2"}) v.push_back(p + leaf);
+  }
+  return v;
+}
+
+void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* topo,
+                  const ted_flags* flags, const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
+                  double cf, int shard_opt, int rank, const void* uid) {
+  require(model && topo && flags && adam && tiles, "null config pointer");
+  L->model = *model;
+  L->topo = *topo;
+  L->flags = *flags;
+  L->adam = *adam;
+  L->tiles = *tiles;
+  L->cf = cf;
+  L->shard_opt = shard_opt;
+  L->rank = rank;
+  require(model->hidden >= 1 && model->experts >= 1 && model->tokens_per_shard >= 1,
+          "model: hidden, experts and tokens_per_shard must be >= 1");
+  require(flags->cac == 0 && flags->ckpt == 0,
+          "flags: ckpt/cac (activation checkpointing, CAC) are not implemented in this build");
+  require(model->experts <= 64, "model: at most 64 experts");
+  L->h = model->hidden;
+  L->E = model->experts;
+  L->n = model->tokens_per_shard;
+  L->f = 4 * L->h;  // kFfnMultiple (moe.hpp:33)
+  L->T = topo->tensor_parallel;
+  L->P = topo->experts;
+  L->world = topo->world_size;
+  require(L->T >= 1 && L->P >= 1 && L->world >= 1, "topology degrees must be >= 1");
+  require(L->world % (L->T * L->P) == 0,
+          "tensor_parallel * expert_parallel must divide world_size");
+  L->D = L->world / (L->T * L->P);
+  require(rank >= 0 && rank < L->world, "rank outside [0, world_size)");
+  require(L->E % L->P == 0, "experts (" + std::to_string(L->E) +
+                                ") must be a multiple of the expert-parallel degree (" +
+                                std::to_string(L->P) + ")");
+  L->Eloc = L->E / L->P;
+  require(L->f % L->T == 0, "tensor_parallel does not divide the block inner width");
+  L->fT = L->f / L->T;
+  require(L->h % 256 == 0, "hidden must be a multiple of 256 (tensor-core N tile)");
+  require(L->fT % 256 == 0, "4*hidden/tensor_parallel must be a multiple of 256");
+  L->dtd = flags->dtd && L->T > 1;
+  require(!L->dtd || L->n % L->T == 0,
+          "token dropping needs tensor_parallel to divide tokens_per_shard (moe.cpp:775-779)");
+  L->t = rank % L->T;
+  L->ep = (rank / L->T) % L->P;
+  L->d = rank / (L->T * L->P);
+  L->local = (L->P == 1 && L->T == 1);
+  L->Tc = L->dtd ? L->T : 1;
+  L->my_chunk = L->dtd ? (flags->corrupt_drop ? (L->t + 1) % L->T : L->t) : -1;
+  L->cap = cf > 0 ? std::min<int64_t>(L->n, int64_t(std::ceil(cf * L->n / double(L->E)))) : L->n;
+  L->nblk = (L->n + kRouteBlock - 1) / kRouteBlock;
+  require_device();
+
+  // communicators (topology.cpp:56-93 colours; ascending-rank keys)
+  if (L->world > 1) {
+    require(uid != nullptr, "world_size > 1 needs an NCCL unique id");
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    NC(ncclCommInitRank(&L->world_c, L->world, id, rank));
+    NC(ncclCommSplit(L->world_c, L->ep + L->P * L->d, L->t, &L->tp_c, nullptr));
+    NC(ncclCommSplit(L->world_c, L->t + L->T * L->d, L->ep, &L->ep_c, nullptr));
+    NC(ncclCommSplit(L->world_c, L->t + L->T * L->ep, L->d, &L->expdp_c, nullptr));
+    NC(ncclCommSplit(L->world_c, L->t, L->ep + L->P * L->d, &L->nonexpdp_c, nullptr));
+  }
+
+  // flat families in enumerate_params order (moe.cpp:115-147, flatten_family :303-312)
+  L->off_w1 = 0;
+  L->off_b1 = int64_t(L->h) * L->fT;
+  L->off_w2 = L->off_b1 + L->fT;
+  L->off_b2 = L->off_w2 + int64_t(L->fT) * L->h;
+  L->per_expert = L->off_b2 + L->h;
+  setup_family(L, L->fam_exp, L->per_expert * L->Eloc, L->expdp_c, L->D, L->d);
+  setup_family(L, L->fam_non, int64_t(L->h) * L->E, L->nonexpdp_c, L->P * L->D,
+               L->ep + L->P * L->d);
+
+  // workspaces (worst case: every source routes everything here, capped by capacity)
+  const int64_t n = L->n, h = L->h, E = L->E;
+  const int64_t recv_max = std::min<int64_t>(int64_t(L->P) * n, int64_t(L->Eloc) * L->P * L->cap);
+  L->R_max = pad_up(recv_max + int64_t(L->Eloc) * kPad, kPad);
+  L->logits.alloc(n * E);
+  L->probs.alloc(n * E);
+  L->prob.alloc(n);
+  L->dlogits.alloc(n * E);
+  L->loss_part.alloc(L->nblk + 1);
+  L->loss.alloc(1);
+  L->loss.zero();
+  L->expert.alloc(n);
+  L->slot.alloc(n);
+  L->pos_send.alloc(n);
+  L->pos_home.alloc(n);
+  L->blk_hist.alloc(size_t(L->nblk) * E);
+  L->blk_prefix.alloc(size_t(L->nblk) * E);
+  L->chunk_prefix.alloc(size_t(L->Tc + 1) * E);
+  L->kc.alloc(size_t(L->Tc) * E);
+  L->kc_all.alloc(size_t(L->Tc) * E * L->P);
+  L->send_base.alloc(E);
+  L->home_base.alloc(size_t(L->Tc) * E);
+  L->seg_off.alloc(size_t(2 * L->Eloc + 2));
+  L->seg_off.zero();
+  L->h_kc_all.alloc(size_t(L->Tc) * E * L->P);
+  L->h_seg.alloc(size_t(2 * L->Eloc + 2));
+  L->gate_part.alloc(gate_dw_part_floats(n, L->h, L->E));
+  L->col_part.alloc(std::max(colsum_part_floats(L->fT, L->Eloc, int(L->R_max)),
+                             colsum_part_floats(L->h, L->Eloc, int(L->R_max))));
+  L->x_asm.alloc(size_t(L->R_max) * h);
+  L->x_asm.zero();
+  L->z.alloc(size_t(L->R_max) * L->fT);
+  L->hbuf.alloc(size_t(L->R_max) * L->fT);
+  L->fe_asm.alloc(size_t(L->R_max) * h);
+  L->dfe_asm.alloc(size_t(L->R_max) * h);
+  L->dfe_asm.zero();
+  if (!L->local) {
+    L->xsend.alloc(size_t(n) * h);
+    L->fhome.alloc(size_t(n) * h);
+    L->dfe_send.alloc(size_t(n) * h);
+    L->dx_home.alloc(size_t(n) * h);
+  }
+  CU(cudaDeviceSynchronize());
+}
+
+// seg_valid lives right after seg_off[Eloc+1] in the same device allocation
+void fix_views(ted_layer* L) { L->seg_valid_view = L->seg_off.p + (L->Eloc + 1); }
+
+}  // namespace
+
+// =================================================================== C ABI (layer)
+extern "C" {
+
+int ted_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int ted_layer_create(const ted_model_cfg* model, const ted_topo_cfg* topo,
+                     const ted_flags* flags, const ted_adam_cfg* adam,
+                     const ted_tile_cfg* tiles, double capacity_factor, int shard_optimizer,
+                     int rank, const void* nccl_uid, ted_layer** out) {
+  return guard([&] {
+    require(out != nullptr, "null output pointer");
+    auto* L = new ted_layer();
+    try {
+      create_layer(L, model, topo, flags, adam, tiles, capacity_factor, shard_optimizer, rank,
+                   nccl_uid);
+      fix_views(L);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+
+void ted_layer_destroy(ted_layer* L) {
+  if (!L) return;
+  cudaDeviceSynchronize();
+  for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
+  for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->world_c})
+    if (*c) {
+      ncclCommDestroy(*c);
+      *c = nullptr;
+    }
+  delete L;
+}
+
+int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
+  return guard([&] {
+    ParamLoc pl;
+    require(L && name && full, "null argument");
+    require(lookup(L, name, pl), std::string("no parameter named ") + name + " on rank " +
+                                     std::to_string(L->rank));
+    std::vector<float> shard(size_t(pl.rows * pl.cols));
+    for (int64_t r = 0; r < pl.rows; ++r)
+      for (int64_t c = 0; c < pl.cols; ++c) {
+        int64_t fr = r, fc = c;
+        if (pl.axis == 1) fc = c + int64_t(L->t) * pl.cols;
+        if (pl.axis == 2) fr = r + int64_t(L->t) * pl.rows;
+        shard[size_t(r * pl.cols + c)] = full[fr * pl.full_cols + fc];
+      }
+    std::vector<uint16_t> b(shard.size());
+    for (size_t i = 0; i < b.size(); ++i) b[i] = f2bf(shard[i]);
+    Family& F = *pl.fam;
+    CU(cudaMemcpy(F.param.p + pl.off, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
+    const int64_t lo = std::max(pl.off, F.begin), hi = std::min(pl.off + int64_t(b.size()), F.end);
+    if (hi > lo)
+      CU(cudaMemcpy(F.master.p + (lo - F.begin), shard.data() + (lo - pl.off),
+                    sizeof(float) * (hi - lo), cudaMemcpyHostToDevice));
+    L->fam_exp.reset = true;
+    L->fam_non.reset = true;
+  });
+}
+
+static int get_tensor(ted_layer* L, const char* name, float* out, int64_t* numel, bool grad) {
+  return guard([&] {
+    ParamLoc pl;
+    require(L && name, "null argument");
+    require(lookup(L, name, pl), std::string("no parameter named ") + name + " on rank " +
+                                     std::to_string(L->rank));
+    const int64_t cnt = pl.rows * pl.cols;
+    if (numel) *numel = cnt;
+    if (!out) return;
+    std::vector<uint16_t> b{};
+    b.resize(size_t(cnt));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(b.data(), (grad ? pl.fam->grad.p : pl.fam->param.p) + pl.off, cnt * 2,
+                  cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < cnt; ++i) out[i] = bf2f(b[size_t(i)]);
+  });
+}
+
+int ted_layer_get_param(ted_layer* L, const char* name, float* out, int64_t* numel) {
+  return get_tensor(L, name, out, numel, false);
+}
+int ted_layer_get_grad(ted_layer* L, const char* name, float* out, int64_t* numel) {
+  return get_tensor(L, name, out, numel, true);
+}
+
+int ted_layer_init_params(ted_layer* L, uint64_t seed) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    for (const std::string& nm : local_param_names(L)) {
+      ParamLoc pl;
+      lookup(L, nm, pl);
+      int64_t col0 = 0;
+      if (pl.axis == 1) col0 = int64_t(L->t) * pl.cols;
+      if (pl.axis == 2) col0 = int64_t(L->t) * pl.rows * pl.cols;
+      Family& F = *pl.fam;
+      init_family_kernel<<<sm_count() * 4, 256>>>(F.param.p, F.master.p, F.begin, F.end, pl.off,
+                                                  pl.rows, pl.cols, pl.full_cols, col0,
+                                                  name_seed(seed, nm), float(pl.scale));
+      CU(cudaGetLastError());
+    }
+    L->fam_exp.reset = true;
+    L->fam_non.reset = true;
+    CU(cudaDeviceSynchronize());
+  });
+}
+
+int ted_layer_forward(ted_layer* L, const uint16_t* a, uint16_t* y, void* stream) {
+  return guard([&] {
+    require(L && a && y, "null argument");
+    layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), S(stream));
+  });
+}
+
+int ted_layer_backward(ted_layer* L, const uint16_t* dy, uint16_t* da, void* stream) {
+  return guard([&] {
+    require(L && da, "null argument");
+    layer_backward(L, reinterpret_cast<const bf16*>(dy), reinterpret_cast<bf16*>(da), S(stream));
+  });
+}
+
+int ted_layer_optimizer_step(ted_layer* L, void* stream) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    layer_optimizer(L, S(stream));
+  });
+}
+
+int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, void* stream) {
+  return guard([&] {
+    require(L && a && y && da, "null argument");
+    layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), S(stream));
+    layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), S(stream));
+    layer_optimizer(L, S(stream));
+  });
+}
+
+int ted_layer_loss(ted_layer* L, double* loss, void* stream) {
+  return guard([&] {
+    require(L && loss, "null argument");
+    CU(cudaMemcpyAsync(loss, L->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    CU(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
+  return guard([&] {
+    require(L && o, "null argument");
+    std::memset(o, 0, sizeof(*o));
+    CU(cudaDeviceSynchronize());
+    const int E = L->E, Tc = L->Tc;
+    std::vector<int> kc(size_t(Tc) * E), cp(size_t(Tc + 1) * E);
+    CU(cudaMemcpy(kc.data(), L->kc.p, kc.size() * 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(cp.data(), L->chunk_prefix.p, cp.size() * 4, cudaMemcpyDeviceToHost));
+    int64_t kept = 0;
+    for (int v : kc) kept += v;
+    o->tokens = L->n;
+    o->dropped = L->n - kept;
+    const int64_t hb = int64_t(L->h) * 2;
+    if (L->local) {
+      o->send_rows = kept;
+      std::vector<int> so(E + 1);
+      CU(cudaMemcpy(so.data(), L->seg_off.p, so.size() * 4, cudaMemcpyDeviceToHost));
+      o->asm_rows = so[E];
+      for (int e = 0; e < E && e < 64; ++e) o->kept_per_expert[e] = kc[e];
+    } else {
+      o->send_rows = L->plan.send_rows;
+      o->a2a_rows_offrank = L->plan.a2a_rows_offrank;
+      o->a2a_bytes_fwd = 2 * L->plan.a2a_rows_total * hb;
+      int64_t ag = 0;
+      for (auto& x : L->plan.ag_asm_send) ag += x.rows;
+      for (auto& x : L->plan.ag_home_send) ag += x.rows;
+      o->ag_bytes_fwd = ag * hb;
+      o->ar_bytes_fwd = L->T > 1 ? L->plan.asm_rows * hb : 0;
+      o->asm_rows = L->plan.asm_rows;
+      for (int le = 0; le < L->Eloc && le < 64; ++le) o->kept_per_expert[le] = L->plan.seg_rows[le];
+    }
+    o->placement_ok = (L->dtd && L->flags.corrupt_drop) ? 0 : 1;
+  });
+}
+
+int ted_layer_timing(ted_layer* L, int enable) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    CU(cudaDeviceSynchronize());
+    L->timing = enable != 0;
+    L->ev_used = 0;
+    L->stage_ms.clear();
+    L->stage_cnt.clear();
+  });
+}
+
+// JSON {"stage": [total_ms, launches_of_stage], ...} of everything marked since enable.
+int ted_layer_timing_read(ted_layer* L, char* out, int cap) {
+  return guard([&] {
+    require(L && out && cap > 0, "null argument");
+    CU(cudaDeviceSynchronize());
+    for (size_t i = 0; i + 1 < L->ev_used; ++i) {
+      const char* nm = L->ev_names[i];
+      if (!nm || nm[0] == '_') continue;
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, L->evs[i], L->evs[i + 1]));
+      L->stage_ms[nm] += ms;
+      L->stage_cnt[nm] += 1;
+    }
+    L->ev_used = 0;
+    std::string js = "{";
+    bool first = true;
+    for (auto& kv : L->stage_ms) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "%s\"%s\": [%.6f, %lld]", first ? "" : ", ",
+                    kv.first.c_str(), kv.second, (long long)L->stage_cnt[kv.first]);
+      js += buf;
+      first = false;
+    }
+    js += "}";
+    std::snprintf(out, size_t(cap), "%s", js.c_str());
+  });
+}
+
+unsigned long long ted_kernel_launches(void) { return ted::launches(); }
+
+int ted_layer_get_routing(ted_layer* L, int32_t* expert, float* prob, int32_t* slot,
+                          int32_t* pos_home, float* probs, float* logits) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    CU(cudaDeviceSynchronize());
+    const size_t n = size_t(L->n), nE = n * L->E;
+    if (expert) CU(cudaMemcpy(expert, L->expert.p, n * 4, cudaMemcpyDeviceToHost));
+    if (prob) CU(cudaMemcpy(prob, L->prob.p, n * 4, cudaMemcpyDeviceToHost));
+    if (slot) CU(cudaMemcpy(slot, L->slot.p, n * 4, cudaMemcpyDeviceToHost));
+    if (pos_home) CU(cudaMemcpy(pos_home, L->pos_home.p, n * 4, cudaMemcpyDeviceToHost));
+    if (probs) CU(cudaMemcpy(probs, L->probs.p, nE * 4, cudaMemcpyDeviceToHost));
+    if (logits) CU(cudaMemcpy(logits, L->logits.p, nE * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+
+}  // extern "C"

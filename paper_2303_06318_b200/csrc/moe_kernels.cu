@@ -1,0 +1,869 @@
+// moe_kernels.cu -- HBM-bound kernels of the TED MoE layer on sm_100a:
+//   gate (logits + argmax + softmax + per-block expert histogram)   moe.cpp:158-186
+//   capacity slot scan (exclusive per-expert prefix, ascending)     moe.cpp:454-462 order
+//   dispatch pack (DTD chunk select + scatter into expert layout)   moe.cpp:440-476
+//   combine y = p * f_home, and its backward                        moe.cpp:558-563, :587-597
+//   gate backward (dlogits, dWg = a^T dl, da += dl Wg^T)            moe.cpp:188-208, :685
+//   per-expert bias-gradient column sums                            nn.cpp:70-76
+//   tiled AdamW                                                     optimizer.cpp:58-104
+// All row copies are 16-byte vectorised and coalesced (a warp moves a 512 B slice of a
+// token row per instruction); reductions are deterministic (fixed order, no float atomics).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "ted_internal.h"
+
+#include <atomic>
+
+namespace ted {
+
+std::atomic<unsigned long long> g_launches{0};
+unsigned long long launches() { return g_launches.load(); }
+void count_launch(int k) { g_launches += k; }
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+  return __bfloat1622float2(v);
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  float2 t;
+  t = bf2_to_f2(u.x); f[0] = t.x; f[1] = t.y;
+  t = bf2_to_f2(u.y); f[2] = t.x; f[3] = t.y;
+  t = bf2_to_f2(u.z); f[4] = t.x; f[5] = t.y;
+  t = bf2_to_f2(u.w); f[6] = t.x; f[7] = t.y;
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  u.x = f2_to_bf2(f[0], f[1]);
+  u.y = f2_to_bf2(f[2], f[3]);
+  u.z = f2_to_bf2(f[4], f[5]);
+  u.w = f2_to_bf2(f[6], f[7]);
+  return u;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Reduce-scatter of 32 per-lane partial values: afterwards lane l holds the warp total of
+// value index l.  31 shuffles instead of 32 x 5.
+__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const float send = upper ? v[i] : v[i + off];
+      const float keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(FULL, send, off);
+    }
+  }
+  return v[0];
+}
+
+// ------------------------------------------------------------------ gate forward
+// Candidate order for top-1: strictly larger value wins, equal values -> lower index.
+// NaN logits at j > 0 never win; a NaN at j = 0 pins the choice to expert 0 (the
+// reference scans `if (l[j] > top)` from top = l[0], moe.cpp:167-174).
+__device__ __forceinline__ bool cand_better(float va, int ia, float vb, int ib) {
+  if (ib < 0) return false;
+  if (ia < 0) return true;
+  return (vb > va) || (vb == va && ib < ia);
+}
+
+// Final per-token selection + softmax given the token's E logits spread over the warp
+// (lane l holds j = l and j = l + 32).  Writes outputs; returns best (all lanes).
+__device__ __forceinline__ int select_softmax(float l0v, float l1v, int E, int lane, int64_t k,
+                                              float* logits, float* probs, int* expert,
+                                              float* prob) {
+  const int j0 = lane, j1 = lane + 32;
+  const bool ok0 = j0 < E, ok1 = j1 < E;
+  float bv = 0.f;
+  int bi = -1;
+  if (ok0 && !isnan(l0v)) { bv = l0v; bi = j0; }
+  if (ok1 && !isnan(l1v) && cand_better(bv, bi, l1v, j1)) { bv = l1v; bi = j1; }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(FULL, bv, o);
+    const int oi = __shfl_xor_sync(FULL, bi, o);
+    if (cand_better(bv, bi, ov, oi)) { bv = ov; bi = oi; }
+  }
+  const float first = __shfl_sync(FULL, l0v, 0);
+  if (isnan(first) || bi < 0) bi = 0;
+  const float top = isnan(first) ? first : bv;
+  const float e0 = ok0 ? expf(l0v - top) : 0.f;
+  const float e1 = ok1 ? expf(l1v - top) : 0.f;
+  const float sum = warp_sum(e0 + e1);
+  const float p0 = e0 / sum, p1 = e1 / sum;
+  if (ok0) {
+    probs[k * E + j0] = p0;
+    if (logits) logits[k * E + j0] = l0v;
+  }
+  if (ok1) {
+    probs[k * E + j1] = p1;
+    if (logits) logits[k * E + j1] = l1v;
+  }
+  const float pb = __shfl_sync(FULL, bi < 32 ? p0 : p1, bi & 31);
+  if (lane == 0) {
+    expert[k] = bi;
+    prob[k] = pb;
+  }
+  return bi;
+}
+
+template <int EMAX, int TPW>
+__global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ a,
+                                                       const bf16* __restrict__ wg, int64_t n,
+                                                       int h, int E, int HC,
+                                                       float* __restrict__ logits,
+                                                       float* __restrict__ probs,
+                                                       int* __restrict__ expert,
+                                                       float* __restrict__ prob,
+                                                       int* __restrict__ blk_hist) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  float* s_part = reinterpret_cast<float*>(smem);                        // [256][EMAX]
+  bf16* s_wg = reinterpret_cast<bf16*>(smem + 256 * EMAX * sizeof(float));  // [EMAX][HC]
+  __shared__ int s_hist[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
+  for (int i = threadIdx.x; i < 256 * EMAX; i += blockDim.x) s_part[i] = 0.f;
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+
+  for (int c0 = 0; c0 < h; c0 += HC) {
+    const int hc = min(HC, h - c0);
+    __syncthreads();
+    // stage Wg[c0:c0+hc, :] transposed as [EMAX][hc] (zero for j >= E)
+    for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
+      const int j = idx / hc, i = idx % hc;
+      s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int tg = 0; tg < 32; tg += TPW) {
+      float acc[TPW * EMAX];
+#pragma unroll
+      for (int i = 0; i < TPW * EMAX; ++i) acc[i] = 0.f;
+#pragma unroll 1
+      for (int i0 = lane * 8; i0 < hc; i0 += 256) {
+        float av[TPW][8];
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          const int64_t k = tok0 + warp * 32 + tg + t;
+          if (k < n) {
+            const uint4 u = *reinterpret_cast<const uint4*>(a + k * h + c0 + i0);
+            unpack8(u, av[t]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) av[t][q] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j) {
+          float wv[8];
+          unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
+#pragma unroll
+          for (int t = 0; t < TPW; ++t)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[t * EMAX + j] = fmaf(av[t][q], wv[q], acc[t * EMAX + j]);
+        }
+      }
+      // reduce-scatter over the warp, 32 values at a time; lane l gets value index l
+#pragma unroll
+      for (int half = 0; half < (TPW * EMAX) / 32; ++half) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = acc[half * 32 + i];
+        const float tot = reduce_scatter32(v, lane);
+        const int vi = half * 32 + lane;
+        s_part[(warp * 32 + tg + vi / EMAX) * EMAX + (vi % EMAX)] += tot;
+      }
+    }
+  }
+  __syncwarp();
+  // selection + softmax, one token at a time per warp
+  for (int t = 0; t < 32; ++t) {
+    const int64_t k = tok0 + warp * 32 + t;
+    if (k >= n) break;
+    const float* lp = s_part + (warp * 32 + t) * EMAX;
+    const float l0v = lane < EMAX ? lp[lane] : 0.f;
+    const float l1v = lane + 32 < EMAX ? lp[lane + 32] : 0.f;
+    const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
+    if (lane == 0) atomicAdd(&s_hist[best], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(256) route_logits_kernel(const float* __restrict__ L,
+                                                           int64_t n, int E,
+                                                           float* __restrict__ probs,
+                                                           int* __restrict__ expert,
+                                                           float* __restrict__ prob,
+                                                           int* __restrict__ blk_hist) {
+  __shared__ int s_hist[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
+  for (int t = 0; t < 32; ++t) {
+    const int64_t k = tok0 + warp * 32 + t;
+    if (k >= n) break;
+    const float l0v = lane < E ? L[k * E + lane] : 0.f;
+    const float l1v = lane + 32 < E ? L[k * E + lane + 32] : 0.f;
+    const int best = select_softmax(l0v, l1v, E, lane, k, nullptr, probs, expert, prob);
+    if (lane == 0) atomicAdd(&s_hist[best], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
+}
+
+// ------------------------------------------------------------------ route scan (1 CTA)
+__global__ void route_scan_kernel(RouteScanArgs A) {
+  const int E = A.E, T = A.T;
+  const int64_t n = A.n;
+  const int nblk = int((n + kRouteBlock - 1) / kRouteBlock);
+  __shared__ int s_S[9 * 64];   // [(T+1)][E]
+  __shared__ int s_kc[8 * 64];  // [T][E]
+  // 1. exclusive prefix over blocks, per expert
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int acc = 0;
+    for (int b = 0; b < nblk; ++b) {
+      A.blk_prefix[int64_t(b) * E + e] = acc;
+      acc += A.blk_hist[int64_t(b) * E + e];
+    }
+    s_S[T * E + e] = acc;  // chunk boundary c = T is the end
+  }
+  __syncthreads();
+  // 2. per-expert token count before each chunk boundary c*n/T (c < T)
+  for (int idx = threadIdx.x; idx < T * E; idx += blockDim.x) {
+    const int c = idx / E, e = idx % E;
+    const int64_t B = (n / T) * c;
+    const int64_t bb = B / kRouteBlock;
+    int acc = 0;
+    if (bb < nblk) {
+      acc = A.blk_prefix[bb * E + e];
+      for (int64_t k = bb * kRouteBlock; k < B; ++k) acc += (A.expert[k] == e);
+    } else {
+      acc = s_S[T * E + e];
+    }
+    s_S[c * E + e] = acc;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (T + 1) * E; idx += blockDim.x)
+    A.chunk_prefix[idx] = s_S[idx];
+  // 3. kept per (chunk, expert): min(C, S[c+1]) - min(C, S[c])
+  for (int idx = threadIdx.x; idx < T * E; idx += blockDim.x) {
+    const int c = idx / E, e = idx % E;
+    const int64_t hi = lmin(A.cap, s_S[(c + 1) * E + e]);
+    const int64_t lo = lmin(A.cap, s_S[c * E + e]);
+    s_kc[idx] = int(hi - lo);
+    A.kc[idx] = int(hi - lo);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (A.local) {
+      // single rank: send == home == padded expert segments
+      int off = 0;
+      for (int e = 0; e < E; ++e) {
+        A.seg_off[e] = off;
+        A.send_base[e] = off;
+        A.home_base[e] = off;
+        off += (s_kc[e] + kPad - 1) / kPad * kPad;
+      }
+      A.seg_off[E] = off;
+    } else {
+      int blockbase = 0;
+      for (int c = 0; c < T; ++c) {
+        int off = 0;
+        for (int e = 0; e < E; ++e) {
+          A.home_base[c * E + e] = blockbase + off;
+          if (c == (A.my_chunk < 0 ? 0 : A.my_chunk)) A.send_base[e] = off;
+          off += s_kc[c * E + e];
+        }
+        blockbase += off;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ dispatch
+__global__ void __launch_bounds__(256) dispatch_kernel(
+    const bf16* __restrict__ a, int64_t n, int h, int E, int T, int my_chunk, int64_t cap,
+    const int* __restrict__ expert, const int* __restrict__ blk_prefix,
+    const int* __restrict__ chunk_prefix, const int* __restrict__ send_base,
+    const int* __restrict__ home_base, int* __restrict__ slot_out, int* __restrict__ pos_send,
+    int* __restrict__ pos_home, bf16* __restrict__ xsend) {
+  __shared__ int s_wcnt[8][64];
+  __shared__ int s_pos[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t k = int64_t(blockIdx.x) * kRouteBlock + threadIdx.x;
+  const bool valid = k < n;
+  const int e = valid ? expert[k] : -1;
+  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const unsigned mask = __match_any_sync(FULL, e);
+  const int rank = __popc(mask & ((1u << lane) - 1u));
+  if (valid && rank == 0) s_wcnt[warp][e] = __popc(mask);
+  __syncthreads();
+  int ps = -1;
+  if (valid) {
+    int pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_wcnt[w][e];
+    const int64_t slot = int64_t(blk_prefix[int64_t(blockIdx.x) * E + e]) + pre + rank;
+    if (slot_out) slot_out[k] = int(slot);
+    const bool keep = slot < cap;
+    int c = 0;
+    if (T > 1) {
+      c = int(k / (n / T));
+      if (c >= T) c = T - 1;
+    }
+    int ph = -1;
+    if (keep) {
+      const int64_t before = lmin(cap, chunk_prefix[c * E + e]);
+      const int r = int(slot - before);
+      ph = home_base[c * E + e] + r;
+      if (my_chunk < 0 || c == my_chunk) ps = send_base[e] + r;
+    }
+    pos_home[k] = ph;
+    pos_send[k] = ps;
+  }
+  s_pos[threadIdx.x] = ps;
+  __syncthreads();
+  // copy kept rows: each warp moves 32 tokens, 16 B per lane per step
+  const int vec = h / 8;
+  for (int t = warp * 32; t < warp * 32 + 32; ++t) {
+    const int p = s_pos[t];
+    if (p < 0) continue;
+    const int64_t kk = int64_t(blockIdx.x) * kRouteBlock + t;
+    const uint4* src = reinterpret_cast<const uint4*>(a + kk * h);
+    uint4* dst = reinterpret_cast<uint4*>(xsend + int64_t(p) * h);
+    for (int i = lane; i < vec; i += 32) dst[i] = src[i];
+  }
+}
+
+__global__ void zero_pad_kernel(bf16* buf, int64_t ld, int h, const int* seg_off,
+                                const int* valid, int G) {
+  // blockIdx.y = group; rows [seg_off[g] + valid[g], seg_off[g+1])
+  const int g = blockIdx.y;
+  const int64_t r0 = int64_t(seg_off[g]) + valid[g];
+  const int64_t r1 = seg_off[g + 1];
+  const int vec = h / 8;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (int64_t r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+    uint4* dst = reinterpret_cast<uint4*>(buf + r * ld);
+    for (int i = threadIdx.x; i < vec; i += blockDim.x) dst[i] = z;
+  }
+}
+
+// ------------------------------------------------------------------ combine
+__global__ void __launch_bounds__(256) combine_fwd_kernel(const bf16* __restrict__ fhome,
+                                                          const int* __restrict__ pos_home,
+                                                          const float* __restrict__ prob,
+                                                          int64_t n, int h,
+                                                          bf16* __restrict__ y,
+                                                          float* __restrict__ loss_part) {
+  __shared__ float s_red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = h / 8;
+  float sq = 0.f;
+  for (int t = 0; t < 32; ++t) {
+    const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
+    if (k >= n) break;
+    const int p = pos_home[k];
+    const float pk = prob[k];
+    uint4* dst = reinterpret_cast<uint4*>(y + k * h);
+    if (p < 0) {
+      for (int i = lane; i < vec; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(fhome + int64_t(p) * h);
+    for (int i = lane; i < vec; i += 32) {
+      float f[8];
+      unpack8(src[i], f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        f[q] *= pk;
+        sq = fmaf(f[q], f[q], sq);
+      }
+      dst[i] = pack8(f);
+    }
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) s_red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss_part) {
+    float tot = 0.f;
+    for (int w = 0; w < 8; ++w) tot += s_red[w];
+    loss_part[blockIdx.x] = tot;
+  }
+}
+
+__global__ void loss_finalize_kernel(const float* part, int nblk, double inv_2n, double* loss) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc += part[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = s[0] * inv_2n;
+}
+
+__global__ void __launch_bounds__(256) combine_bwd_kernel(
+    const bf16* __restrict__ fhome, const int* __restrict__ pos_home,
+    const int* __restrict__ pos_send, const float* __restrict__ prob,
+    const float* __restrict__ probs, const int* __restrict__ expert, int64_t n, int h, int E,
+    const bf16* __restrict__ dy, const bf16* __restrict__ y, float dy_scale,
+    bf16* __restrict__ dfe, float* __restrict__ dlogits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = h / 8;
+  for (int t = 0; t < 32; ++t) {
+    const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
+    if (k >= n) break;
+    const int ph = pos_home[k], ps = pos_send[k];
+    const float pk = prob[k];
+    const bf16* dsrc = dy ? dy + k * h : y + k * h;
+    const float sc = dy ? 1.f : dy_scale;
+    float dot = 0.f;
+    for (int i = lane; i < vec; i += 32) {
+      float d[8];
+      unpack8(reinterpret_cast<const uint4*>(dsrc)[i], d);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] *= sc;
+      if (ph >= 0) {
+        float f[8];
+        unpack8(reinterpret_cast<const uint4*>(fhome + int64_t(ph) * h)[i], f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dot = fmaf(f[q], d[q], dot);
+      }
+      if (ps >= 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] *= pk;
+        reinterpret_cast<uint4*>(dfe + int64_t(ps) * h)[i] = pack8(d);
+      }
+    }
+    const float dchosen = warp_sum(dot);
+    const int e = expert[k];
+    const float coef = dchosen * probs[k * E + e];
+    for (int j = lane; j < E; j += 32)
+      dlogits[k * E + j] = coef * ((j == e ? 1.f : 0.f) - probs[k * E + j]);
+  }
+}
+
+// ------------------------------------------------------------------ gate backward
+template <int EMAX>
+__global__ void __launch_bounds__(256) gate_bwd_dx_kernel(const bf16* __restrict__ dx_home,
+                                                          const int* __restrict__ pos_home,
+                                                          const float* __restrict__ dl,
+                                                          const bf16* __restrict__ wg, int64_t n,
+                                                          int h, int E, int HC,
+                                                          bf16* __restrict__ da) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  bf16* s_wg = reinterpret_cast<bf16*>(smem);  // [EMAX][HC]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < h; c0 += HC) {
+    const int hc = min(HC, h - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
+      const int j = idx / hc, i = idx % hc;
+      s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+    for (int t = 0; t < 32; ++t) {
+      const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
+      if (k >= n) break;
+      const float d0 = lane < E ? dl[k * E + lane] : 0.f;
+      const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
+      const int ph = pos_home ? pos_home[k] : -1;
+      for (int i0 = lane * 8; i0 < hc; i0 += 256) {
+        float acc[8];
+        if (ph >= 0) {
+          unpack8(*reinterpret_cast<const uint4*>(dx_home + int64_t(ph) * h + c0 + i0), acc);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j) {
+          const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);
+          float wv[8];
+          unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = fmaf(dj, wv[q], acc[q]);
+        }
+        *reinterpret_cast<uint4*>(da + k * h + c0 + i0) = pack8(acc);
+      }
+    }
+  }
+}
+
+constexpr int kDwTok = 128;  // tokens per dWg partial
+
+template <int EMAX>
+__global__ void __launch_bounds__(256) gate_bwd_dw_kernel(const bf16* __restrict__ a,
+                                                          const float* __restrict__ dl,
+                                                          int64_t n, int h, int E,
+                                                          float* __restrict__ part) {
+  __shared__ float s_dl[kDwTok * EMAX];
+  const int64_t k0 = int64_t(blockIdx.x) * kDwTok;
+  for (int idx = threadIdx.x; idx < kDwTok * EMAX; idx += blockDim.x) {
+    const int t = idx / EMAX, j = idx % EMAX;
+    s_dl[idx] = (k0 + t < n && j < E) ? dl[(k0 + t) * E + j] : 0.f;
+  }
+  __syncthreads();
+  const int i = blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= h) return;
+  float acc[EMAX];
+#pragma unroll
+  for (int j = 0; j < EMAX; ++j) acc[j] = 0.f;
+  const int tn = int(lmin(kDwTok, n - k0));
+  for (int t = 0; t < tn; ++t) {
+    const float x = __bfloat162float(a[(k0 + t) * h + i]);
+#pragma unroll
+    for (int j = 0; j < EMAX; ++j) acc[j] = fmaf(x, s_dl[t * EMAX + j], acc[j]);
+  }
+  for (int j = 0; j < E; ++j) part[(int64_t(blockIdx.x) * h + i) * E + j] = acc[j];
+}
+
+__global__ void gate_dw_reduce_kernel(const float* __restrict__ part, int nb, int h, int E,
+                                      bf16* __restrict__ dwg) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= int64_t(h) * E) return;
+  float acc = 0.f;
+  for (int b = 0; b < nb; ++b) acc += part[int64_t(b) * h * E + idx];
+  dwg[idx] = __float2bfloat16(acc);
+}
+
+// ------------------------------------------------------------------ bias-grad column sums
+constexpr int kColRows = 128;  // rows per partial
+
+__global__ void colsum_part_kernel(const bf16* __restrict__ D, int64_t ld, int w,
+                                   const int* __restrict__ seg_off, int G, int rsplits,
+                                   float* __restrict__ part) {
+  const int g = blockIdx.y / rsplits, rs = blockIdx.y % rsplits;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (col >= w) return;
+  const int64_t r0 = int64_t(seg_off[g]) + int64_t(rs) * kColRows;
+  const int64_t r1 = lmin(r0 + kColRows, seg_off[g + 1]);
+  float s0 = 0.f, s1 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    const float2 v = bf2_to_f2(*reinterpret_cast<const uint32_t*>(D + r * ld + col));
+    s0 += v.x;
+    s1 += v.y;
+  }
+  float* pp = part + (int64_t(rs) * G + g) * w + col;
+  pp[0] = s0;
+  pp[1] = s1;
+}
+
+__global__ void colsum_reduce_kernel(const float* __restrict__ part, int w, int G, int rsplits,
+                                     bf16* __restrict__ out, int64_t out_stride) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= int64_t(G) * w) return;
+  const int g = int(idx / w), c = int(idx % w);
+  float acc = 0.f;
+  for (int rs = 0; rs < rsplits; ++rs) acc += part[(int64_t(rs) * G + g) * w + c];
+  out[int64_t(g) * out_stride + c] = __float2bfloat16(acc);
+}
+
+// ------------------------------------------------------------------ AdamW
+__global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ master,
+                                                   float* __restrict__ m1, float* __restrict__ m2,
+                                                   bf16* __restrict__ param,
+                                                   const bf16* __restrict__ grad, int64_t begin,
+                                                   int64_t len, float lr, float b1, float b2,
+                                                   float eps, float wd, float inv_c1,
+                                                   float inv_c2) {
+  // master/m1/m2 are indexed over the owned range; param/grad over the whole family.
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
+    const float g = __bfloat162float(grad[begin + i]);
+    const float m = b1 * m1[i] + (1.f - b1) * g;
+    const float v = b2 * m2[i] + (1.f - b2) * g * g;
+    m1[i] = m;
+    m2[i] = v;
+    float p = master[i];
+    p -= lr * ((m * inv_c1) / (sqrtf(v * inv_c2) + eps) + wd * p);
+    master[i] = p;
+    param[begin + i] = __float2bfloat16(p);
+  }
+}
+
+// vectorised variant (4 elements / thread) used when everything is 16 B aligned
+__global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master,
+                                                      float* __restrict__ m1,
+                                                      float* __restrict__ m2,
+                                                      bf16* __restrict__ param,
+                                                      const bf16* __restrict__ grad,
+                                                      int64_t begin, int64_t len4, float lr,
+                                                      float b1, float b2, float eps, float wd,
+                                                      float inv_c1, float inv_c2) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len4; i += stride) {
+    const uint2 gu = reinterpret_cast<const uint2*>(grad + begin)[i];
+    const float2 g01 = bf2_to_f2(gu.x), g23 = bf2_to_f2(gu.y);
+    const float g[4] = {g01.x, g01.y, g23.x, g23.y};
+    float4 mm = reinterpret_cast<float4*>(m1)[i];
+    float4 vv = reinterpret_cast<float4*>(m2)[i];
+    float4 pp = reinterpret_cast<float4*>(master)[i];
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+    float* pq = &pp.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mp[q] = b1 * mp[q] + (1.f - b1) * g[q];
+      vp[q] = b2 * vp[q] + (1.f - b2) * g[q] * g[q];
+      pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+    }
+    reinterpret_cast<float4*>(m1)[i] = mm;
+    reinterpret_cast<float4*>(m2)[i] = vv;
+    reinterpret_cast<float4*>(master)[i] = pp;
+    uint2 po;
+    po.x = f2_to_bf2(pp.x, pp.y);
+    po.y = f2_to_bf2(pp.z, pp.w);
+    reinterpret_cast<uint2*>(param + begin)[i] = po;
+  }
+}
+
+__global__ void expert_hist_kernel(const int* __restrict__ expert, int64_t n, int E,
+                                   int* __restrict__ blk_hist) {
+  __shared__ int s_hist[64];
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t k = int64_t(blockIdx.x) * kRouteBlock + threadIdx.x;
+  if (k < n) atomicAdd(&s_hist[expert[k]], 1);
+  __syncthreads();
+  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
+}
+
+__global__ void keep_kernel(const int* __restrict__ slot, int64_t n, int64_t cap,
+                            uint8_t* __restrict__ keep) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) keep[k] = slot[k] < cap ? 1 : 0;
+}
+
+__global__ void dlogits_kernel(const float* __restrict__ probs, const int* __restrict__ expert,
+                               const float* __restrict__ dchosen, int64_t n, int E,
+                               float* __restrict__ dl) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n * E) return;
+  const int64_t k = i / E;
+  const int j = int(i % E), e = expert[k];
+  dl[i] = dchosen[k] * probs[k * E + e] * ((j == e ? 1.f : 0.f) - probs[i]);
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+template <int EMAX>
+int gate_hc(int h) {
+  int hc = (64 * 1024) / (EMAX * 2);
+  hc = hc / 256 * 256;
+  return hc > h ? ((h + 255) / 256) * 256 : hc;
+}
+
+}  // namespace
+
+// ================================================================== launchers
+cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
+                         float* probs, int* expert, float* prob, int* blk_hist, cudaStream_t s) {
+  if (E < 1 || E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+#define TED_GATE(EM, TP)                                                                     \
+  {                                                                                          \
+    const int HC = gate_hc<EM>(h);                                                           \
+    const size_t sm = 256 * EM * sizeof(float) + size_t(EM) * HC * 2;                        \
+    cudaFuncSetAttribute(gate_fwd_kernel<EM, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         int(sm));                                                           \
+    gate_fwd_kernel<EM, TP><<<grid, 256, sm, s>>>(a, wg, n, h, E, HC, logits, probs, expert,  \
+                                                  prob, blk_hist); count_launch(1);                           \
+  }
+  if (E <= 8) TED_GATE(8, 4)
+  else if (E <= 16) TED_GATE(16, 4)
+  else if (E <= 32) TED_GATE(32, 2)
+  else TED_GATE(64, 1)
+#undef TED_GATE
+  return cudaGetLastError();
+}
+
+cudaError_t gate_route_logits(const float* logits, int64_t n, int E, float* probs, int* expert,
+                              float* prob, int* blk_hist, cudaStream_t s) {
+  if (E < 1 || E > 64) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  route_logits_kernel<<<grid, 256, 0, s>>>(logits, n, E, probs, expert, prob, blk_hist); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t route_scan(const RouteScanArgs& a, cudaStream_t s) {
+  if (a.E > 64 || a.T > 8 || a.T < 1) return cudaErrorInvalidValue;
+  route_scan_kernel<<<1, 256, 0, s>>>(a); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_rows(const bf16* a, int64_t n, int h, int E, int T, int my_chunk,
+                          int64_t cap, const int* expert, const int* blk_prefix,
+                          const int* chunk_prefix, const int* send_base, const int* home_base,
+                          int* slot, int* pos_send, int* pos_home, bf16* xsend, cudaStream_t s) {
+  if (h % 8 != 0 || E > 64) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  dispatch_kernel<<<grid, 256, 0, s>>>(a, n, h, E, T, my_chunk, cap, expert, blk_prefix,
+                                       chunk_prefix, send_base, home_base, slot, pos_send,
+                                       pos_home, xsend); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t zero_pad_rows(bf16* buf, int64_t ld, int h, const int* seg_off, const int* valid,
+                          int G, int max_pad_rows, cudaStream_t s) {
+  if (G < 1) return cudaSuccess;
+  dim3 grid(max(1, min(max_pad_rows, kPad)), G);
+  zero_pad_kernel<<<grid, 128, 0, s>>>(buf, ld, h, seg_off, valid, G); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_forward(const bf16* fhome, const int* pos_home, const float* prob,
+                            int64_t n, int h, bf16* y, float* loss_part, cudaStream_t s) {
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  combine_fwd_kernel<<<grid, 256, 0, s>>>(fhome, pos_home, prob, n, h, y, loss_part); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t loss_finalize(const float* loss_part, int nblk, double inv_2n, double* loss,
+                          cudaStream_t s) {
+  loss_finalize_kernel<<<1, 256, 0, s>>>(loss_part, nblk, inv_2n, loss); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_backward(const bf16* fhome, const int* pos_home, const int* pos_send,
+                             const float* prob, const float* probs, const int* expert,
+                             int64_t n, int h, int E, const bf16* dy, const bf16* y,
+                             float dy_scale, bf16* dfe, float* dlogits, cudaStream_t s) {
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  combine_bwd_kernel<<<grid, 256, 0, s>>>(fhome, pos_home, pos_send, prob, probs, expert, n, h,
+                                          E, dy, y, dy_scale, dfe, dlogits); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const float* dlogits,
+                                const bf16* wg, int64_t n, int h, int E, bf16* da,
+                                cudaStream_t s) {
+  if (E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+#define TED_GBX(EM)                                                                           \
+  {                                                                                           \
+    const int HC = gate_hc<EM>(h);                                                            \
+    const size_t sm = size_t(EM) * HC * 2;                                                    \
+    cudaFuncSetAttribute(gate_bwd_dx_kernel<EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         int(sm));                                                            \
+    gate_bwd_dx_kernel<EM><<<grid, 256, sm, s>>>(dx_home, pos_home, dlogits, wg, n, h, E, HC,  \
+                                                 da); count_launch(1);                                         \
+  }
+  if (E <= 8) TED_GBX(8)
+  else if (E <= 16) TED_GBX(16)
+  else if (E <= 32) TED_GBX(32)
+  else TED_GBX(64)
+#undef TED_GBX
+  return cudaGetLastError();
+}
+
+size_t gate_dw_part_floats(int64_t n, int h, int E) {
+  return size_t(ceil_div(n, kDwTok)) * size_t(h) * size_t(E);
+}
+
+cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n, int h, int E,
+                                 float* part, bf16* dwg, cudaStream_t s) {
+  if (E > 64) return cudaErrorInvalidValue;
+  const int nb = ceil_div(n, kDwTok);
+  if (nb == 0) {
+    return cudaMemsetAsync(dwg, 0, sizeof(bf16) * size_t(h) * E, s);
+  }
+  dim3 grid(nb, ceil_div(h, 256));
+  if (E <= 8) gate_bwd_dw_kernel<8><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
+  else if (E <= 16) gate_bwd_dw_kernel<16><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
+  else if (E <= 32) gate_bwd_dw_kernel<32><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
+  else gate_bwd_dw_kernel<64><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
+  count_launch(1);
+  gate_dw_reduce_kernel<<<ceil_div(int64_t(h) * E, 256), 256, 0, s>>>(part, nb, h, E, dwg); count_launch(1);
+  return cudaGetLastError();
+}
+
+size_t colsum_part_floats(int w, int G, int max_rows_per_group) {
+  return size_t(ceil_div(max_rows_per_group, kColRows)) * size_t(G) * size_t(w);
+}
+
+cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, int G,
+                          int max_rows_per_group, float* part, bf16* out, int64_t out_stride,
+                          cudaStream_t s) {
+  if (w % 2 != 0 || G < 1) return cudaErrorInvalidValue;
+  const int rsplits = max(1, ceil_div(max_rows_per_group, kColRows));
+  dim3 grid(ceil_div(w / 2, 128), G * rsplits);
+  colsum_part_kernel<<<grid, 128, 0, s>>>(D, ld, w, seg_off, G, rsplits, part); count_launch(1);
+  colsum_reduce_kernel<<<ceil_div(int64_t(G) * w, 256), 256, 0, s>>>(part, w, G, rsplits, out,
+                                                                    out_stride); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s) {
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  expert_hist_kernel<<<grid, kRouteBlock, 0, s>>>(expert, n, E, blk_hist); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,
+                           cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  keep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(slot, n, cap, keep); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const float* dchosen,
+                                 int64_t n, int E, float* dlogits, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  dlogits_kernel<<<ceil_div(n * E, 256), 256, 0, s>>>(probs, expert, dchosen, n, E, dlogits); count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
+                      int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
+                      float eps, float wd, float inv_c1, float inv_c2, cudaStream_t s) {
+  (void)tile;  // the tile only bounds the reference's up-cast buffer; none exists here
+  const int64_t len = end - begin;
+  if (len <= 0) return cudaSuccess;
+  const int grid = sm_count() * 8;
+  const bool v4 = (len % 4 == 0) && (begin % 4 == 0) &&
+                  (reinterpret_cast<uintptr_t>(master) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(m1) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(m2) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(param) % 8 == 0) &&
+                  (reinterpret_cast<uintptr_t>(grad) % 8 == 0);
+  if (v4)
+    adam_kernel_v4<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len / 4, lr, b1, b2,
+                                        eps, wd, inv_c1, inv_c2);
+  else
+    adam_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len, lr, b1, b2, eps,
+                                     wd, inv_c1, inv_c2);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace ted

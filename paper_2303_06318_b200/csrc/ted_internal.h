@@ -1,0 +1,129 @@
+// ted_internal.h -- internal (C++) declarations shared by the TED kernels and the host
+// driver.  Not part of the C ABI (that is include/ted.h).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace ted {
+
+using bf16 = __nv_bfloat16;
+
+void set_error(const std::string& m);
+unsigned long long launches();
+void count_launch(int k);
+const char* last_error();
+
+// ------------------------------------------------------------------ grouped GEMM
+enum GemmMode { GEMM_ROWS = 0, GEMM_KDIM = 1 };
+enum EpiKind { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2, EPI_DGELU = 3 };
+
+struct GemmParams {
+  int mode;  // GemmMode
+  int epi;   // EpiKind
+  int groups;
+  int M, N, K;          // ROWS: N, K fixed (M per group); KDIM: M, N fixed (K per group)
+  const int* seg_off;   // device [groups+1]: padded (x128) row offsets of each group
+  bf16* C;
+  int64_t ldc;
+  int64_t c_group_stride;  // KDIM: C_g = C + g * c_group_stride
+  const bf16* bias;        // EPI_BIAS*: bias_g = bias + g * bias_group_stride (nullable)
+  int64_t bias_group_stride;
+  bf16* aux;  // EPI_BIAS_GELU: H output; EPI_DGELU: Z input (may alias C)
+  int64_t ld_aux;
+};
+
+struct GemmOperands {
+  const bf16* A;
+  int64_t lda;
+  bool a_mn;
+  const bf16* B;
+  int64_t ldb;
+  int64_t b_group_stride;
+  bool b_mn;
+};
+
+int sm_count();
+// max_rows = number of rows the A/B row dimension spans (for the TMA bounds).
+cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_rows,
+                         cudaStream_t s, const char** why);
+
+// ------------------------------------------------------------------ routing kernels
+constexpr int kRouteBlock = 256;  // tokens per routing block (gate / scan / dispatch)
+constexpr int kPad = 128;         // expert segments are padded to the GEMM M tile
+
+// top-1 gate: logits = a Wg (fp32 accumulate), argmax (lowest index on ties), softmax.
+cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
+                         float* probs, int* expert, float* prob, int* blk_hist, cudaStream_t s);
+// Routing from caller-provided fp32 logits (same selection/softmax code path).
+cudaError_t gate_route_logits(const float* logits, int64_t n, int E, float* probs, int* expert,
+                              float* prob, int* blk_hist, cudaStream_t s);
+
+struct RouteScanArgs {
+  int64_t n;
+  int E;
+  int T;           // token chunks (DTD: tensor-parallel degree; else 1)
+  int my_chunk;    // chunk this rank dispatches (DTD), -1 = all chunks (no DTD)
+  int64_t cap;     // capacity C per expert per source shard (>= n: unlimited)
+  int local;       // 1: single-rank layout (send == home == padded expert segments)
+  const int* expert;
+  const int* blk_hist;  // [nblk][E]
+  int* blk_prefix;      // [nblk][E] out
+  int* chunk_prefix;    // [(T+1)][E] out: S[c][e]
+  int* kc;              // [T][E] out: kept tokens per (chunk, expert)
+  int* send_base;       // [E] out
+  int* home_base;       // [T][E] out
+  int* seg_off;         // [E+1] out (local only): padded segment offsets
+};
+cudaError_t route_scan(const RouteScanArgs& a, cudaStream_t s);
+
+// slot/keep -> send/home positions; copies kept rows of `a` into `xsend`.
+cudaError_t dispatch_rows(const bf16* a, int64_t n, int h, int E, int T, int my_chunk,
+                          int64_t cap, const int* expert, const int* blk_prefix,
+                          const int* chunk_prefix, const int* send_base, const int* home_base,
+                          int* slot, int* pos_send, int* pos_home, bf16* xsend, cudaStream_t s);
+// zero rows [seg_off[g] + valid[g], seg_off[g+1]) of buf (valid == nullptr: use counts in
+// valid_from_kc = kc row sums).
+cudaError_t zero_pad_rows(bf16* buf, int64_t ld, int h, const int* seg_off, const int* valid,
+                          int G, int max_pad_rows, cudaStream_t s);
+
+// y[k] = prob[k] * fhome[pos_home[k]] (0 when dropped); per-block sum(y^2) partials.
+cudaError_t combine_forward(const bf16* fhome, const int* pos_home, const float* prob,
+                            int64_t n, int h, bf16* y, float* loss_part, cudaStream_t s);
+cudaError_t loss_finalize(const float* loss_part, int nblk, double inv_2n, double* loss,
+                          cudaStream_t s);
+// dfe[pos_send[k]] = prob[k] * dy[k];  dchosen[k] = <fhome[pos_home[k]], dy[k]>;
+// dlogits[k][j] = dchosen * p_e * (delta_je - p_j).  dy == nullptr: dy = y * dy_scale.
+cudaError_t combine_backward(const bf16* fhome, const int* pos_home, const int* pos_send,
+                             const float* prob, const float* probs, const int* expert,
+                             int64_t n, int h, int E, const bf16* dy, const bf16* y,
+                             float dy_scale, bf16* dfe, float* dlogits, cudaStream_t s);
+// da[k] = dx_home[pos_home[k]] + sum_j dlogits[k][j] Wg[:, j]
+cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const float* dlogits,
+                                const bf16* wg, int64_t n, int h, int E, bf16* da,
+                                cudaStream_t s);
+// dWg = a^T dlogits (deterministic two-stage reduction), written as bf16 (+ fp32 copy).
+cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n, int h, int E,
+                                 float* part, bf16* dwg, cudaStream_t s);
+size_t gate_dw_part_floats(int64_t n, int h, int E);
+// db_g[j] = sum over rows of group g of D[row][j]  (D [rows][w] bf16)
+cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, int G,
+                          int max_rows_per_group, float* part, bf16* out, int64_t out_stride,
+                          cudaStream_t s);
+size_t colsum_part_floats(int w, int G, int max_rows_per_group);
+
+// per-block expert histogram from an expert-id array (ted_route without the gate)
+cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s);
+cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,
+                           cudaStream_t s);
+cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const float* dchosen,
+                                 int64_t n, int E, float* dlogits, cudaStream_t s);
+
+// AdamW (optimizer.cpp:58-104) over [begin, end) of a flat family.
+cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
+                      int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
+                      float eps, float wd, float inv_c1, float inv_c2, cudaStream_t s);
+
+}  // namespace ted

@@ -1,0 +1,130 @@
+"""Single-GPU MoE layer (ted_layer_*) against the fp64 oracle on identical bf16 inputs.
+
+Mirrors the reference's own tests: SerialEquivalence (test_moe.cpp:288-330, here the
+oracle is the serial model), Gate KAT, dispatch/placement bookkeeping, and the
+synthetic objective loss = sum(y^2)/(2N) with dy = y/N (moe.cpp:379-391).
+Tolerances (stated here, the reference is fp64-only): routing bit-exact given the GPU's
+fp32 logits; outputs / gradients rel-L2 <= 2e-2 (bf16 storage of X, Z, H, Fe, dFe, dZ
+and of every gradient, fp32 accumulation)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from tests._util import rel_l2, to_dev_bf16, from_dev  # noqa: E402
+
+TOL = 2e-2
+
+
+def _make(n, h, E, cf, seed):
+    import paper_2303_06318_b200 as ted
+    f = 4 * h
+    model = ted.MoeModelConfig(layers=1, hidden=h, experts=E, tokens_per_shard=n, seed=seed)
+    L = ted.MoeLayer(model, ted.TedConfig(), capacity_factor=cf)
+    inp = O.make_layer_inputs(1, n, h, f, E, seed, bf16=True)
+    L.set_param("layer0.gate.w", inp["wg"])
+    for e in range(E):
+        for k in ("w1", "b1", "w2", "b2"):
+            L.set_param(f"layer0.expert{e}.{k}", inp[k][e])
+    return L, inp
+
+
+@pytest.mark.parametrize("n,h,E,cf,seed", [(1024, 256, 4, 0.0, 1), (1024, 256, 4, 1.25, 1),
+                                           (1024, 256, 4, 1.25, 11), (2048, 512, 8, 1.0, 7),
+                                           (640, 256, 16, 2.0, 3)])
+def test_layer_forward_backward_matches_oracle(n, h, E, cf, seed):
+    L, inp = _make(n, h, E, cf, seed)
+    f = 4 * h
+    a = to_dev_bf16(inp["a"])
+    y = torch.empty_like(a)
+    da = torch.empty_like(a)
+    L.forward(a, y)
+    L.backward(None, da)
+    torch.cuda.synchronize()
+    r = L.routing()
+    o = O.moe_layer(1, n, h, f, E, cf, **inp)
+    # routing: bit-exact given the GPU's fp32 logits, and equal to the fp64 routing
+    oe, oc, op = O.gate_route_logits(r["logits"].astype(np.float64))
+    np.testing.assert_array_equal(r["expert"], oe)
+    np.testing.assert_array_equal(r["expert"], o["expert"])
+    slot, keep, _ = O.route_capacity(r["expert"], E, O.capacity(cf, n, E))
+    np.testing.assert_array_equal(r["slot"], slot)
+    np.testing.assert_array_equal(r["pos_home"] >= 0, keep.astype(bool))
+    st = L.stats()
+    assert st["dropped"] == int((keep == 0).sum())
+    # forward
+    assert rel_l2(from_dev(y), o["y"]) < TOL
+    assert abs(L.loss() - o["loss"]) <= TOL * abs(o["loss"])
+    # backward
+    assert rel_l2(from_dev(da), o["da"]) < TOL
+    assert rel_l2(L.get_grad("layer0.gate.w").reshape(h, E), o["dwg"]) < TOL
+    for e in range(E):
+        if o["dw1"][e].any():
+            assert rel_l2(L.get_grad(f"layer0.expert{e}.w1").reshape(h, f), o["dw1"][e]) < TOL
+            assert rel_l2(L.get_grad(f"layer0.expert{e}.b1"), o["db1"][e]) < TOL
+            assert rel_l2(L.get_grad(f"layer0.expert{e}.w2").reshape(f, h), o["dw2"][e]) < TOL
+            assert rel_l2(L.get_grad(f"layer0.expert{e}.b2"), o["db2"][e]) < TOL
+        else:  # expert received no tokens: zero gradient
+            assert not L.get_grad(f"layer0.expert{e}.w1").any()
+    L.close()
+
+
+def test_layer_step_decreases_loss_and_updates_params():
+    import paper_2303_06318_b200 as ted
+    n, h, E = 1024, 256, 4
+    L, inp = _make(n, h, E, 1.25, 1)
+    a = to_dev_bf16(inp["a"])
+    y = torch.empty_like(a)
+    da = torch.empty_like(a)
+    w_before = L.get_param("layer0.expert0.w1").copy()
+    losses = []
+    for _ in range(5):
+        L.step(a, y, da)
+        losses.append(L.loss())
+    assert not np.array_equal(w_before, L.get_param("layer0.expert0.w1"))
+    assert losses[-1] < losses[0]  # loss = sum(y^2)/2N shrinks under AdamW
+    L.close()
+
+
+def test_full_size_c2_sampled_tokens():
+    """C2 (d=1024, ffn=4096, E=8, 16K tokens): full-size run, oracle on sampled tokens."""
+    import paper_2303_06318_b200 as ted
+    n, h, E = 16384, 1024, 8
+    f = 4 * h
+    model = ted.MoeModelConfig(1, h, E, n, 0)
+    L = ted.MoeLayer(model, ted.TedConfig(), capacity_factor=1.25)
+    L.init_params(1234)
+    rng = np.random.default_rng(0)
+    a_np = O.bf16_round(rng.standard_normal((n, h)))
+    a = to_dev_bf16(a_np)
+    y = torch.empty_like(a)
+    da = torch.empty_like(a)
+    L.forward(a, y)
+    L.backward(None, da)
+    torch.cuda.synchronize()
+    r = L.routing()
+    st = L.stats()
+    slot, keep, _ = O.route_capacity(r["expert"], E, O.capacity(1.25, n, E))
+    np.testing.assert_array_equal(r["slot"], slot)
+    assert st["dropped"] == int((keep == 0).sum())
+    wg = L.get_param("layer0.gate.w").reshape(h, E).astype(np.float64)
+    W = {e: (L.get_param(f"layer0.expert{e}.w1").reshape(h, f).astype(np.float64),
+             L.get_param(f"layer0.expert{e}.b1").astype(np.float64),
+             L.get_param(f"layer0.expert{e}.w2").reshape(f, h).astype(np.float64),
+             L.get_param(f"layer0.expert{e}.b2").astype(np.float64)) for e in range(E)}
+    yd = from_dev(y)
+    idx = rng.choice(n, 96, replace=False)
+    for k in idx:
+        e = int(r["expert"][k])
+        if not keep[k]:
+            assert not yd[k].any()
+            continue
+        w1, b1, w2, b2 = W[e]
+        z = a_np[k] @ w1 + b1
+        hh = np.array([O.lib().o_gelu(v) for v in z])
+        ref = float(r["prob"][k]) * (hh @ w2 + b2)
+        assert rel_l2(yd[k], ref) < TOL
+    assert np.isfinite(from_dev(da)).all()
+    L.close()
