@@ -15,7 +15,8 @@
 // (dZ = acc * gelu'(Z)).
 //
 // Tile 128 x 256 x 64; warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
-// allocator, warps 4..7 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31).
+// allocator, warps 4..11 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31, one half of
+// the tile's 256 columns each).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -34,7 +35,8 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int MAX_GROUPS = 256;
-constexpr int NUM_THREADS = 256;
+constexpr int NUM_THREADS = 384;  // 4 control warps + 8 epilogue warps
+constexpr int EPI_WARPS = 8;
 constexpr uint32_t TMEM_COLS = 512;  // 2 accumulator buffers x 256 fp32 columns
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256 /*bars*/ +
                               2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -129,7 +131,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], EPI_WARPS);
     }
     ptx::fence_barrier_init();
   }
@@ -227,8 +229,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int ew = warp - 4;  // TMEM sub-partition
-    const int r = ew * 32 + lane;
+    const int ew = warp - 4;
+    const int sp = ew & 3;          // TMEM sub-partition: lanes 32*(warp%4)..+31
+    const int chalf = ew >> 2;      // column half of the 256-wide tile
+    const int r = sp * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     TileInfo ti;
@@ -245,9 +249,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         cbase = p.C + int64_t(ti.g) * p.c_group_stride + row * p.ldc;
       }
       const bool zero = ti.k_len == 0;
-      const uint32_t tbase = tmem_base + acc * BN + (uint32_t(ew * 32) << 16);
+      const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32) {
         float v[32];
         ptx::tmem_ld32(tbase + c0, v);
         if (zero) {

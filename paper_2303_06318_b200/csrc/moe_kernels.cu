@@ -6,16 +6,18 @@
 //   gate backward (dlogits, dWg = a^T dl, da += dl Wg^T)            moe.cpp:188-208, :685
 //   per-expert bias-gradient column sums                            nn.cpp:70-76
 //   tiled AdamW                                                     optimizer.cpp:58-104
-// All row copies are 16-byte vectorised and coalesced (a warp moves a 512 B slice of a
-// token row per instruction); reductions are deterministic (fixed order, no float atomics).
+// Design: 64-token routing blocks (16K tokens -> 256 CTAs, > 148 SMs), one warp per 8
+// tokens, every row access a 16-byte vector with several loads in flight per lane
+// (two token rows interleaved), all reductions deterministic (fixed order, no float
+// atomics).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
-#include "ted_internal.h"
-
 #include <atomic>
+
+#include "ted_internal.h"
 
 namespace ted {
 
@@ -26,6 +28,8 @@ void count_launch(int k) { g_launches += k; }
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int kThreads = 256;              // 8 warps
+constexpr int kWarpTok = kRouteBlock / 8;  // tokens per warp (8)
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
@@ -51,6 +55,14 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   u.z = f2_to_bf2(f[4], f[5]);
   u.w = f2_to_bf2(f[6], f[7]);
   return u;
+}
+// streaming 16-byte load that does not allocate in L1
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
 }
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -84,8 +96,8 @@ __device__ __forceinline__ bool cand_better(float va, int ia, float vb, int ib) 
   return (vb > va) || (vb == va && ib < ia);
 }
 
-// Final per-token selection + softmax given the token's E logits spread over the warp
-// (lane l holds j = l and j = l + 32).  Writes outputs; returns best (all lanes).
+// Per-token selection + softmax; the token's E logits are spread over the warp (lane l
+// holds j = l and j = l + 32).  Writes outputs; returns best (all lanes).
 __device__ __forceinline__ int select_softmax(float l0v, float l1v, int E, int lane, int64_t k,
                                               float* logits, float* probs, int* expert,
                                               float* prob) {
@@ -124,35 +136,43 @@ __device__ __forceinline__ int select_softmax(float l0v, float l1v, int E, int l
   return bi;
 }
 
+// Stage Wg[c0:c0+hc, :] transposed into smem as [EMAX][HC] bf16 (zero for j >= E).
+template <int EMAX>
+__device__ __forceinline__ void stage_wg(const bf16* __restrict__ wg, int E, int c0, int hc,
+                                         int HC, bf16* s_wg) {
+  for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
+    const int j = idx / hc, i = idx % hc;
+    s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
+  }
+}
+
+// TPW tokens of a warp are processed together so each Wg slice read from smem feeds
+// TPW * 8 FMAs; TPW * EMAX == 64 accumulators for every EMAX.
 template <int EMAX, int TPW>
-__global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ a,
-                                                       const bf16* __restrict__ wg, int64_t n,
-                                                       int h, int E, int HC,
-                                                       float* __restrict__ logits,
-                                                       float* __restrict__ probs,
-                                                       int* __restrict__ expert,
-                                                       float* __restrict__ prob,
-                                                       int* __restrict__ blk_hist) {
+__global__ void __launch_bounds__(kThreads) gate_fwd_kernel(const bf16* __restrict__ a,
+                                                            const bf16* __restrict__ wg,
+                                                            int64_t n, int h, int E, int HC,
+                                                            float* __restrict__ logits,
+                                                            float* __restrict__ probs,
+                                                            int* __restrict__ expert,
+                                                            float* __restrict__ prob,
+                                                            int* __restrict__ blk_hist) {
   extern __shared__ __align__(16) uint8_t smem[];
-  float* s_part = reinterpret_cast<float*>(smem);                        // [256][EMAX]
-  bf16* s_wg = reinterpret_cast<bf16*>(smem + 256 * EMAX * sizeof(float));  // [EMAX][HC]
+  float* s_part = reinterpret_cast<float*>(smem);  // [kRouteBlock][EMAX]
+  bf16* s_wg = reinterpret_cast<bf16*>(smem + kRouteBlock * EMAX * sizeof(float));
   __shared__ int s_hist[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
-  for (int i = threadIdx.x; i < 256 * EMAX; i += blockDim.x) s_part[i] = 0.f;
+  for (int i = threadIdx.x; i < kRouteBlock * EMAX; i += blockDim.x) s_part[i] = 0.f;
   if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
 
   for (int c0 = 0; c0 < h; c0 += HC) {
     const int hc = min(HC, h - c0);
     __syncthreads();
-    // stage Wg[c0:c0+hc, :] transposed as [EMAX][hc] (zero for j >= E)
-    for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
-      const int j = idx / hc, i = idx % hc;
-      s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
-    }
+    stage_wg<EMAX>(wg, E, c0, hc, HC, s_wg);
     __syncthreads();
 #pragma unroll 1
-    for (int tg = 0; tg < 32; tg += TPW) {
+    for (int tg = 0; tg < kWarpTok; tg += TPW) {
       float acc[TPW * EMAX];
 #pragma unroll
       for (int i = 0; i < TPW * EMAX; ++i) acc[i] = 0.f;
@@ -161,10 +181,9 @@ __global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ 
         float av[TPW][8];
 #pragma unroll
         for (int t = 0; t < TPW; ++t) {
-          const int64_t k = tok0 + warp * 32 + tg + t;
+          const int64_t k = tok0 + warp * kWarpTok + tg + t;
           if (k < n) {
-            const uint4 u = *reinterpret_cast<const uint4*>(a + k * h + c0 + i0);
-            unpack8(u, av[t]);
+            unpack8(ldg_stream(a + k * h + c0 + i0), av[t]);
           } else {
 #pragma unroll
             for (int q = 0; q < 8; ++q) av[t][q] = 0.f;
@@ -180,7 +199,6 @@ __global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ 
             for (int q = 0; q < 8; ++q) acc[t * EMAX + j] = fmaf(av[t][q], wv[q], acc[t * EMAX + j]);
         }
       }
-      // reduce-scatter over the warp, 32 values at a time; lane l gets value index l
 #pragma unroll
       for (int half = 0; half < (TPW * EMAX) / 32; ++half) {
         float v[32];
@@ -188,16 +206,15 @@ __global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ 
         for (int i = 0; i < 32; ++i) v[i] = acc[half * 32 + i];
         const float tot = reduce_scatter32(v, lane);
         const int vi = half * 32 + lane;
-        s_part[(warp * 32 + tg + vi / EMAX) * EMAX + (vi % EMAX)] += tot;
+        s_part[(warp * kWarpTok + tg + vi / EMAX) * EMAX + (vi % EMAX)] += tot;
       }
     }
   }
   __syncwarp();
-  // selection + softmax, one token at a time per warp
-  for (int t = 0; t < 32; ++t) {
-    const int64_t k = tok0 + warp * 32 + t;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + warp * kWarpTok + t;
     if (k >= n) break;
-    const float* lp = s_part + (warp * 32 + t) * EMAX;
+    const float* lp = s_part + (warp * kWarpTok + t) * EMAX;
     const float l0v = lane < EMAX ? lp[lane] : 0.f;
     const float l1v = lane + 32 < EMAX ? lp[lane + 32] : 0.f;
     const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
@@ -207,19 +224,19 @@ __global__ void __launch_bounds__(256) gate_fwd_kernel(const bf16* __restrict__ 
   if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(256) route_logits_kernel(const float* __restrict__ L,
-                                                           int64_t n, int E,
-                                                           float* __restrict__ probs,
-                                                           int* __restrict__ expert,
-                                                           float* __restrict__ prob,
-                                                           int* __restrict__ blk_hist) {
+__global__ void __launch_bounds__(kThreads) route_logits_kernel(const float* __restrict__ L,
+                                                                int64_t n, int E,
+                                                                float* __restrict__ probs,
+                                                                int* __restrict__ expert,
+                                                                float* __restrict__ prob,
+                                                                int* __restrict__ blk_hist) {
   __shared__ int s_hist[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
   __syncthreads();
   const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
-  for (int t = 0; t < 32; ++t) {
-    const int64_t k = tok0 + warp * 32 + t;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + warp * kWarpTok + t;
     if (k >= n) break;
     const float l0v = lane < E ? L[k * E + lane] : 0.f;
     const float l1v = lane + 32 < E ? L[k * E + lane + 32] : 0.f;
@@ -231,67 +248,86 @@ __global__ void __launch_bounds__(256) route_logits_kernel(const float* __restri
 }
 
 // ------------------------------------------------------------------ route scan (1 CTA)
-__global__ void route_scan_kernel(RouteScanArgs A) {
+// Thread (e, p) owns a contiguous range of blocks for expert e: range sums, an exclusive
+// scan over the ranges, then the per-block exclusive prefixes.
+__global__ void __launch_bounds__(kThreads) route_scan_kernel(RouteScanArgs A) {
   const int E = A.E, T = A.T;
   const int64_t n = A.n;
   const int nblk = int((n + kRouteBlock - 1) / kRouteBlock);
+  __shared__ int s_rng[kThreads];
   __shared__ int s_S[9 * 64];   // [(T+1)][E]
   __shared__ int s_kc[8 * 64];  // [T][E]
-  // 1. exclusive prefix over blocks, per expert
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  const int parts = kThreads / E;  // >= 4 (E <= 64)
+  const int chunk = (nblk + parts - 1) / parts;
+  const int tid = threadIdx.x;
+  const int e = tid % E, p = tid / E;
+  const bool active = p < parts;
+  const int b0 = p * chunk, b1 = min(nblk, b0 + chunk);
+  int sum = 0;
+  if (active)
+    for (int b = b0; b < b1; ++b) sum += A.blk_hist[int64_t(b) * E + e];
+  s_rng[tid] = sum;
+  __syncthreads();
+  if (tid < E) {  // exclusive scan over parts for expert tid
     int acc = 0;
-    for (int b = 0; b < nblk; ++b) {
+    for (int q = 0; q < parts; ++q) {
+      const int v = s_rng[q * E + tid];
+      s_rng[q * E + tid] = acc;
+      acc += v;
+    }
+    s_S[T * E + tid] = acc;  // boundary c = T: all tokens
+  }
+  __syncthreads();
+  if (active) {
+    int acc = s_rng[tid];
+    for (int b = b0; b < b1; ++b) {
       A.blk_prefix[int64_t(b) * E + e] = acc;
       acc += A.blk_hist[int64_t(b) * E + e];
     }
-    s_S[T * E + e] = acc;  // chunk boundary c = T is the end
   }
   __syncthreads();
-  // 2. per-expert token count before each chunk boundary c*n/T (c < T)
-  for (int idx = threadIdx.x; idx < T * E; idx += blockDim.x) {
-    const int c = idx / E, e = idx % E;
+  // per-expert token count before each chunk boundary c * n/T (c < T)
+  for (int idx = tid; idx < T * E; idx += blockDim.x) {
+    const int c = idx / E, ee = idx % E;
     const int64_t B = (n / T) * c;
     const int64_t bb = B / kRouteBlock;
-    int acc = 0;
+    int acc;
     if (bb < nblk) {
-      acc = A.blk_prefix[bb * E + e];
-      for (int64_t k = bb * kRouteBlock; k < B; ++k) acc += (A.expert[k] == e);
+      acc = A.blk_prefix[bb * E + ee];
+      for (int64_t k = bb * kRouteBlock; k < B; ++k) acc += (A.expert[k] == ee);
     } else {
-      acc = s_S[T * E + e];
+      acc = s_S[T * E + ee];
     }
-    s_S[c * E + e] = acc;
+    s_S[c * E + ee] = acc;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < (T + 1) * E; idx += blockDim.x)
-    A.chunk_prefix[idx] = s_S[idx];
-  // 3. kept per (chunk, expert): min(C, S[c+1]) - min(C, S[c])
-  for (int idx = threadIdx.x; idx < T * E; idx += blockDim.x) {
-    const int c = idx / E, e = idx % E;
-    const int64_t hi = lmin(A.cap, s_S[(c + 1) * E + e]);
-    const int64_t lo = lmin(A.cap, s_S[c * E + e]);
+  for (int idx = tid; idx < (T + 1) * E; idx += blockDim.x) A.chunk_prefix[idx] = s_S[idx];
+  for (int idx = tid; idx < T * E; idx += blockDim.x) {
+    const int c = idx / E, ee = idx % E;
+    const int64_t hi = lmin(A.cap, s_S[(c + 1) * E + ee]);
+    const int64_t lo = lmin(A.cap, s_S[c * E + ee]);
     s_kc[idx] = int(hi - lo);
     A.kc[idx] = int(hi - lo);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     if (A.local) {
-      // single rank: send == home == padded expert segments
       int off = 0;
-      for (int e = 0; e < E; ++e) {
-        A.seg_off[e] = off;
-        A.send_base[e] = off;
-        A.home_base[e] = off;
-        off += (s_kc[e] + kPad - 1) / kPad * kPad;
+      for (int ee = 0; ee < E; ++ee) {
+        A.seg_off[ee] = off;
+        A.send_base[ee] = off;
+        A.home_base[ee] = off;
+        off += (s_kc[ee] + kPad - 1) / kPad * kPad;
       }
       A.seg_off[E] = off;
     } else {
       int blockbase = 0;
       for (int c = 0; c < T; ++c) {
         int off = 0;
-        for (int e = 0; e < E; ++e) {
-          A.home_base[c * E + e] = blockbase + off;
-          if (c == (A.my_chunk < 0 ? 0 : A.my_chunk)) A.send_base[e] = off;
-          off += s_kc[c * E + e];
+        for (int ee = 0; ee < E; ++ee) {
+          A.home_base[c * E + ee] = blockbase + off;
+          if (c == (A.my_chunk < 0 ? 0 : A.my_chunk)) A.send_base[ee] = off;
+          off += s_kc[c * E + ee];
         }
         blockbase += off;
       }
@@ -299,64 +335,93 @@ __global__ void route_scan_kernel(RouteScanArgs A) {
   }
 }
 
+// ------------------------------------------------------------------ row movers
+// Copy rows with U 16-byte loads in flight per lane per row, two rows interleaved.
+template <int U>
+__device__ __forceinline__ void copy_rows2(const bf16* s0, bf16* d0, const bf16* s1, bf16* d1,
+                                           int vec, int lane) {
+  for (int base = lane; base < vec; base += 32 * U) {
+    uint4 v0[U], v1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * 32;
+      if (i < vec) {
+        if (s0) v0[u] = ldg_stream(reinterpret_cast<const uint4*>(s0) + i);
+        if (s1) v1[u] = ldg_stream(reinterpret_cast<const uint4*>(s1) + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * 32;
+      if (i < vec) {
+        if (s0) reinterpret_cast<uint4*>(d0)[i] = v0[u];
+        if (s1) reinterpret_cast<uint4*>(d1)[i] = v1[u];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ dispatch
-__global__ void __launch_bounds__(256) dispatch_kernel(
+__global__ void __launch_bounds__(kThreads) dispatch_kernel(
     const bf16* __restrict__ a, int64_t n, int h, int E, int T, int my_chunk, int64_t cap,
     const int* __restrict__ expert, const int* __restrict__ blk_prefix,
     const int* __restrict__ chunk_prefix, const int* __restrict__ send_base,
     const int* __restrict__ home_base, int* __restrict__ slot_out, int* __restrict__ pos_send,
     int* __restrict__ pos_home, bf16* __restrict__ xsend) {
-  __shared__ int s_wcnt[8][64];
-  __shared__ int s_pos[256];
+  __shared__ int s_wcnt[kRouteBlock / 32][64];
+  __shared__ int s_pos[kRouteBlock];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (kRouteBlock / 32) * 64; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
+  __syncthreads();
   const int64_t k = int64_t(blockIdx.x) * kRouteBlock + threadIdx.x;
-  const bool valid = k < n;
+  const bool ranker = threadIdx.x < kRouteBlock;  // warp-uniform (kRouteBlock % 32 == 0)
+  const bool valid = ranker && k < n;
   const int e = valid ? expert[k] : -1;
-  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) (&s_wcnt[0][0])[i] = 0;
-  __syncthreads();
-  const unsigned mask = __match_any_sync(FULL, e);
-  const int rank = __popc(mask & ((1u << lane) - 1u));
-  if (valid && rank == 0) s_wcnt[warp][e] = __popc(mask);
-  __syncthreads();
-  int ps = -1;
-  if (valid) {
-    int pre = 0;
-    for (int w = 0; w < warp; ++w) pre += s_wcnt[w][e];
-    const int64_t slot = int64_t(blk_prefix[int64_t(blockIdx.x) * E + e]) + pre + rank;
-    if (slot_out) slot_out[k] = int(slot);
-    const bool keep = slot < cap;
-    int c = 0;
-    if (T > 1) {
-      c = int(k / (n / T));
-      if (c >= T) c = T - 1;
-    }
-    int ph = -1;
-    if (keep) {
-      const int64_t before = lmin(cap, chunk_prefix[c * E + e]);
-      const int r = int(slot - before);
-      ph = home_base[c * E + e] + r;
-      if (my_chunk < 0 || c == my_chunk) ps = send_base[e] + r;
-    }
-    pos_home[k] = ph;
-    pos_send[k] = ps;
+  int rank = 0;
+  if (ranker) {
+    const unsigned mask = __match_any_sync(FULL, e);
+    rank = __popc(mask & ((1u << lane) - 1u));
+    if (valid && rank == 0) s_wcnt[warp][e] = __popc(mask);
   }
-  s_pos[threadIdx.x] = ps;
   __syncthreads();
-  // copy kept rows: each warp moves 32 tokens, 16 B per lane per step
+  if (ranker) {
+    int ps = -1;
+    if (valid) {
+      int pre = 0;
+      for (int w = 0; w < warp; ++w) pre += s_wcnt[w][e];
+      const int64_t slot = int64_t(blk_prefix[int64_t(blockIdx.x) * E + e]) + pre + rank;
+      if (slot_out) slot_out[k] = int(slot);
+      int c = 0;
+      if (T > 1) {
+        c = int(k / (n / T));
+        if (c >= T) c = T - 1;
+      }
+      int ph = -1;
+      if (slot < cap) {
+        const int64_t before = lmin(cap, chunk_prefix[c * E + e]);
+        const int r = int(slot - before);
+        ph = home_base[c * E + e] + r;
+        if (my_chunk < 0 || c == my_chunk) ps = send_base[e] + r;
+      }
+      pos_home[k] = ph;
+      pos_send[k] = ps;
+    }
+    s_pos[threadIdx.x] = ps;
+  }
+  __syncthreads();
+  if (xsend == nullptr || h == 0) return;
   const int vec = h / 8;
-  for (int t = warp * 32; t < warp * 32 + 32; ++t) {
-    const int p = s_pos[t];
-    if (p < 0) continue;
-    const int64_t kk = int64_t(blockIdx.x) * kRouteBlock + t;
-    const uint4* src = reinterpret_cast<const uint4*>(a + kk * h);
-    uint4* dst = reinterpret_cast<uint4*>(xsend + int64_t(p) * h);
-    for (int i = lane; i < vec; i += 32) dst[i] = src[i];
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
+  for (int t = warp * kWarpTok; t < warp * kWarpTok + kWarpTok; t += 2) {
+    const int p0 = s_pos[t], p1 = s_pos[t + 1];
+    copy_rows2<4>(p0 >= 0 ? a + (tok0 + t) * h : nullptr, xsend + int64_t(p0 < 0 ? 0 : p0) * h,
+                  p1 >= 0 ? a + (tok0 + t + 1) * h : nullptr,
+                  xsend + int64_t(p1 < 0 ? 0 : p1) * h, vec, lane);
   }
 }
 
 __global__ void zero_pad_kernel(bf16* buf, int64_t ld, int h, const int* seg_off,
                                 const int* valid, int G) {
-  // blockIdx.y = group; rows [seg_off[g] + valid[g], seg_off[g+1])
   const int g = blockIdx.y;
   const int64_t r0 = int64_t(seg_off[g]) + valid[g];
   const int64_t r1 = seg_off[g + 1];
@@ -369,36 +434,58 @@ __global__ void zero_pad_kernel(bf16* buf, int64_t ld, int h, const int* seg_off
 }
 
 // ------------------------------------------------------------------ combine
-__global__ void __launch_bounds__(256) combine_fwd_kernel(const bf16* __restrict__ fhome,
-                                                          const int* __restrict__ pos_home,
-                                                          const float* __restrict__ prob,
-                                                          int64_t n, int h,
-                                                          bf16* __restrict__ y,
-                                                          float* __restrict__ loss_part) {
+__global__ void __launch_bounds__(kThreads) combine_fwd_kernel(const bf16* __restrict__ fhome,
+                                                               const int* __restrict__ pos_home,
+                                                               const float* __restrict__ prob,
+                                                               int64_t n, int h,
+                                                               bf16* __restrict__ y,
+                                                               float* __restrict__ loss_part) {
   __shared__ float s_red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int vec = h / 8;
   float sq = 0.f;
-  for (int t = 0; t < 32; ++t) {
-    const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
-    if (k >= n) break;
-    const int p = pos_home[k];
-    const float pk = prob[k];
-    uint4* dst = reinterpret_cast<uint4*>(y + k * h);
-    if (p < 0) {
-      for (int i = lane; i < vec; i += 32) dst[i] = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const uint4* src = reinterpret_cast<const uint4*>(fhome + int64_t(p) * h);
-    for (int i = lane; i < vec; i += 32) {
-      float f[8];
-      unpack8(src[i], f);
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int t = 0; t < kWarpTok; t += 2) {
+    const int64_t k0 = tok0 + t, k1 = tok0 + t + 1;
+    const bool v0 = k0 < n, v1 = k1 < n;
+    const int p0 = v0 ? pos_home[k0] : -1, p1 = v1 ? pos_home[k1] : -1;
+    const float q0 = v0 ? prob[k0] : 0.f, q1 = v1 ? prob[k1] : 0.f;
+    for (int base = lane; base < vec; base += 32 * 4) {
+      uint4 f0[4], f1[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        f[q] *= pk;
-        sq = fmaf(f[q], f[q], sq);
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        f0[u] = make_uint4(0, 0, 0, 0);
+        f1[u] = make_uint4(0, 0, 0, 0);
+        if (i < vec) {
+          if (p0 >= 0) f0[u] = ldg_stream(fhome + int64_t(p0) * h + i * 8);
+          if (p1 >= 0) f1[u] = ldg_stream(fhome + int64_t(p1) * h + i * 8);
+        }
       }
-      dst[i] = pack8(f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        if (i >= vec) continue;
+        float f[8];
+        if (v0) {
+          unpack8(f0[u], f);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            f[q] *= q0;
+            sq = fmaf(f[q], f[q], sq);
+          }
+          reinterpret_cast<uint4*>(y + k0 * h)[i] = pack8(f);
+        }
+        if (v1) {
+          unpack8(f1[u], f);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            f[q] *= q1;
+            sq = fmaf(f[q], f[q], sq);
+          }
+          reinterpret_cast<uint4*>(y + k1 * h)[i] = pack8(f);
+        }
+      }
     }
   }
   sq = warp_sum(sq);
@@ -424,7 +511,8 @@ __global__ void loss_finalize_kernel(const float* part, int nblk, double inv_2n,
   if (threadIdx.x == 0) *loss = s[0] * inv_2n;
 }
 
-__global__ void __launch_bounds__(256) combine_bwd_kernel(
+// dfe[pos_send] = p * dy; dchosen = <f_home, dy>; dlogits = dchosen p_e (delta - p_j)
+__global__ void __launch_bounds__(kThreads) combine_bwd_kernel(
     const bf16* __restrict__ fhome, const int* __restrict__ pos_home,
     const int* __restrict__ pos_send, const float* __restrict__ prob,
     const float* __restrict__ probs, const int* __restrict__ expert, int64_t n, int h, int E,
@@ -432,29 +520,42 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
     bf16* __restrict__ dfe, float* __restrict__ dlogits) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int vec = h / 8;
-  for (int t = 0; t < 32; ++t) {
-    const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
+  const bf16* dsrc_base = dy ? dy : y;
+  const float sc = dy ? 1.f : dy_scale;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + t;
     if (k >= n) break;
     const int ph = pos_home[k], ps = pos_send[k];
     const float pk = prob[k];
-    const bf16* dsrc = dy ? dy + k * h : y + k * h;
-    const float sc = dy ? 1.f : dy_scale;
+    const bf16* dsrc = dsrc_base + k * h;
     float dot = 0.f;
-    for (int i = lane; i < vec; i += 32) {
-      float d[8];
-      unpack8(reinterpret_cast<const uint4*>(dsrc)[i], d);
+    for (int base = lane; base < vec; base += 32 * 4) {
+      uint4 dv[4], fv[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) d[q] *= sc;
-      if (ph >= 0) {
-        float f[8];
-        unpack8(reinterpret_cast<const uint4*>(fhome + int64_t(ph) * h)[i], f);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dot = fmaf(f[q], d[q], dot);
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        dv[u] = make_uint4(0, 0, 0, 0);
+        fv[u] = make_uint4(0, 0, 0, 0);
+        if (i < vec) {
+          dv[u] = ldg_stream(dsrc + i * 8);
+          if (ph >= 0) fv[u] = ldg_stream(fhome + int64_t(ph) * h + i * 8);
+        }
       }
-      if (ps >= 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) d[q] *= pk;
-        reinterpret_cast<uint4*>(dfe + int64_t(ps) * h)[i] = pack8(d);
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        if (i >= vec) continue;
+        float d[8], f[8];
+        unpack8(dv[u], d);
+        unpack8(fv[u], f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d[q] *= sc;
+          dot = fmaf(f[q], d[q], dot);
+          d[q] *= pk;
+        }
+        if (ps >= 0) reinterpret_cast<uint4*>(dfe + int64_t(ps) * h)[i] = pack8(d);
       }
     }
     const float dchosen = warp_sum(dot);
@@ -467,55 +568,61 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(
 
 // ------------------------------------------------------------------ gate backward
 template <int EMAX>
-__global__ void __launch_bounds__(256) gate_bwd_dx_kernel(const bf16* __restrict__ dx_home,
-                                                          const int* __restrict__ pos_home,
-                                                          const float* __restrict__ dl,
-                                                          const bf16* __restrict__ wg, int64_t n,
-                                                          int h, int E, int HC,
-                                                          bf16* __restrict__ da) {
+__global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const bf16* __restrict__ dx_home,
+                                                               const int* __restrict__ pos_home,
+                                                               const float* __restrict__ dl,
+                                                               const bf16* __restrict__ wg,
+                                                               int64_t n, int h, int E, int HC,
+                                                               bf16* __restrict__ da) {
   extern __shared__ __align__(16) uint8_t smem[];
   bf16* s_wg = reinterpret_cast<bf16*>(smem);  // [EMAX][HC]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
   for (int c0 = 0; c0 < h; c0 += HC) {
     const int hc = min(HC, h - c0);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
-      const int j = idx / hc, i = idx % hc;
-      s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
-    }
+    stage_wg<EMAX>(wg, E, c0, hc, HC, s_wg);
     __syncthreads();
-    for (int t = 0; t < 32; ++t) {
-      const int64_t k = int64_t(blockIdx.x) * kRouteBlock + warp * 32 + t;
+    for (int t = 0; t < kWarpTok; ++t) {
+      const int64_t k = tok0 + t;
       if (k >= n) break;
       const float d0 = lane < E ? dl[k * E + lane] : 0.f;
       const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
       const int ph = pos_home ? pos_home[k] : -1;
-      for (int i0 = lane * 8; i0 < hc; i0 += 256) {
-        float acc[8];
-        if (ph >= 0) {
-          unpack8(*reinterpret_cast<const uint4*>(dx_home + int64_t(ph) * h + c0 + i0), acc);
-        } else {
+      const bf16* src = ph >= 0 ? dx_home + int64_t(ph) * h + c0 : nullptr;
+      for (int base = lane * 8; base < hc; base += 256 * 4) {
+        uint4 xv[4];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+        for (int u = 0; u < 4; ++u) {
+          const int i0 = base + u * 256;
+          xv[u] = (src && i0 < hc) ? ldg_stream(src + i0) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int j = 0; j < EMAX; ++j) {
-          const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);
-          float wv[8];
-          unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
+        for (int u = 0; u < 4; ++u) {
+          const int i0 = base + u * 256;
+          if (i0 >= hc) continue;
+          float acc[8];
+          unpack8(xv[u], acc);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[q] = fmaf(dj, wv[q], acc[q]);
+          for (int j = 0; j < EMAX; ++j) {
+            const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);
+            float wv[8];
+            unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = fmaf(dj, wv[q], acc[q]);
+          }
+          *reinterpret_cast<uint4*>(da + k * h + c0 + i0) = pack8(acc);
         }
-        *reinterpret_cast<uint4*>(da + k * h + c0 + i0) = pack8(acc);
       }
     }
   }
 }
 
-constexpr int kDwTok = 128;  // tokens per dWg partial
+constexpr int kDwTok = 64;  // tokens per dWg partial
 
-template <int EMAX>
-__global__ void __launch_bounds__(256) gate_bwd_dw_kernel(const bf16* __restrict__ a,
+// dWg partials: thread owns CPT consecutive columns for all EMAX experts.
+template <int EMAX, int CPT>
+__global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict__ a,
                                                           const float* __restrict__ dl,
                                                           int64_t n, int h, int E,
                                                           float* __restrict__ part) {
@@ -526,18 +633,44 @@ __global__ void __launch_bounds__(256) gate_bwd_dw_kernel(const bf16* __restrict
     s_dl[idx] = (k0 + t < n && j < E) ? dl[(k0 + t) * E + j] : 0.f;
   }
   __syncthreads();
-  const int i = blockIdx.y * blockDim.x + threadIdx.x;
-  if (i >= h) return;
-  float acc[EMAX];
+  const int i0 = (blockIdx.y * blockDim.x + threadIdx.x) * CPT;
+  if (i0 >= h) return;
+  float acc[CPT][EMAX];
 #pragma unroll
-  for (int j = 0; j < EMAX; ++j) acc[j] = 0.f;
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int j = 0; j < EMAX; ++j) acc[c][j] = 0.f;
   const int tn = int(lmin(kDwTok, n - k0));
+#pragma unroll 4
   for (int t = 0; t < tn; ++t) {
-    const float x = __bfloat162float(a[(k0 + t) * h + i]);
+    float x[CPT];
+    const bf16* src = a + (k0 + t) * h + i0;
+    if constexpr (CPT == 8) {
+      float f[8];
+      unpack8(ldg_stream(src), f);
 #pragma unroll
-    for (int j = 0; j < EMAX; ++j) acc[j] = fmaf(x, s_dl[t * EMAX + j], acc[j]);
+      for (int c = 0; c < 8; ++c) x[c] = f[c];
+    } else if constexpr (CPT == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(src);
+      const float2 f0 = bf2_to_f2(u.x), f1 = bf2_to_f2(u.y);
+      x[0] = f0.x; x[1] = f0.y; x[2] = f1.x; x[3] = f1.y;
+    } else if constexpr (CPT == 2) {
+      const float2 f0 = bf2_to_f2(*reinterpret_cast<const uint32_t*>(src));
+      x[0] = f0.x; x[1] = f0.y;
+    } else {
+      x[0] = __bfloat162float(src[0]);
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+#pragma unroll
+      for (int j = 0; j < EMAX; ++j) acc[c][j] = fmaf(x[c], s_dl[t * EMAX + j], acc[c][j]);
   }
-  for (int j = 0; j < E; ++j) part[(int64_t(blockIdx.x) * h + i) * E + j] = acc[j];
+  float* out = part + (int64_t(blockIdx.x) * h + i0) * E;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c)
+#pragma unroll
+    for (int j = 0; j < EMAX; ++j)
+      if (j < E) out[c * E + j] = acc[c][j];
 }
 
 __global__ void gate_dw_reduce_kernel(const float* __restrict__ part, int nb, int h, int E,
@@ -550,34 +683,54 @@ __global__ void gate_dw_reduce_kernel(const float* __restrict__ part, int nb, in
 }
 
 // ------------------------------------------------------------------ bias-grad column sums
-constexpr int kColRows = 128;  // rows per partial
+constexpr int kColRows = 64;  // rows per partial
 
-__global__ void colsum_part_kernel(const bf16* __restrict__ D, int64_t ld, int w,
-                                   const int* __restrict__ seg_off, int G, int rsplits,
-                                   float* __restrict__ part) {
+// thread = 8 columns (one 16 B vector per row), block = 128 threads = 1024 columns
+__global__ void __launch_bounds__(128) colsum_part_kernel(const bf16* __restrict__ D, int64_t ld,
+                                                          int w, const int* __restrict__ seg_off,
+                                                          int G, int rsplits,
+                                                          float* __restrict__ part) {
   const int g = blockIdx.y / rsplits, rs = blockIdx.y % rsplits;
-  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (col >= w) return;
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   const int64_t r0 = int64_t(seg_off[g]) + int64_t(rs) * kColRows;
   const int64_t r1 = lmin(r0 + kColRows, seg_off[g + 1]);
-  float s0 = 0.f, s1 = 0.f;
-  for (int64_t r = r0; r < r1; ++r) {
-    const float2 v = bf2_to_f2(*reinterpret_cast<const uint32_t*>(D + r * ld + col));
-    s0 += v.x;
-    s1 += v.y;
+  if (col >= w || r0 >= r1) return;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ldg_stream(D + (r + u) * ld + col);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      float f[8];
+      unpack8(v[u], f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s[q] += f[q];
+    }
   }
-  float* pp = part + (int64_t(rs) * G + g) * w + col;
-  pp[0] = s0;
-  pp[1] = s1;
+  for (; r < r1; ++r) {
+    float f[8];
+    unpack8(ldg_stream(D + r * ld + col), f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] += f[q];
+  }
+  float4* pp = reinterpret_cast<float4*>(part + (int64_t(rs) * G + g) * w + col);
+  pp[0] = make_float4(s[0], s[1], s[2], s[3]);
+  pp[1] = make_float4(s[4], s[5], s[6], s[7]);
 }
 
-__global__ void colsum_reduce_kernel(const float* __restrict__ part, int w, int G, int rsplits,
-                                     bf16* __restrict__ out, int64_t out_stride) {
+// sums only the splits that exist for each group (seg_off is device-resident)
+__global__ void colsum_reduce_kernel(const float* __restrict__ part, int w, int G,
+                                     const int* __restrict__ seg_off, bf16* __restrict__ out,
+                                     int64_t out_stride) {
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= int64_t(G) * w) return;
   const int g = int(idx / w), c = int(idx % w);
+  const int rows = seg_off[g + 1] - seg_off[g];
+  const int ns = (rows + kColRows - 1) / kColRows;
   float acc = 0.f;
-  for (int rs = 0; rs < rsplits; ++rs) acc += part[(int64_t(rs) * G + g) * w + c];
+  for (int rs = 0; rs < ns; ++rs) acc += part[(int64_t(rs) * G + g) * w + c];
   out[int64_t(g) * out_stride + c] = __float2bfloat16(acc);
 }
 
@@ -646,7 +799,7 @@ __global__ void expert_hist_kernel(const int* __restrict__ expert, int64_t n, in
   if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
   __syncthreads();
   const int64_t k = int64_t(blockIdx.x) * kRouteBlock + threadIdx.x;
-  if (k < n) atomicAdd(&s_hist[expert[k]], 1);
+  if (threadIdx.x < kRouteBlock && k < n) atomicAdd(&s_hist[expert[k]], 1);
   __syncthreads();
   if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
 }
@@ -676,6 +829,15 @@ int gate_hc(int h) {
   return hc > h ? ((h + 255) / 256) * 256 : hc;
 }
 
+template <class K>
+void smem_attr(K k, size_t bytes) {
+  static size_t set = 0;  // per instantiation
+  if (bytes > set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    set = bytes;
+  }
+}
+
 }  // namespace
 
 // ================================================================== launchers
@@ -684,20 +846,20 @@ cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E,
   if (E < 1 || E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-#define TED_GATE(EM, TP)                                                                     \
-  {                                                                                          \
-    const int HC = gate_hc<EM>(h);                                                           \
-    const size_t sm = 256 * EM * sizeof(float) + size_t(EM) * HC * 2;                        \
-    cudaFuncSetAttribute(gate_fwd_kernel<EM, TP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         int(sm));                                                           \
-    gate_fwd_kernel<EM, TP><<<grid, 256, sm, s>>>(a, wg, n, h, E, HC, logits, probs, expert,  \
-                                                  prob, blk_hist); count_launch(1);                           \
+#define TED_GATE(EM, TP)                                                                      \
+  {                                                                                           \
+    const int HC = gate_hc<EM>(h);                                                            \
+    const size_t sm = kRouteBlock * EM * sizeof(float) + size_t(EM) * HC * 2;                 \
+    smem_attr(gate_fwd_kernel<EM, TP>, sm);                                                   \
+    gate_fwd_kernel<EM, TP><<<grid, kThreads, sm, s>>>(a, wg, n, h, E, HC, logits, probs,     \
+                                                       expert, prob, blk_hist);               \
   }
-  if (E <= 8) TED_GATE(8, 4)
+  if (E <= 8) TED_GATE(8, 8)
   else if (E <= 16) TED_GATE(16, 4)
   else if (E <= 32) TED_GATE(32, 2)
   else TED_GATE(64, 1)
 #undef TED_GATE
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -706,13 +868,15 @@ cudaError_t gate_route_logits(const float* logits, int64_t n, int E, float* prob
   if (E < 1 || E > 64) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  route_logits_kernel<<<grid, 256, 0, s>>>(logits, n, E, probs, expert, prob, blk_hist); count_launch(1);
+  route_logits_kernel<<<grid, kThreads, 0, s>>>(logits, n, E, probs, expert, prob, blk_hist);
+  count_launch(1);
   return cudaGetLastError();
 }
 
 cudaError_t route_scan(const RouteScanArgs& a, cudaStream_t s) {
   if (a.E > 64 || a.T > 8 || a.T < 1) return cudaErrorInvalidValue;
-  route_scan_kernel<<<1, 256, 0, s>>>(a); count_launch(1);
+  route_scan_kernel<<<1, kThreads, 0, s>>>(a);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -723,9 +887,10 @@ cudaError_t dispatch_rows(const bf16* a, int64_t n, int h, int E, int T, int my_
   if (h % 8 != 0 || E > 64) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  dispatch_kernel<<<grid, 256, 0, s>>>(a, n, h, E, T, my_chunk, cap, expert, blk_prefix,
-                                       chunk_prefix, send_base, home_base, slot, pos_send,
-                                       pos_home, xsend); count_launch(1);
+  dispatch_kernel<<<grid, kThreads, 0, s>>>(a, n, h, E, T, my_chunk, cap, expert, blk_prefix,
+                                            chunk_prefix, send_base, home_base, slot, pos_send,
+                                            pos_home, xsend);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -733,7 +898,8 @@ cudaError_t zero_pad_rows(bf16* buf, int64_t ld, int h, const int* seg_off, cons
                           int G, int max_pad_rows, cudaStream_t s) {
   if (G < 1) return cudaSuccess;
   dim3 grid(max(1, min(max_pad_rows, kPad)), G);
-  zero_pad_kernel<<<grid, 128, 0, s>>>(buf, ld, h, seg_off, valid, G); count_launch(1);
+  zero_pad_kernel<<<grid, 128, 0, s>>>(buf, ld, h, seg_off, valid, G);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -741,13 +907,15 @@ cudaError_t combine_forward(const bf16* fhome, const int* pos_home, const float*
                             int64_t n, int h, bf16* y, float* loss_part, cudaStream_t s) {
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  combine_fwd_kernel<<<grid, 256, 0, s>>>(fhome, pos_home, prob, n, h, y, loss_part); count_launch(1);
+  combine_fwd_kernel<<<grid, kThreads, 0, s>>>(fhome, pos_home, prob, n, h, y, loss_part);
+  count_launch(1);
   return cudaGetLastError();
 }
 
 cudaError_t loss_finalize(const float* loss_part, int nblk, double inv_2n, double* loss,
                           cudaStream_t s) {
-  loss_finalize_kernel<<<1, 256, 0, s>>>(loss_part, nblk, inv_2n, loss); count_launch(1);
+  loss_finalize_kernel<<<1, 256, 0, s>>>(loss_part, nblk, inv_2n, loss);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -757,8 +925,9 @@ cudaError_t combine_backward(const bf16* fhome, const int* pos_home, const int* 
                              float dy_scale, bf16* dfe, float* dlogits, cudaStream_t s) {
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  combine_bwd_kernel<<<grid, 256, 0, s>>>(fhome, pos_home, pos_send, prob, probs, expert, n, h,
-                                          E, dy, y, dy_scale, dfe, dlogits); count_launch(1);
+  combine_bwd_kernel<<<grid, kThreads, 0, s>>>(fhome, pos_home, pos_send, prob, probs, expert, n,
+                                               h, E, dy, y, dy_scale, dfe, dlogits);
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -768,20 +937,20 @@ cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const 
   if (E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-#define TED_GBX(EM)                                                                           \
-  {                                                                                           \
-    const int HC = gate_hc<EM>(h);                                                            \
-    const size_t sm = size_t(EM) * HC * 2;                                                    \
-    cudaFuncSetAttribute(gate_bwd_dx_kernel<EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                         int(sm));                                                            \
-    gate_bwd_dx_kernel<EM><<<grid, 256, sm, s>>>(dx_home, pos_home, dlogits, wg, n, h, E, HC,  \
-                                                 da); count_launch(1);                                         \
+#define TED_GBX(EM)                                                                            \
+  {                                                                                            \
+    const int HC = gate_hc<EM>(h);                                                             \
+    const size_t sm = size_t(EM) * HC * 2;                                                     \
+    smem_attr(gate_bwd_dx_kernel<EM>, sm);                                                     \
+    gate_bwd_dx_kernel<EM><<<grid, kThreads, sm, s>>>(dx_home, pos_home, dlogits, wg, n, h, E,  \
+                                                      HC, da);                                 \
   }
   if (E <= 8) TED_GBX(8)
   else if (E <= 16) TED_GBX(16)
   else if (E <= 32) TED_GBX(32)
   else TED_GBX(64)
 #undef TED_GBX
+  count_launch(1);
   return cudaGetLastError();
 }
 
@@ -791,18 +960,26 @@ size_t gate_dw_part_floats(int64_t n, int h, int E) {
 
 cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n, int h, int E,
                                  float* part, bf16* dwg, cudaStream_t s) {
-  if (E > 64) return cudaErrorInvalidValue;
+  if (E > 64 || h % 8 != 0) return cudaErrorInvalidValue;
   const int nb = ceil_div(n, kDwTok);
   if (nb == 0) {
     return cudaMemsetAsync(dwg, 0, sizeof(bf16) * size_t(h) * E, s);
   }
-  dim3 grid(nb, ceil_div(h, 256));
-  if (E <= 8) gate_bwd_dw_kernel<8><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
-  else if (E <= 16) gate_bwd_dw_kernel<16><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
-  else if (E <= 32) gate_bwd_dw_kernel<32><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
-  else gate_bwd_dw_kernel<64><<<grid, 256, 0, s>>>(a, dlogits, n, h, E, part);
-  count_launch(1);
-  gate_dw_reduce_kernel<<<ceil_div(int64_t(h) * E, 256), 256, 0, s>>>(part, nb, h, E, dwg); count_launch(1);
+  if (E <= 8) {
+    gate_bwd_dw_kernel<8, 8><<<dim3(nb, ceil_div(h, 128 * 8)), 128, 0, s>>>(a, dlogits, n, h, E,
+                                                                          part);
+  } else if (E <= 16) {
+    gate_bwd_dw_kernel<16, 4><<<dim3(nb, ceil_div(h, 128 * 4)), 128, 0, s>>>(a, dlogits, n, h,
+                                                                           E, part);
+  } else if (E <= 32) {
+    gate_bwd_dw_kernel<32, 2><<<dim3(nb, ceil_div(h, 128 * 2)), 128, 0, s>>>(a, dlogits, n, h,
+                                                                           E, part);
+  } else {
+    gate_bwd_dw_kernel<64, 1><<<dim3(nb, ceil_div(h, 128)), 128, 0, s>>>(a, dlogits, n, h, E,
+                                                                       part);
+  }
+  gate_dw_reduce_kernel<<<ceil_div(int64_t(h) * E, 256), 256, 0, s>>>(part, nb, h, E, dwg);
+  count_launch(2);
   return cudaGetLastError();
 }
 
@@ -813,33 +990,37 @@ size_t colsum_part_floats(int w, int G, int max_rows_per_group) {
 cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, int G,
                           int max_rows_per_group, float* part, bf16* out, int64_t out_stride,
                           cudaStream_t s) {
-  if (w % 2 != 0 || G < 1) return cudaErrorInvalidValue;
+  if (w % 8 != 0 || G < 1) return cudaErrorInvalidValue;
   const int rsplits = max(1, ceil_div(max_rows_per_group, kColRows));
-  dim3 grid(ceil_div(w / 2, 128), G * rsplits);
-  colsum_part_kernel<<<grid, 128, 0, s>>>(D, ld, w, seg_off, G, rsplits, part); count_launch(1);
-  colsum_reduce_kernel<<<ceil_div(int64_t(G) * w, 256), 256, 0, s>>>(part, w, G, rsplits, out,
-                                                                    out_stride); count_launch(1);
+  dim3 grid(ceil_div(w / 8, 128), G * rsplits);
+  colsum_part_kernel<<<grid, 128, 0, s>>>(D, ld, w, seg_off, G, rsplits, part);
+  colsum_reduce_kernel<<<ceil_div(int64_t(G) * w, 256), 256, 0, s>>>(part, w, G, seg_off, out,
+                                                                    out_stride);
+  count_launch(2);
   return cudaGetLastError();
 }
 
 cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s) {
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  expert_hist_kernel<<<grid, kRouteBlock, 0, s>>>(expert, n, E, blk_hist); count_launch(1);
+  expert_hist_kernel<<<grid, kRouteBlock, 0, s>>>(expert, n, E, blk_hist);
+  count_launch(1);
   return cudaGetLastError();
 }
 
 cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,
                            cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  keep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(slot, n, cap, keep); count_launch(1);
+  keep_kernel<<<ceil_div(n, 256), 256, 0, s>>>(slot, n, cap, keep);
+  count_launch(1);
   return cudaGetLastError();
 }
 
 cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const float* dchosen,
                                  int64_t n, int E, float* dlogits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  dlogits_kernel<<<ceil_div(n * E, 256), 256, 0, s>>>(probs, expert, dchosen, n, E, dlogits); count_launch(1);
+  dlogits_kernel<<<ceil_div(n * E, 256), 256, 0, s>>>(probs, expert, dchosen, n, E, dlogits);
+  count_launch(1);
   return cudaGetLastError();
 }
 

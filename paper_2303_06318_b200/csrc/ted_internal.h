@@ -51,7 +51,7 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
                          cudaStream_t s, const char** why);
 
 // ------------------------------------------------------------------ routing kernels
-constexpr int kRouteBlock = 256;  // tokens per routing block (gate / scan / dispatch)
+constexpr int kRouteBlock = 64;  // tokens per routing block (gate / scan / dispatch)
 constexpr int kPad = 128;         // expert segments are padded to the GEMM M tile
 
 // top-1 gate: logits = a Wg (fp32 accumulate), argmax (lowest index on ties), softmax.
