@@ -250,7 +250,8 @@ int ted_adam_step(float* master, float* m1, float* m2, uint16_t* param, const ui
     const double c2 = 1.0 - std::pow(adam->beta2, double(step));
     cuda_ok(adam_step(master, m1, m2, reinterpret_cast<bf16*>(param),
                       reinterpret_cast<const bf16*>(grad), begin, end, tile, float(adam->lr),
-                      float(adam->beta1), float(adam->beta2), float(adam->eps),
+                      float(adam->beta1), float(adam->beta2), float(1.0 - adam->beta1),
+                      float(1.0 - adam->beta2), float(adam->eps),
                       float(adam->weight_decay), float(1.0 / c1), float(1.0 / c2), S(stream)),
             "adam_step");
   });

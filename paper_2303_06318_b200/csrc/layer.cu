@@ -388,7 +388,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(zero_pad_rows(L->x_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s), "zero_pad");
     rows = L->R_max;
   } else {
-    L->mark("exchange_fwd", s);
+    L->mark("count_exchange", s);
     // count exchange over EP (the reference's A2A metadata, fabric.cpp:282-285)
     const size_t nc = size_t(L->Tc) * E;
     if (L->P > 1) {
@@ -409,10 +409,14 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(cudaMemcpyAsync(L->seg_off.p, hs, sizeof(int) * (2 * L->Eloc + 1),
                           cudaMemcpyHostToDevice, s),
           "memcpy");
+    L->mark("a2a_fwd", s);
     a2a_dispatch(L, L->xsend.p, L->x_asm.p, s);
-    if (L->dtd)
+    if (L->dtd) {
+      L->mark("ag_fwd", s);
       grouped_p2p(L->plan.ag_asm_send, L->x_asm.p, L->plan.ag_asm_recv, L->x_asm.p, h, L->tp_c,
                   s);
+    }
+    L->mark("zero_pad", s);
     zero_asm_pads(L, L->x_asm.p, s);
     rows = std::max<int64_t>(L->plan.asm_rows, 128);
   }
@@ -466,11 +470,13 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     if (L->T > 1 && L->plan.asm_rows > 0)
       NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
                        ncclSum, L->tp_c, s));
-    L->mark("return_fwd", s);
+    L->mark("a2a_ret_fwd", s);
     a2a_return(L, L->fe_asm.p, L->fhome.p, s);
-    if (L->dtd)
+    if (L->dtd) {
+      L->mark("ag_home_fwd", s);
       grouped_p2p(L->plan.ag_home_send, L->fhome.p, L->plan.ag_home_recv, L->fhome.p, h,
                   L->tp_c, s);
+    }
     fh = L->fhome.p;
   }
   L->mark("combine_fwd", s);
@@ -504,16 +510,19 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
                              L->fam_non.grad.p, s),
         "gate_backward_weight");
   int64_t rows;
-  L->mark("exchange_bwd", s);
+  L->mark(L->local ? "zero_pad" : "a2a_bwd", s);
   if (L->local) {
     check(zero_pad_rows(L->dfe_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s),
           "zero_pad");
     rows = L->R_max;
   } else {
     a2a_dispatch(L, L->dfe_send.p, L->dfe_asm.p, s);  // moe.cpp:614
-    if (L->dtd)
+    if (L->dtd) {
+      L->mark("ag_bwd", s);
       grouped_p2p(L->plan.ag_asm_send, L->dfe_asm.p, L->plan.ag_asm_recv, L->dfe_asm.p, h,
                   L->tp_c, s);  // moe.cpp:626
+    }
+    L->mark("zero_pad", s);
     zero_asm_pads(L, L->dfe_asm.p, s);
     rows = std::max<int64_t>(L->plan.asm_rows, 128);
   }
@@ -618,11 +627,13 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     if (L->T > 1 && L->plan.asm_rows > 0)  // parallel_linear.cpp:19
       NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
                        ncclSum, L->tp_c, s));
-    L->mark("return_bwd", s);
+    L->mark("a2a_ret_bwd", s);
     a2a_return(L, L->fe_asm.p, L->dx_home.p, s);  // moe.cpp:660
-    if (L->dtd)
+    if (L->dtd) {
+      L->mark("ag_home_bwd", s);
       grouped_p2p(L->plan.ag_home_send, L->dx_home.p, L->plan.ag_home_recv, L->dx_home.p, h,
                   L->tp_c, s);  // moe.cpp:678
+    }
     dxh = L->dx_home.p;
   }
   L->mark("gate_dx", s);
@@ -651,7 +662,7 @@ void family_step(ted_layer* L, Family& F, cudaStream_t s) {
   F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
   check(adam_step(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, F.begin, F.end, tile,
                   float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
-                  float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
+                  float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
                   float(1.0 / c2), s),
         "adam_step");
   if (F.group > 1) {  // ZeRO-1 completion (moe.cpp:718-732), zero-padded equal chunks
@@ -813,7 +824,9 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->dfe_asm.zero();
   if (!L->local) {
     L->xsend.alloc(size_t(n) * h);
+    L->xsend.zero();
     L->fhome.alloc(size_t(n) * h);
+    L->fhome.zero();
     L->dfe_send.alloc(size_t(n) * h);
     L->dx_home.alloc(size_t(n) * h);
   }

@@ -140,14 +140,28 @@ __device__ __forceinline__ int select_softmax(float l0v, float l1v, int E, int l
 template <int EMAX>
 __device__ __forceinline__ void stage_wg(const bf16* __restrict__ wg, int E, int c0, int hc,
                                          int HC, bf16* s_wg) {
-  for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
-    const int j = idx / hc, i = idx % hc;
-    s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
+  if (E % 8 == 0) {
+    // rows of Wg are E contiguous bf16: one 16 B vector per 8 experts, coalesced
+    const int vpr = E / 8;
+    for (int idx = threadIdx.x; idx < hc * vpr; idx += blockDim.x) {
+      const int i = idx / vpr, q = idx % vpr;
+      const uint4 u = *reinterpret_cast<const uint4*>(wg + int64_t(c0 + i) * E + q * 8);
+      const bf16* pv = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s_wg[(q * 8 + j) * HC + i] = pv[j];
+    }
+    for (int idx = threadIdx.x; idx < (EMAX - E) * hc; idx += blockDim.x)
+      s_wg[(E + idx / hc) * HC + idx % hc] = __float2bfloat16(0.f);
+  } else {
+    for (int idx = threadIdx.x; idx < EMAX * hc; idx += blockDim.x) {
+      const int j = idx / hc, i = idx % hc;
+      s_wg[j * HC + i] = j < E ? wg[int64_t(c0 + i) * E + j] : __float2bfloat16(0.f);
+    }
   }
 }
 
 // TPW tokens of a warp are processed together so each Wg slice read from smem feeds
-// TPW * 8 FMAs; TPW * EMAX == 64 accumulators for every EMAX.
+// TPW * 8 FMAs; TPW * EMAX = 32 accumulators (64 for EMAX = 64) keeps 2 CTAs / SM.
 template <int EMAX, int TPW>
 __global__ void __launch_bounds__(kThreads) gate_fwd_kernel(const bf16* __restrict__ a,
                                                             const bf16* __restrict__ wg,
@@ -673,13 +687,44 @@ __global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict
       if (j < E) out[c * E + j] = acc[c][j];
 }
 
-__global__ void gate_dw_reduce_kernel(const float* __restrict__ part, int nb, int h, int E,
-                                      bf16* __restrict__ dwg) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= int64_t(h) * E) return;
+// out[m] = sum_{s < ns(m)} part[s * stride + m] in a fixed order.  A CTA owns 32
+// consecutive m; its 8 warps take every 8th partial with 4 independent loads in flight,
+// then combine through smem.  ns(m) = ns_const, or (rows of group m / w) / rows_per_split
+// when seg_off is given (column sums: partials past a group's rows are never written).
+__global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restrict__ part,
+                                                           int64_t stride, int64_t M,
+                                                           int ns_const,
+                                                           const int* __restrict__ seg_off,
+                                                           int w, int rows_per_split,
+                                                           bf16* __restrict__ out,
+                                                           int64_t out_stride) {
+  __shared__ float s_acc[8][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = int64_t(blockIdx.x) * 32 + lane;
   float acc = 0.f;
-  for (int b = 0; b < nb; ++b) acc += part[int64_t(b) * h * E + idx];
-  dwg[idx] = __float2bfloat16(acc);
+  if (m < M) {
+    int ns = ns_const;
+    if (seg_off) {
+      const int g = int(m / w);
+      ns = (seg_off[g + 1] - seg_off[g] + rows_per_split - 1) / rows_per_split;
+    }
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+    int sidx = warp;
+    for (; sidx + 24 < ns; sidx += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a4[u] += part[int64_t(sidx + 8 * u) * stride + m];
+    }
+    for (; sidx < ns; sidx += 8) a4[0] += part[int64_t(sidx) * stride + m];
+    acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+  }
+  s_acc[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && m < M) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t += s_acc[q][lane];
+    out[(m / w) * out_stride + (m % w)] = __float2bfloat16(t);
+  }
 }
 
 // ------------------------------------------------------------------ bias-grad column sums
@@ -720,19 +765,6 @@ __global__ void __launch_bounds__(128) colsum_part_kernel(const bf16* __restrict
   pp[1] = make_float4(s[4], s[5], s[6], s[7]);
 }
 
-// sums only the splits that exist for each group (seg_off is device-resident)
-__global__ void colsum_reduce_kernel(const float* __restrict__ part, int w, int G,
-                                     const int* __restrict__ seg_off, bf16* __restrict__ out,
-                                     int64_t out_stride) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= int64_t(G) * w) return;
-  const int g = int(idx / w), c = int(idx % w);
-  const int rows = seg_off[g + 1] - seg_off[g];
-  const int ns = (rows + kColRows - 1) / kColRows;
-  float acc = 0.f;
-  for (int rs = 0; rs < ns; ++rs) acc += part[(int64_t(rs) * G + g) * w + c];
-  out[int64_t(g) * out_stride + c] = __float2bfloat16(acc);
-}
 
 // ------------------------------------------------------------------ AdamW
 __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ master,
@@ -740,14 +772,14 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ master,
                                                    bf16* __restrict__ param,
                                                    const bf16* __restrict__ grad, int64_t begin,
                                                    int64_t len, float lr, float b1, float b2,
-                                                   float eps, float wd, float inv_c1,
-                                                   float inv_c2) {
+                                                   float omb1, float omb2, float eps, float wd,
+                                                   float inv_c1, float inv_c2) {
   // master/m1/m2 are indexed over the owned range; param/grad over the whole family.
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
     const float g = __bfloat162float(grad[begin + i]);
-    const float m = b1 * m1[i] + (1.f - b1) * g;
-    const float v = b2 * m2[i] + (1.f - b2) * g * g;
+    const float m = b1 * m1[i] + omb1 * g;
+    const float v = b2 * m2[i] + omb2 * g * g;
     m1[i] = m;
     m2[i] = v;
     float p = master[i];
@@ -764,8 +796,9 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
                                                       bf16* __restrict__ param,
                                                       const bf16* __restrict__ grad,
                                                       int64_t begin, int64_t len4, float lr,
-                                                      float b1, float b2, float eps, float wd,
-                                                      float inv_c1, float inv_c2) {
+                                                      float b1, float b2, float omb1, float omb2,
+                                                      float eps, float wd, float inv_c1,
+                                                      float inv_c2) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len4; i += stride) {
     const uint2 gu = reinterpret_cast<const uint2*>(grad + begin)[i];
@@ -779,8 +812,8 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
     float* pq = &pp.x;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      mp[q] = b1 * mp[q] + (1.f - b1) * g[q];
-      vp[q] = b2 * vp[q] + (1.f - b2) * g[q] * g[q];
+      mp[q] = b1 * mp[q] + omb1 * g[q];
+      vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
       pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
     }
     reinterpret_cast<float4*>(m1)[i] = mm;
@@ -831,11 +864,27 @@ int gate_hc(int h) {
 
 template <class K>
 void smem_attr(K k, size_t bytes) {
-  static size_t set = 0;  // per instantiation
-  if (bytes > set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    set = bytes;
+  static std::atomic<size_t> cache[16];  // (kernel, bytes) slots; the kernel set is tiny
+  static std::atomic<const void*> keys[16];
+  const void* key = reinterpret_cast<const void*>(k);
+  for (int i = 0; i < 16; ++i) {
+    const void* cur = keys[i].load();
+    if (cur == key) {
+      if (cache[i].load() >= bytes) return;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+      cache[i] = bytes;
+      return;
+    }
+    if (cur == nullptr) {
+      const void* expect = nullptr;
+      if (keys[i].compare_exchange_strong(expect, key) || expect == key) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+        cache[i] = bytes;
+        return;
+      }
+    }
   }
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
 }  // namespace
@@ -854,9 +903,9 @@ cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E,
     gate_fwd_kernel<EM, TP><<<grid, kThreads, sm, s>>>(a, wg, n, h, E, HC, logits, probs,     \
                                                        expert, prob, blk_hist);               \
   }
-  if (E <= 8) TED_GATE(8, 8)
-  else if (E <= 16) TED_GATE(16, 4)
-  else if (E <= 32) TED_GATE(32, 2)
+  if (E <= 8) TED_GATE(8, 4)
+  else if (E <= 16) TED_GATE(16, 2)
+  else if (E <= 32) TED_GATE(32, 1)
   else TED_GATE(64, 1)
 #undef TED_GATE
   count_launch(1);
@@ -978,7 +1027,8 @@ cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n,
     gate_bwd_dw_kernel<64, 1><<<dim3(nb, ceil_div(h, 128)), 128, 0, s>>>(a, dlogits, n, h, E,
                                                                        part);
   }
-  gate_dw_reduce_kernel<<<ceil_div(int64_t(h) * E, 256), 256, 0, s>>>(part, nb, h, E, dwg);
+  const int64_t M = int64_t(h) * E;
+  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, nb, nullptr, int(M), 1, dwg, 0);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -994,8 +1044,9 @@ cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, 
   const int rsplits = max(1, ceil_div(max_rows_per_group, kColRows));
   dim3 grid(ceil_div(w / 8, 128), G * rsplits);
   colsum_part_kernel<<<grid, 128, 0, s>>>(D, ld, w, seg_off, G, rsplits, part);
-  colsum_reduce_kernel<<<ceil_div(int64_t(G) * w, 256), 256, 0, s>>>(part, w, G, seg_off, out,
-                                                                    out_stride);
+  const int64_t M = int64_t(G) * w;
+  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, 0, seg_off, w, kColRows, out,
+                                                      out_stride);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -1026,7 +1077,8 @@ cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const fl
 
 cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                       int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
-                      float eps, float wd, float inv_c1, float inv_c2, cudaStream_t s) {
+                      float omb1, float omb2, float eps, float wd, float inv_c1, float inv_c2,
+                      cudaStream_t s) {
   (void)tile;  // the tile only bounds the reference's up-cast buffer; none exists here
   const int64_t len = end - begin;
   if (len <= 0) return cudaSuccess;
@@ -1039,10 +1091,10 @@ cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf
                   (reinterpret_cast<uintptr_t>(grad) % 8 == 0);
   if (v4)
     adam_kernel_v4<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len / 4, lr, b1, b2,
-                                        eps, wd, inv_c1, inv_c2);
+                                        omb1, omb2, eps, wd, inv_c1, inv_c2);
   else
-    adam_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len, lr, b1, b2, eps,
-                                     wd, inv_c1, inv_c2);
+    adam_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len, lr, b1, b2, omb1,
+                                     omb2, eps, wd, inv_c1, inv_c2);
   count_launch(1);
   return cudaGetLastError();
 }

@@ -124,6 +124,7 @@ cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const fl
 // AdamW (optimizer.cpp:58-104) over [begin, end) of a flat family.
 cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                       int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
-                      float eps, float wd, float inv_c1, float inv_c2, cudaStream_t s);
+                      float omb1, float omb2, float eps, float wd, float inv_c1, float inv_c2,
+                      cudaStream_t s);
 
 }  // namespace ted

@@ -1,0 +1,145 @@
+"""Multi-GPU parity of the TED MoE layer (run under torchrun, one rank per GPU).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/mgpu_layer_check.py \
+        --tp T --ep P [--dtd 0|1] [--experts E] [--hidden h] [--tokens n] [--cf c]
+
+Every rank holds its TP shard of its local experts' weights (set from the FULL tensors by
+reference name, like Trainer::set_parameter, moe.cpp:857-868), runs forward + synthetic
+backward on its data shard (shard index d*EP + e, moe.cpp:229), and rank 0 compares the
+gathered outputs and gradients against the fp64 oracle run serially over all shards
+(SerialModel's role in the reference's parallel-equivalence tests, test_moe.cpp:288-330,
+acceptance_test.cpp:199-247).  Prints "MGPU-OK <json>" on success, raises otherwise.
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+TOL = 2e-2
+
+
+def rel(x, ref):
+    x = np.asarray(x, np.float64).ravel()
+    ref = np.asarray(ref, np.float64).ravel()
+    return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tp", type=int, default=2)
+    ap.add_argument("--ep", type=int, default=1)
+    ap.add_argument("--dtd", type=int, default=1)
+    ap.add_argument("--experts", type=int, default=8)
+    ap.add_argument("--hidden", type=int, default=256)
+    ap.add_argument("--tokens", type=int, default=512)
+    ap.add_argument("--cf", type=float, default=1.25)
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--corrupt", type=int, default=0)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_06318_b200 as ted
+    from oracle import oracle as O
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    ted.set_device(local)
+    dist.init_process_group("gloo")
+    T, P = args.tp, args.ep
+    D = world // (T * P)
+    S = P * D
+    n, h, E, cf = args.tokens, args.hidden, args.experts, args.cf
+    f = 4 * h
+    t, ep, d = rank % T, (rank // T) % P, rank // (T * P)
+    shard = d * P + ep
+    uid = [ted.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    topo = ted.derive_config(world, T, P)
+    L = ted.MoeLayer(ted.MoeModelConfig(1, h, E, n, args.seed), topo,
+                     ted.RunFlags(dtd=bool(args.dtd), corrupt_drop=bool(args.corrupt)),
+                     capacity_factor=cf, rank=rank, nccl_uid=uid[0])
+    inp = O.make_layer_inputs(S, n, h, f, E, args.seed, bf16=True)
+    L.set_param("layer0.gate.w", inp["wg"])
+    Eloc = E // P
+    for le in range(Eloc):
+        e = ep * Eloc + le
+        for k in ("w1", "b1", "w2", "b2"):
+            L.set_param(f"layer0.expert{e}.{k}", inp[k][e])
+    a = torch.from_numpy(inp["a"][shard * n:(shard + 1) * n].astype(np.float32)).cuda().bfloat16()
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    L.forward(a, y)
+    L.backward(None, da)
+    torch.cuda.synchronize()
+    st = L.stats()
+    mine = dict(rank=rank, t=t, ep=ep, d=d, shard=shard, loss=L.loss(), stats=st,
+                y=y.float().cpu().numpy(), da=da.float().cpu().numpy(),
+                dwg=L.get_grad("layer0.gate.w").reshape(h, E),
+                grads={e: {k: L.get_grad(f"layer0.expert{e}.{k}")
+                           for k in ("w1", "b1", "w2", "b2")}
+                       for e in range(ep * Eloc, (ep + 1) * Eloc)})
+    # one optimizer step must run (grad sync + AdamW + ZeRO-1 completion) without error
+    L.optimizer_step()
+    torch.cuda.synchronize()
+    mine["w1_after"] = L.get_param(f"layer0.expert{ep * Eloc}.w1")
+    allr = [None] * world
+    dist.gather_object(mine, allr if rank == 0 else None, dst=0)
+    if rank == 0:
+        o = O.moe_layer(S, n, h, f, E, cf, **inp)
+        fT = f // T
+        report = {"world": world, "tp": T, "ep": P, "dtd": bool(args.dtd), "E": E, "h": h,
+                  "n": n, "cf": cf}
+        worst = 0.0
+        loss = 0.0
+        dwg = np.zeros((h, E))
+        gsum = {}  # (e, t) -> grads summed over the expert-data replicas (run_grad_sync)
+        for r in allr:
+            s = r["shard"]
+            ey = rel(r["y"], o["y"][s * n:(s + 1) * n])
+            eda = rel(r["da"], o["da"][s * n:(s + 1) * n])
+            worst = max(worst, ey, eda)
+            if r["t"] == 0:
+                loss += r["loss"]
+                dwg += r["dwg"]
+            for e, g in r["grads"].items():
+                acc = gsum.setdefault((e, r["t"]), {k: np.zeros_like(v) for k, v in g.items()})
+                for k, v in g.items():
+                    acc[k] += v
+        for (e, tt), g in gsum.items():
+            cols = slice(tt * fT, (tt + 1) * fT)
+            errs = [rel(g["w1"].reshape(h, fT), o["dw1"][e][:, cols]),
+                    rel(g["b1"], o["db1"][e][cols]),
+                    rel(g["w2"].reshape(fT, h), o["dw2"][e][cols, :]),
+                    rel(g["b2"], o["db2"][e])]
+            if np.abs(o["dw1"][e]).sum() > 0:
+                worst = max(worst, *errs)
+        eloss = abs(loss - o["loss"]) / abs(o["loss"])
+        edwg = rel(dwg, o["dwg"])
+        worst = max(worst, eloss, edwg)
+        report.update(worst_rel=worst, loss=loss, loss_oracle=o["loss"],
+                      a2a_rows_offrank=[r["stats"]["a2a_rows_offrank"] for r in allr],
+                      send_rows=[r["stats"]["send_rows"] for r in allr],
+                      dropped=[r["stats"]["dropped"] for r in allr])
+        if args.corrupt:
+            assert not (worst <= 0.1), f"corrupt_drop went unnoticed: {report}"
+            assert not all(r["stats"]["placement_ok"] for r in allr)
+            assert worst > 0.1 or np.isnan(worst), f"corrupt_drop went unnoticed: {report}"
+            print("MGPU-OK " + json.dumps(report), flush=True)
+        else:
+            assert worst < TOL, f"multi-GPU parity failed: {report}"
+            print("MGPU-OK " + json.dumps(report), flush=True)
+    dist.barrier()
+    L.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,53 @@
+"""Multi-GPU parity (TP x EP with and without DTD) through torchrun; skipped unless the
+box exposes enough GPUs.  See tests/mgpu_layer_check.py."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(nproc, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(HERE, "mgpu_layer_check.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "MGPU-OK" in r.stdout, r.stdout[-4000:]
+    return r.stdout
+
+
+@pytest.mark.parametrize("tp,ep,dtd", [(2, 1, 1), (2, 1, 0), (1, 2, 0)])
+def test_two_gpus(tp, ep, dtd):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd))
+
+
+@pytest.mark.parametrize("tp,ep,dtd,E", [(2, 2, 1, 8), (2, 2, 0, 8), (1, 4, 0, 16), (2, 1, 1, 4)])
+def test_four_gpus(tp, ep, dtd, E):
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd), "--experts", str(E))
+
+
+def test_four_gpus_corrupt_drop_is_detected():
+    """Fault injection (test_moe.cpp:388-414): dispatching the wrong DTD chunk breaks
+    the layer output."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--corrupt", "1", "--cf", "0")
