@@ -1,7 +1,10 @@
 // gemm_sm100.cu -- persistent, warp-specialised grouped GEMM on the 5th-gen tensor
 // cores (tcgen05.mma kind::f16, bf16 in / fp32 accumulate in TMEM), operands staged by
-// TMA (SWIZZLE_128B) through a 4-stage mbarrier ring, double-buffered TMEM accumulators
-// so the epilogue of tile i overlaps the MMAs of tile i+1.
+// TMA (SWIZZLE_128B) through an mbarrier ring, double-buffered TMEM accumulators so the
+// epilogue of tile i overlaps the MMAs of tile i+1, and a TMA-staged epilogue: every
+// epilogue warp drains 32x32 accumulator blocks through a 64B-swizzled shared-memory
+// tile and writes it with one bulk tensor store (full-line HBM writes instead of
+// row-strided 16 B stores).
 //
 // This is the expert FFN of the TED MoE layer (reference: column_parallel_forward /
 // row_parallel_forward / *_backward, parallel_linear.cpp:8-40 over linear_forward /
@@ -12,7 +15,7 @@
 //   KDIM mode (wgrad):       group g reduces over rows [seg_off[g], seg_off[g+1]) of
 //                            A^T and B, writing C_g = A_g^T B_g.
 // Epilogues are fused: bias, bias+GELU (writes pre-activation Z and H), dGELU
-// (dZ = acc * gelu'(Z)).
+// (dZ = acc * gelu'(Z), Z brought in by TMA).
 //
 // Tile 128 x 256 x 64; warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
 // allocator, warps 4..11 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31, one half of
@@ -30,16 +33,24 @@ namespace ted {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int MAX_GROUPS = 256;
-constexpr int NUM_THREADS = 384;  // 4 control warps + 8 epilogue warps
 constexpr int EPI_WARPS = 8;
-constexpr uint32_t TMEM_COLS = 512;  // 2 accumulator buffers x 256 fp32 columns
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + size_t(STAGES) * STAGE_BYTES + 256 /*bars*/ +
-                              2 * (MAX_GROUPS + 1) * sizeof(int);
+constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + 8 epilogue warps
+constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
+constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
+
+template <int EPI>
+struct Cfg {
+  static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
+  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : 4;
+  static constexpr size_t STAGING = size_t(EPI_WARPS) * NOUT * EPI_BLOCK_BYTES;
+  static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
+  static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
+};
 
 struct TileInfo {
   int g, m_blk, n_blk, k_len;  // k_len = number of K elements (multiple of 64)
@@ -68,16 +79,18 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
   return true;
 }
 
+__device__ __forceinline__ float tanh_fast(float u) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return t;
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float c = 0.7978845608028654f, k3 = 0.044715f;
-  float u = c * (x + k3 * x * x * x), t;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
-  return 0.5f * x * (1.f + t);
+  return 0.5f * x * (1.f + tanh_fast(c * (x + k3 * x * x * x)));
 }
 __device__ __forceinline__ float gelu_grad_f(float x) {
   const float c = 0.7978845608028654f, k3 = 0.044715f;
-  float u = c * (x + k3 * x * x * x), t;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  const float t = tanh_fast(c * (x + k3 * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * c * (1.f + 3.f * k3 * x * x);
 }
 
@@ -90,21 +103,34 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
   return __bfloat1622float2(v);
 }
 
+// 64B-swizzled 32x32 bf16 block (TMA SWIZZLE_64B with 64-byte rows): the 16 B chunk j of
+// row r lives at chunk j ^ ((r >> 1) & 3).  A warp writing chunk j of all 32 rows hits 8
+// distinct 4-bank groups -> 4 wavefronts per 16 B store (optimal).
+__device__ __forceinline__ uint4* blk_chunk(uint8_t* blk, int r, int j) {
+  return reinterpret_cast<uint4*>(blk + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+}
+
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC,
+                        const __grid_constant__ CUtensorMap tmAux, const GemmParams p) {
+  using CF = Cfg<EPI>;
+  constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* sEpi = smem + STAGES * STAGE_BYTES;  // 1024-aligned staging blocks
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
-  int* s_off = reinterpret_cast<int*>(smem + STAGES * STAGE_BYTES + 256);
+  uint64_t* zbar = tempty + 2;  // per epilogue warp (dGELU Z loads)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(zbar + EPI_WARPS);
+  int* s_off = reinterpret_cast<int*>(smem + CF::BAR_OFF + 512);
   int* s_tstart = s_off + (MAX_GROUPS + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -125,6 +151,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    ptx::prefetch_tmap(&tmC);
+    if (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU) ptx::prefetch_tmap(&tmAux);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -133,6 +161,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], EPI_WARPS);
     }
+    for (int w = 0; w < EPI_WARPS; ++w) ptx::mbar_init(&zbar[w], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
@@ -230,35 +259,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
-    const int sp = ew & 3;          // TMEM sub-partition: lanes 32*(warp%4)..+31
-    const int chalf = ew >> 2;      // column half of the 256-wide tile
-    const int r = sp * 32 + lane;
+    const int sp = ew & 3;      // TMEM sub-partition: lanes 32*(warp%4)..+31
+    const int chalf = ew >> 2;  // column half of the 256-wide tile
+    uint8_t* blk0 = sEpi + size_t(ew) * CF::NOUT * EPI_BLOCK_BYTES;
+    uint8_t* blk1 = blk0 + EPI_BLOCK_BYTES;  // H (bias+GELU only)
     int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t acc_phase = 0, zphase = 0;
     TileInfo ti;
     for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      int64_t row;
-      __nv_bfloat16* cbase;
+      int row0, gz;
       if (p.mode == GEMM_ROWS) {
-        row = s_off[ti.g] + ti.m_blk * BM + r;
-        cbase = p.C + row * p.ldc;
+        row0 = s_off[ti.g] + ti.m_blk * BM + sp * 32;
+        gz = 0;
       } else {
-        row = int64_t(ti.m_blk) * BM + r;
-        cbase = p.C + int64_t(ti.g) * p.c_group_stride + row * p.ldc;
+        row0 = ti.m_blk * BM + sp * 32;
+        gz = ti.g;
       }
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
 #pragma unroll 1
       for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32) {
+        const int col = ti.n_blk * BN + c0;
         float v[32];
         ptx::tmem_ld32(tbase + c0, v);
         if (zero) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        const int col = ti.n_blk * BN + c0;
+        // the previous block's bulk store must have finished reading the staging tile
+        if (lane == 0) ptx::bulk_wait_read0();
+        __syncwarp();
+        if (EPI == EPI_DGELU) {
+          if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(&zbar[ew], EPI_BLOCK_BYTES);
+            ptx::tma_load_3d(blk0, &tmAux, &zbar[ew], col, row0, gz);
+          }
+          ptx::mbar_wait(&zbar[ew], zphase);
+          zphase ^= 1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 zv = *blk_chunk(blk0, lane, j);
+            const uint32_t zw[4] = {zv.x, zv.y, zv.z, zv.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = unpack_bf16(zw[q]);
+              v[8 * j + 2 * q] *= gelu_grad_f(f.x);
+              v[8 * j + 2 * q + 1] *= gelu_grad_f(f.y);
+            }
+          }
+        }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
             const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride + col;
@@ -275,41 +326,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
-        if (EPI == EPI_DGELU) {
-          const __nv_bfloat16* z = p.aux + row * p.ld_aux + col;
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            const uint4 zv = *reinterpret_cast<const uint4*>(z + i);
-            const uint32_t zw[4] = {zv.x, zv.y, zv.z, zv.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 f = unpack_bf16(zw[j]);
-              v[i + 2 * j] *= gelu_grad_f(f.x);
-              v[i + 2 * j + 1] *= gelu_grad_f(f.y);
-            }
-          }
-        }
-        uint4* dst = reinterpret_cast<uint4*>(cbase + col);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int j = 0; j < 4; ++j) {
           uint4 o;
-          o.x = pack_bf16(v[8 * i + 0], v[8 * i + 1]);
-          o.y = pack_bf16(v[8 * i + 2], v[8 * i + 3]);
-          o.z = pack_bf16(v[8 * i + 4], v[8 * i + 5]);
-          o.w = pack_bf16(v[8 * i + 6], v[8 * i + 7]);
-          dst[i] = o;
+          o.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+          o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+          o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+          o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+          *blk_chunk(blk0, lane, j) = o;
         }
         if (EPI == EPI_BIAS_GELU) {
-          uint4* hd = reinterpret_cast<uint4*>(p.aux + row * p.ld_aux + col);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int j = 0; j < 4; ++j) {
             uint4 o;
-            o.x = pack_bf16(gelu_f(v[8 * i + 0]), gelu_f(v[8 * i + 1]));
-            o.y = pack_bf16(gelu_f(v[8 * i + 2]), gelu_f(v[8 * i + 3]));
-            o.z = pack_bf16(gelu_f(v[8 * i + 4]), gelu_f(v[8 * i + 5]));
-            o.w = pack_bf16(gelu_f(v[8 * i + 6]), gelu_f(v[8 * i + 7]));
-            hd[i] = o;
+            o.x = pack_bf16(gelu_f(v[8 * j + 0]), gelu_f(v[8 * j + 1]));
+            o.y = pack_bf16(gelu_f(v[8 * j + 2]), gelu_f(v[8 * j + 3]));
+            o.z = pack_bf16(gelu_f(v[8 * j + 4]), gelu_f(v[8 * j + 5]));
+            o.w = pack_bf16(gelu_f(v[8 * j + 6]), gelu_f(v[8 * j + 7]));
+            *blk_chunk(blk1, lane, j) = o;
           }
+        }
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_3d(&tmC, blk0, col, row0, gz);
+          if (EPI == EPI_BIAS_GELU) ptx::tma_store_3d(&tmAux, blk1, col, row0, gz);
+          ptx::bulk_commit();
         }
       }
       ptx::tc_fence_before();
@@ -320,6 +362,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) ptx::bulk_wait0();
   }
   __syncthreads();
   if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
@@ -342,31 +385,31 @@ bool get_encoder() {
 
 // 3-D bf16 tensor map: dims {d0 (contiguous), d1, d2}, byte strides {s1, s2}, box {b0, b1, 1}.
 bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-              uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1) {
+              uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1,
+              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   if (!get_encoder()) return false;
   cuuint64_t dims[3] = {d0, d1, d2 == 0 ? 1 : d2};
   cuuint64_t strides[2] = {s1, s2 == 0 ? s1 * d1 : s2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const GemmParams& p,
-                     int grid, cudaStream_t s) {
+cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                     const CUtensorMap& mx, const GemmParams& p, int grid, cudaStream_t s) {
   auto k = grouped_gemm_kernel<A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(SMEM_BYTES));
+                                         int(Cfg<EPI>::SMEM));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(ma, mb, p);
+  k<<<grid, NUM_THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, p);
   count_launch(1);
   return cudaGetLastError();
 }
@@ -389,6 +432,7 @@ int sm_count() {
 //   ROWS / B MN-major: B_g [K][N] at B + g*b_group_stride  (ldb = row stride)
 //   ROWS / B K-major : B_g [N][K] at B + g*b_group_stride
 //   KDIM / A MN-major: A [rows_total][M];   B MN-major: B [rows_total][N]
+//   C (and aux): ROWS [rows_total][N] (ldc / ld_aux);  KDIM C_g [M][N] at C + g*c_group_stride
 cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_rows,
                          cudaStream_t s, const char** why) {
   auto fail = [&](const char* w) {
@@ -403,33 +447,44 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   } else {
     if (!o.a_mn || !o.b_mn) return fail("gemm: KDIM mode needs MN-major A and B");
     if (p.M % BM != 0) return fail("gemm: M must be a multiple of 128");
+    if (p.epi != EPI_STORE) return fail("gemm: KDIM mode supports the plain store epilogue");
   }
+  if ((p.epi == EPI_BIAS_GELU || p.epi == EPI_DGELU) && p.aux == nullptr)
+    return fail("gemm: epilogue needs the aux tensor");
   const uint64_t rows = uint64_t(max_rows > 0 ? max_rows : 1);
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mx;
   bool ok;
+  const auto SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
   if (p.mode == GEMM_ROWS) {
     ok = make_map(&ma, o.A, p.K, rows, 1, o.lda * 2, 0, BK, BM);
     if (o.b_mn)
       ok = ok && make_map(&mb, o.B, p.N, p.K, p.groups, o.ldb * 2, o.b_group_stride * 2, 64, BK);
     else
       ok = ok && make_map(&mb, o.B, p.K, p.N, p.groups, o.ldb * 2, o.b_group_stride * 2, BK, BN);
+    ok = ok && make_map(&mc, p.C, p.N, rows, 1, p.ldc * 2, 0, 32, 32, SW64);
+    if (p.aux) ok = ok && make_map(&mx, p.aux, p.N, rows, 1, p.ld_aux * 2, 0, 32, 32, SW64);
+    else mx = mc;
   } else {
     ok = make_map(&ma, o.A, p.M, rows, 1, o.lda * 2, 0, 64, BK) &&
-         make_map(&mb, o.B, p.N, rows, 1, o.ldb * 2, 0, 64, BK);
+         make_map(&mb, o.B, p.N, rows, 1, o.ldb * 2, 0, 64, BK) &&
+         make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2,
+                  (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 2, 32, 32, SW64);
+    mx = mc;
   }
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
   if (p.mode == GEMM_ROWS) {
     if (o.b_mn) {
-      if (p.epi == EPI_BIAS_GELU) return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, p, grid, s);
-      if (p.epi == EPI_BIAS) return launch_t<false, true, EPI_BIAS>(ma, mb, p, grid, s);
-      return launch_t<false, true, EPI_STORE>(ma, mb, p, grid, s);
+      if (p.epi == EPI_BIAS_GELU)
+        return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, mc, mx, p, grid, s);
+      if (p.epi == EPI_BIAS) return launch_t<false, true, EPI_BIAS>(ma, mb, mc, mx, p, grid, s);
+      return launch_t<false, true, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
     }
-    if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, p, grid, s);
-    if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, p, grid, s);
-    return launch_t<false, false, EPI_STORE>(ma, mb, p, grid, s);
+    if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, mc, mx, p, grid, s);
+    if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, mc, mx, p, grid, s);
+    return launch_t<false, false, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
   }
-  return launch_t<true, true, EPI_STORE>(ma, mb, p, grid, s);
+  return launch_t<true, true, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
 }
 
 }  // namespace ted
