@@ -148,6 +148,14 @@ struct ted_layer {
   int64_t last_dropped = 0;
   bool have_forward = false;
 
+  // side stream: the expert family's AdamW overlaps the tail of the backward
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr;
+  bool overlap_opt = false, exp_done_on_side = false;
+  double side_c1 = 1.0, side_c2 = 1.0;  // bias corrections of the in-flight side step
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
+  size_t side_used = 0;
+
   // live per-stage timing (CUDA events on the launching stream)
   bool timing = false;
   std::vector<cudaEvent_t> evs;
@@ -167,6 +175,22 @@ struct ted_layer {
     CU(cudaEventRecord(evs[ev_used], s));
     ev_names[ev_used] = name;
     ++ev_used;
+  }
+  // interval on the side stream: call with begin=true before, false after the work
+  void side_mark(bool begin, cudaStream_t s) {
+    if (!timing) return;
+    if (begin) {
+      if (side_used == side_evs.size()) {
+        cudaEvent_t a, b;
+        CU(cudaEventCreate(&a));
+        CU(cudaEventCreate(&b));
+        side_evs.push_back({a, b});
+      }
+      CU(cudaEventRecord(side_evs[side_used].first, s));
+    } else {
+      CU(cudaEventRecord(side_evs[side_used].second, s));
+      ++side_used;
+    }
   }
 };
 
@@ -492,6 +516,44 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
 
 namespace {
 
+// reset (set_param) + step count + bias corrections for one family step, on stream s
+void family_begin(ted_layer* L, Family& F, cudaStream_t s, double& c1, double& c2) {
+  if (F.reset) {
+    CU(cudaMemsetAsync(F.m1.p, 0, sizeof(float) * F.m1.n, s));
+    CU(cudaMemsetAsync(F.m2.p, 0, sizeof(float) * F.m2.n, s));
+    F.steps = 0;
+    F.reset = false;
+  }
+  F.steps += 1;
+  c1 = 1.0 - std::pow(L->adam.beta1, double(F.steps));
+  c2 = 1.0 - std::pow(L->adam.beta2, double(F.steps));
+}
+
+// AdamW of one tensor kind of every local expert (W1+b1 or W2+b2, contiguous per expert)
+// on the side stream once the main stream has produced its final gradient.
+void side_adam(ted_layer* L, cudaEvent_t ready, int64_t off, int64_t len, cudaStream_t s,
+               bool first) {
+  Family& F = L->fam_exp;
+  CU(cudaEventRecord(ready, s));
+  CU(cudaStreamWaitEvent(L->side, ready, 0));
+  double& c1 = L->side_c1;
+  double& c2 = L->side_c2;
+  if (first) family_begin(L, F, L->side, c1, c2);
+  const int64_t owned = F.end - F.begin;
+  const int64_t one = std::max<int64_t>(owned, 1);
+  const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
+  F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
+  L->side_mark(true, L->side);
+  // one CTA per SM: fits beside the persistent GEMM CTA (registers / threads)
+  check(adam_segments(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, L->Eloc, L->per_expert,
+                      off, len, float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
+                      float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2),
+                      float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
+                      float(1.0 / c2), sm_count(), L->side),
+        "adam_segments");
+  L->side_mark(false, L->side);
+}
+
 // --------------------------------------------------------------- backward
 void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   if (!L->have_forward) throw ConfigError("backward called before forward");
@@ -575,6 +637,9 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   check(colsum_groups(L->dfe_asm.p, h, h, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
                       G + L->off_b2, L->per_expert, s),
         "colsum db2");
+  const bool side_opt = L->overlap_opt && L->side != nullptr;
+  if (side_opt)  // W2 and b2 are final: update them while dgrad1 / wgrad1 run
+    side_adam(L, L->ev_w2, L->off_w2, int64_t(L->fT) * h + h, s, true);
   L->mark("dgrad1", s);
   // dgrad of GEMM1: dX = dZ W1^T  (column_parallel_backward :16)
   g = GemmParams{};
@@ -619,6 +684,11 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   check(colsum_groups(L->z.p, L->fT, L->fT, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
                       G + L->off_b1, L->per_expert, s),
         "colsum db1");
+  if (side_opt) {
+    side_adam(L, L->ev_w1, L->off_w1, int64_t(h) * L->fT + L->fT, s, false);
+    CU(cudaEventRecord(L->ev_side_done, L->side));
+    L->exp_done_on_side = true;
+  }
   const bf16* dxh;
   if (L->local) {
     dxh = L->fe_asm.p;
@@ -647,15 +717,8 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
 // --------------------------------------------------------------- optimizer
 void family_step(ted_layer* L, Family& F, cudaStream_t s) {
   if (F.elems == 0) return;
-  if (F.reset) {
-    CU(cudaMemsetAsync(F.m1.p, 0, sizeof(float) * F.m1.n, s));
-    CU(cudaMemsetAsync(F.m2.p, 0, sizeof(float) * F.m2.n, s));
-    F.steps = 0;
-    F.reset = false;
-  }
-  F.steps += 1;
-  const double c1 = 1.0 - std::pow(L->adam.beta1, double(F.steps));
-  const double c2 = 1.0 - std::pow(L->adam.beta2, double(F.steps));
+  double c1, c2;
+  family_begin(L, F, s, c1, c2);
   const int64_t owned = F.end - F.begin;
   const int64_t one = std::max<int64_t>(owned, 1);
   const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
@@ -692,7 +755,12 @@ void layer_optimizer(ted_layer* L, cudaStream_t s) {
                      ncclBfloat16, ncclSum, L->nonexpdp_c, s));
   L->mark("adam", s);
   family_step(L, L->fam_non, s);
-  family_step(L, L->fam_exp, s);
+  if (L->exp_done_on_side) {  // already updated on the side stream: join it
+    CU(cudaStreamWaitEvent(s, L->ev_side_done, 0));
+    L->exp_done_on_side = false;
+  } else {
+    family_step(L, L->fam_exp, s);
+  }
   L->mark("_end", s);
 }
 
@@ -830,6 +898,12 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     L->dfe_send.alloc(size_t(n) * h);
     L->dx_home.alloc(size_t(n) * h);
   }
+  if (L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 && (L->off_w2 % 4) == 0) {
+    CU(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&L->ev_w1, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&L->ev_side_done, cudaEventDisableTiming));
+  }
   CU(cudaDeviceSynchronize());
 }
 
@@ -872,6 +946,13 @@ void ted_layer_destroy(ted_layer* L) {
   if (!L) return;
   cudaDeviceSynchronize();
   for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
+  for (auto& pr : L->side_evs) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  for (cudaEvent_t e : {L->ev_w2, L->ev_w1, L->ev_side_done})
+    if (e) cudaEventDestroy(e);
+  if (L->side) cudaStreamDestroy(L->side);
   for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->world_c})
     if (*c) {
       ncclCommDestroy(*c);
@@ -978,7 +1059,14 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
   return guard([&] {
     require(L && a && y && da, "null argument");
     layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), S(stream));
-    layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), S(stream));
+    L->overlap_opt = true;  // the optimizer follows immediately: overlap it with the backward
+    try {
+      layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), S(stream));
+    } catch (...) {
+      L->overlap_opt = false;
+      throw;
+    }
+    L->overlap_opt = false;
     layer_optimizer(L, S(stream));
   });
 }
@@ -1033,6 +1121,7 @@ int ted_layer_timing(ted_layer* L, int enable) {
     CU(cudaDeviceSynchronize());
     L->timing = enable != 0;
     L->ev_used = 0;
+    L->side_used = 0;
     L->stage_ms.clear();
     L->stage_cnt.clear();
   });
@@ -1052,6 +1141,13 @@ int ted_layer_timing_read(ted_layer* L, char* out, int cap) {
       L->stage_cnt[nm] += 1;
     }
     L->ev_used = 0;
+    for (size_t i = 0; i < L->side_used; ++i) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, L->side_evs[i].first, L->side_evs[i].second));
+      L->stage_ms["adam_overlapped"] += ms;
+      L->stage_cnt["adam_overlapped"] += 1;
+    }
+    L->side_used = 0;
     std::string js = "{";
     bool first = true;
     for (auto& kv : L->stage_ms) {

@@ -826,6 +826,45 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
   }
 }
 
+// AdamW over nseg equally sized, equally strided segments of an unsharded family
+// (element e of segment k = family index k*seg_stride + seg_off + e), 4 elements per
+// thread.  Used to update one tensor kind of every local expert as soon as its gradient
+// is final, on a side stream, while the remaining backward GEMMs run.
+__global__ void __launch_bounds__(256) adam_segments_kernel(
+    float* __restrict__ master, float* __restrict__ m1, float* __restrict__ m2,
+    bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride4,
+    int64_t seg_off4, int64_t seg_len4, float lr, float b1, float b2, float omb1, float omb2,
+    float eps, float wd, float inv_c1, float inv_c2) {
+  const int64_t total = int64_t(nseg) * seg_len4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int64_t seg = t / seg_len4;
+    const int64_t i = seg * seg_stride4 + seg_off4 + (t - seg * seg_len4);
+    const uint2 gu = reinterpret_cast<const uint2*>(grad)[i];
+    const float2 g01 = bf2_to_f2(gu.x), g23 = bf2_to_f2(gu.y);
+    const float g[4] = {g01.x, g01.y, g23.x, g23.y};
+    float4 mm = reinterpret_cast<float4*>(m1)[i];
+    float4 vv = reinterpret_cast<float4*>(m2)[i];
+    float4 pp = reinterpret_cast<float4*>(master)[i];
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+    float* pq = &pp.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mp[q] = b1 * mp[q] + omb1 * g[q];
+      vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
+      pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+    }
+    reinterpret_cast<float4*>(m1)[i] = mm;
+    reinterpret_cast<float4*>(m2)[i] = vv;
+    reinterpret_cast<float4*>(master)[i] = pp;
+    uint2 po;
+    po.x = f2_to_bf2(pp.x, pp.y);
+    po.y = f2_to_bf2(pp.z, pp.w);
+    reinterpret_cast<uint2*>(param)[i] = po;
+  }
+}
+
 __global__ void expert_hist_kernel(const int* __restrict__ expert, int64_t n, int E,
                                    int* __restrict__ blk_hist) {
   __shared__ int s_hist[64];
@@ -1071,6 +1110,19 @@ cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const fl
                                  int64_t n, int E, float* dlogits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   dlogits_kernel<<<ceil_div(n * E, 256), 256, 0, s>>>(probs, expert, dchosen, n, E, dlogits);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
+                          int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
+                          float b1, float b2, float omb1, float omb2, float eps, float wd,
+                          float inv_c1, float inv_c2, int grid, cudaStream_t s) {
+  if (seg_stride % 4 || seg_off % 4 || seg_len % 4 || nseg < 1) return cudaErrorInvalidValue;
+  if (seg_len == 0) return cudaSuccess;
+  adam_segments_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
+                                            seg_off / 4, seg_len / 4, lr, b1, b2, omb1, omb2,
+                                            eps, wd, inv_c1, inv_c2);
   count_launch(1);
   return cudaGetLastError();
 }

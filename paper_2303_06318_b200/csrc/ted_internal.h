@@ -127,4 +127,10 @@ cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf
                       float omb1, float omb2, float eps, float wd, float inv_c1, float inv_c2,
                       cudaStream_t s);
 
+// AdamW over nseg equal, equally strided segments of an unsharded family (side stream).
+cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
+                          int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
+                          float b1, float b2, float omb1, float omb2, float eps, float wd,
+                          float inv_c1, float inv_c2, int grid, cudaStream_t s);
+
 }  // namespace ted
