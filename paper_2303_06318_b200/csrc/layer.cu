@@ -149,8 +149,10 @@ struct ted_layer {
   bool have_forward = false;
 
   // side stream: the expert family's AdamW overlaps the tail of the backward
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr;
+  cudaStream_t side = nullptr;  // lowest priority
+  cudaStream_t hs = nullptr;    // highest priority: the step's main work in ted_layer_step
+  cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr, ev_fork = nullptr,
+              ev_join = nullptr;
   bool overlap_opt = false, exp_done_on_side = false;
   double side_c1 = 1.0, side_c2 = 1.0;  // bias corrections of the in-flight side step
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
@@ -899,7 +901,12 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     L->dx_home.alloc(size_t(n) * h);
   }
   if (L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 && (L->off_w2 % 4) == 0) {
-    CU(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CU(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, least));
+    CU(cudaStreamCreateWithPriority(&L->hs, cudaStreamNonBlocking, greatest));
+    CU(cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&L->ev_w1, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&L->ev_side_done, cudaEventDisableTiming));
@@ -950,9 +957,10 @@ void ted_layer_destroy(ted_layer* L) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
   }
-  for (cudaEvent_t e : {L->ev_w2, L->ev_w1, L->ev_side_done})
+  for (cudaEvent_t e : {L->ev_w2, L->ev_w1, L->ev_side_done, L->ev_fork, L->ev_join})
     if (e) cudaEventDestroy(e);
   if (L->side) cudaStreamDestroy(L->side);
+  if (L->hs) cudaStreamDestroy(L->hs);
   for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->world_c})
     if (*c) {
       ncclCommDestroy(*c);
@@ -1058,16 +1066,27 @@ int ted_layer_optimizer_step(ted_layer* L, void* stream) {
 int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, void* stream) {
   return guard([&] {
     require(L && a && y && da, "null argument");
-    layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), S(stream));
-    L->overlap_opt = true;  // the optimizer follows immediately: overlap it with the backward
+    cudaStream_t cs = S(stream);
+    cudaStream_t ms = cs;
+    if (L->hs) {  // fork onto the high-priority stream; the side stream runs AdamW under it
+      CU(cudaEventRecord(L->ev_fork, cs));
+      CU(cudaStreamWaitEvent(L->hs, L->ev_fork, 0));
+      ms = L->hs;
+    }
+    layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), ms);
+    L->overlap_opt = L->hs != nullptr;  // the optimizer follows: overlap it with the backward
     try {
-      layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), S(stream));
+      layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), ms);
     } catch (...) {
       L->overlap_opt = false;
       throw;
     }
     L->overlap_opt = false;
-    layer_optimizer(L, S(stream));
+    layer_optimizer(L, ms);
+    if (L->hs) {  // join back into the caller's stream
+      CU(cudaEventRecord(L->ev_join, L->hs));
+      CU(cudaStreamWaitEvent(cs, L->ev_join, 0));
+    }
   });
 }
 

@@ -835,33 +835,51 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
     bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride4,
     int64_t seg_off4, int64_t seg_len4, float lr, float b1, float b2, float omb1, float omb2,
     float eps, float wd, float inv_c1, float inv_c2) {
+  constexpr int U = 4;  // independent 4-element vectors in flight per thread
   const int64_t total = int64_t(nseg) * seg_len4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
-    const int64_t seg = t / seg_len4;
-    const int64_t i = seg * seg_stride4 + seg_off4 + (t - seg * seg_len4);
-    const uint2 gu = reinterpret_cast<const uint2*>(grad)[i];
-    const float2 g01 = bf2_to_f2(gu.x), g23 = bf2_to_f2(gu.y);
-    const float g[4] = {g01.x, g01.y, g23.x, g23.y};
-    float4 mm = reinterpret_cast<float4*>(m1)[i];
-    float4 vv = reinterpret_cast<float4*>(m2)[i];
-    float4 pp = reinterpret_cast<float4*>(master)[i];
-    float* mp = &mm.x;
-    float* vp = &vv.x;
-    float* pq = &pp.x;
+  // short-lived CTAs (U*256 vectors each) so a concurrently launched persistent GEMM on a
+  // higher-priority stream gets SMs back quickly
+  const int64_t stride = blockDim.x;
+  {
+    const int64_t t0 = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x;
+    int64_t idx[U];
+    uint2 gu[U];
+    float4 mm[U], vv[U], pp[U];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      mp[q] = b1 * mp[q] + omb1 * g[q];
-      vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
-      pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = t0 + u * stride;
+      idx[u] = -1;
+      if (t < total) {
+        const int64_t seg = t / seg_len4;
+        idx[u] = seg * seg_stride4 + seg_off4 + (t - seg * seg_len4);
+        gu[u] = reinterpret_cast<const uint2*>(grad)[idx[u]];
+        mm[u] = reinterpret_cast<float4*>(m1)[idx[u]];
+        vv[u] = reinterpret_cast<float4*>(m2)[idx[u]];
+        pp[u] = reinterpret_cast<float4*>(master)[idx[u]];
+      }
     }
-    reinterpret_cast<float4*>(m1)[i] = mm;
-    reinterpret_cast<float4*>(m2)[i] = vv;
-    reinterpret_cast<float4*>(master)[i] = pp;
-    uint2 po;
-    po.x = f2_to_bf2(pp.x, pp.y);
-    po.y = f2_to_bf2(pp.z, pp.w);
-    reinterpret_cast<uint2*>(param)[i] = po;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (idx[u] < 0) continue;
+      const float2 g01 = bf2_to_f2(gu[u].x), g23 = bf2_to_f2(gu[u].y);
+      const float g[4] = {g01.x, g01.y, g23.x, g23.y};
+      float* mp = &mm[u].x;
+      float* vp = &vv[u].x;
+      float* pq = &pp[u].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        mp[q] = b1 * mp[q] + omb1 * g[q];
+        vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
+        pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+      }
+      reinterpret_cast<float4*>(m1)[idx[u]] = mm[u];
+      reinterpret_cast<float4*>(m2)[idx[u]] = vv[u];
+      reinterpret_cast<float4*>(master)[idx[u]] = pp[u];
+      uint2 po;
+      po.x = f2_to_bf2(pp[u].x, pp[u].y);
+      po.y = f2_to_bf2(pp[u].z, pp[u].w);
+      reinterpret_cast<uint2*>(param)[idx[u]] = po;
+    }
   }
 }
 
@@ -1120,7 +1138,10 @@ cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, cons
                           float inv_c1, float inv_c2, int grid, cudaStream_t s) {
   if (seg_stride % 4 || seg_off % 4 || seg_len % 4 || nseg < 1) return cudaErrorInvalidValue;
   if (seg_len == 0) return cudaSuccess;
-  adam_segments_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
+  (void)grid;
+  const int64_t items = int64_t(nseg) * (seg_len / 4);
+  const int ctas = int((items + 256 * 4 - 1) / (256 * 4));
+  adam_segments_kernel<<<ctas, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
                                             seg_off / 4, seg_len / 4, lr, b1, b2, omb1, omb2,
                                             eps, wd, inv_c1, inv_c2);
   count_launch(1);
