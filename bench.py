@@ -278,6 +278,11 @@ def run_ours(args, w, rank, world, local_rank, dist):
     gemm_flops = 12.0 * kept_rows * w["hidden"] * f_t  # 2 fwd + 4 bwd GEMMs, algorithmic
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak_tc = pk["bf16_tflops_sustained"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    if os.path.exists(tp) and world == 1:  # from the committed ncu --set full capture
+        with open(tp) as f:
+            traffic = json.load(f)["traffic_bytes_per_launch_mean"]
     stage_ms = {k: round(v[0] / args.steps, 4) for k, v in sorted(stages.items())}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -292,7 +297,9 @@ def run_ours(args, w, rank, world, local_rank, dist):
                          "> 126 MB L2"},
         "roofline": {"bound": "tensor", "kernel": "expert FFN tcgen05 grouped GEMMs (6/step)",
                      "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
-                     "frac": (achieved / peak_tc) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak_tc) if achieved else None, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per GEMM launch (ncu, mean of the 6)",
+                     "flops_per_launch": gemm_flops / 6,
                      "peak_source": pk["source"] + " bf16_tflops_sustained",
                      "flops_per_step": gemm_flops, "ms_per_step": gemm_ms},
         "stage_ms": stage_ms,

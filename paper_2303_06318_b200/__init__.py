@@ -48,6 +48,24 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run paper_2303_06318_b200.build() "
                       "(the TED hot path has no CPU fallback)")
 
+def _preload_nccl() -> None:
+    """libted_b200.so needs libnccl.so.2.  If torch's bundled NCCL (newer, ABI-compatible)
+    exists, load it first so that torch and this library share one NCCL whatever the
+    import order (otherwise the system 2.27 copy would shadow the symbols torch needs)."""
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        spec = None
+    for base in (spec.submodule_search_locations if spec else []) or []:
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            C.CDLL(cand, mode=C.RTLD_GLOBAL)
+            return
+
+
+_preload_nccl()
 _lib = C.CDLL(LIB_PATH)
 _vp, _i64, _i32, _u64, _dbl = C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_double
 
