@@ -187,8 +187,8 @@ int ted_gate_backward(const uint16_t* a, const uint16_t* wg, const float* probs,
                                    reinterpret_cast<bf16*>(dwg), s),
               "gate_backward_weight");
     if (dinput)
-      cuda_ok(gate_backward_input(nullptr, nullptr, dl.p, reinterpret_cast<const bf16*>(wg), n, h,
-                                  E, reinterpret_cast<bf16*>(dinput), s),
+      cuda_ok(gate_backward_input(RowSrc{}, dl.p, reinterpret_cast<const bf16*>(wg), n, h, E,
+                                  reinterpret_cast<bf16*>(dinput), s),
               "gate_backward_input");
   });
 }

@@ -17,6 +17,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -127,7 +128,16 @@ struct ted_layer {
 
   // comms
   ncclComm_t world_c = nullptr, tp_c = nullptr, ep_c = nullptr, expdp_c = nullptr,
-             nonexpdp_c = nullptr;
+             nonexpdp_c = nullptr, plane_c = nullptr;  // plane = TP x EP ranks of one d
+
+  // peer-memory exchange: IPC mappings of every plane rank's assembled buffers
+  bool direct = false;
+  int plane_rank = 0, plane_size = 1;
+  DevBuf<unsigned long long> peer_tab;  // [4][plane]: x_asm, dfe_asm, fe_asm, dx_asm
+  std::vector<void*> ipc_opened;
+  DevBuf<long long> disp_base;  // [E] dispatch rows, then [Tc][E] pull rows
+  HostBuf<long long> h_tabs;
+  DevBuf<int> bar;
 
   // parameters: expert family (local experts: w1,b1,w2,b2 each) + non-expert (gate)
   Family fam_exp, fam_non;
@@ -141,7 +151,7 @@ struct ted_layer {
   DevBuf<double> loss;
   HostBuf<int> h_kc_all, h_seg;
   // activations
-  DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home;
+  DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home, dx_asm;
   const bf16* last_a = nullptr;
   const bf16* last_y = nullptr;
   LayerPlan plan;
@@ -356,6 +366,32 @@ void a2a_return(ted_layer* L, const bf16* asm_rows, bf16* home_rows, cudaStream_
   grouped_p2p(L->plan.a2a_recv, asm_rows, recv, home_rows, L->h, L->ep_c, s);
 }
 
+// stream-ordered barrier over the TP x EP plane (all writers' kernels are fenced)
+void plane_barrier(ted_layer* L, cudaStream_t s) {
+  NC(ncclAllReduce(L->bar.p, L->bar.p, 1, ncclInt32, ncclSum, L->plane_c, s));
+}
+
+const unsigned long long* peer_table(ted_layer* L, int which) {
+  return L->peer_tab.p + size_t(which) * L->plane_size;
+}
+
+// Destination / source row bases of this rank's blocks inside every expert rank's
+// assembled buffer (all ranks hold all counts, so every rank can lay out every peer).
+void build_peer_tables(ted_layer* L, const int* cnt) {
+  const int E = L->E, Tc = L->Tc, P = L->P, Eloc = L->Eloc;
+  const int my_c = L->dtd ? L->t : 0;
+  long long* tab = L->h_tabs.p;  // [E] disp, then [Tc][E] pull
+  for (int ep2 = 0; ep2 < P; ++ep2) {
+    const LayerPlan pl = build_plan(P, L->T, E, L->dtd, ep2, 0, cnt);
+    for (int le = 0; le < Eloc; ++le) {
+      const int e = ep2 * Eloc + le;
+      tab[e] = pl.blk_row[(size_t(le) * Tc + my_c) * P + L->ep];
+      for (int c = 0; c < Tc; ++c)
+        tab[E + c * E + e] = pl.blk_row[(size_t(le) * Tc + c) * P + L->ep];
+    }
+  }
+}
+
 void zero_asm_pads(ted_layer* L, bf16* buf, cudaStream_t s) {
   int maxpad = 0;
   for (int le = 0; le < L->Eloc; ++le)
@@ -370,6 +406,22 @@ void run_gemm(const GemmOperands& o, const GemmParams& p, int64_t rows, cudaStre
   cudaError_t e = grouped_gemm(o, p, int(rows), s, &why);
   if (e != cudaSuccess)
     throw RuntimeError(std::string("grouped_gemm: ") + (why ? why : cudaGetErrorString(e)));
+}
+
+RowSrc pull_src(ted_layer* L, int which) {
+  RowSrc r;
+  r.pos_home = L->pos_home.p;
+  r.peers = peer_table(L, which);
+  r.pull_base = L->disp_base.p + L->E;
+  r.home_base = L->home_base.p;
+  r.expert = L->expert.p;
+  r.chunk_len = L->n / L->Tc;
+  r.Tc = L->Tc;
+  r.E = L->E;
+  r.Eloc = L->Eloc;
+  r.Tp = L->T;
+  r.my_t = L->t;
+  return r;
 }
 
 // --------------------------------------------------------------- forward
@@ -399,7 +451,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   ra.home_base = L->home_base.p;
   ra.seg_off = L->seg_off.p;
   check(route_scan(ra, s), "route_scan");
-  bf16* xs = L->local ? L->x_asm.p : L->xsend.p;
+  bf16* xs = L->local ? L->x_asm.p : (L->direct ? nullptr : L->xsend.p);
   check(dispatch_rows(a, L->n, h, E, L->Tc, L->my_chunk, L->cap, L->expert.p, L->blk_prefix.p,
                       L->chunk_prefix.p, L->send_base.p, L->home_base.p, L->slot.p,
                       L->pos_send.p, L->pos_home.p, xs, s),
@@ -417,17 +469,32 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     L->mark("count_exchange", s);
     // count exchange over EP (the reference's A2A metadata, fabric.cpp:282-285)
     const size_t nc = size_t(L->Tc) * E;
-    if (L->P > 1) {
-      NC(ncclAllGather(L->kc.p, L->kc_all.p, nc, ncclInt32, L->ep_c, s));
-    } else {
-      check(cudaMemcpyAsync(L->kc_all.p, L->kc.p, nc * sizeof(int), cudaMemcpyDeviceToDevice, s),
+    std::vector<int> cnt(nc * L->P);
+    if (L->direct) {
+      // over the whole plane: also orders this step's peer writes after every peer's
+      // previous-step reads of its buffers
+      NC(ncclAllGather(L->kc.p, L->kc_all.p, nc, ncclInt32, L->plane_c, s));
+      check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->plane_size * sizeof(int),
+                            cudaMemcpyDeviceToHost, s),
             "memcpy");
+      check(cudaStreamSynchronize(s), "sync");
+      for (int src = 0; src < L->P; ++src)  // TP peers hold identical counts: take t = 0
+        std::memcpy(cnt.data() + size_t(src) * nc, L->h_kc_all.p + size_t(L->T * src) * nc,
+                    nc * sizeof(int));
+    } else {
+      if (L->P > 1) {
+        NC(ncclAllGather(L->kc.p, L->kc_all.p, nc, ncclInt32, L->ep_c, s));
+      } else {
+        check(cudaMemcpyAsync(L->kc_all.p, L->kc.p, nc * sizeof(int), cudaMemcpyDeviceToDevice, s),
+              "memcpy");
+      }
+      check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->P * sizeof(int),
+                            cudaMemcpyDeviceToHost, s),
+            "memcpy");
+      check(cudaStreamSynchronize(s), "sync");
+      std::memcpy(cnt.data(), L->h_kc_all.p, nc * L->P * sizeof(int));
     }
-    check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->P * sizeof(int),
-                          cudaMemcpyDeviceToHost, s),
-          "memcpy");
-    check(cudaStreamSynchronize(s), "sync");
-    L->plan = build_plan(L->P, L->T, E, L->dtd, L->ep, L->t, L->h_kc_all.p);
+    L->plan = build_plan(L->P, L->T, E, L->dtd, L->ep, L->t, cnt.data());
     if (L->plan.asm_rows > L->R_max) throw RuntimeError("assembled rows exceed workspace");
     int* hs = L->h_seg.p;
     for (int i = 0; i <= L->Eloc; ++i) hs[i] = L->plan.seg_off[i];
@@ -435,12 +502,33 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(cudaMemcpyAsync(L->seg_off.p, hs, sizeof(int) * (2 * L->Eloc + 1),
                           cudaMemcpyHostToDevice, s),
           "memcpy");
-    L->mark("a2a_fwd", s);
-    a2a_dispatch(L, L->xsend.p, L->x_asm.p, s);
-    if (L->dtd) {
-      L->mark("ag_fwd", s);
-      grouped_p2p(L->plan.ag_asm_send, L->x_asm.p, L->plan.ag_asm_recv, L->x_asm.p, h, L->tp_c,
-                  s);
+    if (L->direct) {
+      build_peer_tables(L, cnt.data());
+      check(cudaMemcpyAsync(L->disp_base.p, L->h_tabs.p, sizeof(long long) * E * (1 + L->Tc),
+                            cudaMemcpyHostToDevice, s),
+            "memcpy");
+      // the all-to-all (and, with DTD, the expert-side all-gather) as one NVLink scatter
+      L->mark("dispatch_peer", s);
+      PeerDst pd;
+      pd.peers = peer_table(L, 0);
+      pd.disp_base = L->disp_base.p;
+      pd.send_base = L->send_base.p;
+      pd.Eloc = L->Eloc;
+      pd.Tp = L->T;
+      pd.my_t = L->t;
+      pd.all_replicas = L->dtd ? 1 : 0;
+      check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
+            "scatter_rows_peer");
+      L->mark("barrier", s);
+      plane_barrier(L, s);
+    } else {
+      L->mark("a2a_fwd", s);
+      a2a_dispatch(L, L->xsend.p, L->x_asm.p, s);
+      if (L->dtd) {
+        L->mark("ag_fwd", s);
+        grouped_p2p(L->plan.ag_asm_send, L->x_asm.p, L->plan.ag_asm_recv, L->x_asm.p, h,
+                    L->tp_c, s);
+      }
     }
     L->mark("zero_pad", s);
     zero_asm_pads(L, L->x_asm.p, s);
@@ -489,6 +577,23 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   run_gemm(o, g, rows, s);
 
   const bf16* fh;
+  const double nglob = double(L->n) * L->P * L->D;
+  if (L->direct) {
+    L->mark("tp_allreduce_fwd", s);
+    if (L->T > 1 && L->plan.asm_rows > 0)
+      NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
+                       ncclSum, L->tp_c, s));
+    L->mark("barrier", s);
+    plane_barrier(L, s);
+    // return trip + DTD home gather + combine: pull each token's row from its expert rank
+    L->mark("combine_pull", s);
+    check(combine_pull(pull_src(L, 2), L->prob.p, L->n, h, y, L->fhome.p, L->loss_part.p, s),
+          "combine_pull");
+    check(loss_finalize(L->loss_part.p, L->nblk, 1.0 / (2.0 * nglob), L->loss.p, s), "loss");
+    L->mark("_end", s);
+    L->have_forward = true;
+    return;
+  }
   if (L->local) {
     fh = L->fe_asm.p;
   } else {
@@ -508,7 +613,6 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   L->mark("combine_fwd", s);
   check(combine_forward(fh, L->pos_home.p, L->prob.p, L->n, h, y, L->loss_part.p, s),
         "combine_forward");
-  const double nglob = double(L->n) * L->P * L->D;
   check(loss_finalize(L->loss_part.p, L->nblk, 1.0 / (2.0 * nglob), L->loss.p, s), "loss");
   L->mark("_end", s);
   L->have_forward = true;
@@ -565,6 +669,20 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   bf16* dfe_t = L->local ? L->dfe_asm.p : L->dfe_send.p;
   L->mark("combine_bwd", s);
   // combine backward + dlogits (moe.cpp:587-597, :197-203)
+  if (L->direct) {  // p*dy rows go straight into the experts' dFe buffers (moe.cpp:603-632)
+    PeerDst pd;
+    pd.peers = peer_table(L, 1);
+    pd.disp_base = L->disp_base.p;
+    pd.send_base = L->send_base.p;
+    pd.Eloc = L->Eloc;
+    pd.Tp = L->T;
+    pd.my_t = L->t;
+    pd.all_replicas = L->dtd ? 1 : 0;
+    check(combine_backward_peer(L->fhome.p, L->pos_home.p, L->pos_send.p, L->prob.p, L->probs.p,
+                                L->expert.p, L->n, h, E, dy, L->last_y, float(1.0 / nglob), pd,
+                                L->dlogits.p, s),
+          "combine_backward_peer");
+  } else
   check(combine_backward(fh, L->pos_home.p, L->pos_send.p, L->prob.p, L->probs.p, L->expert.p,
                          L->n, h, E, dy, L->last_y, float(1.0 / nglob), dfe_t, L->dlogits.p, s),
         "combine_backward");
@@ -579,6 +697,12 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     check(zero_pad_rows(L->dfe_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s),
           "zero_pad");
     rows = L->R_max;
+  } else if (L->direct) {
+    L->mark("barrier", s);
+    plane_barrier(L, s);
+    L->mark("zero_pad", s);
+    zero_asm_pads(L, L->dfe_asm.p, s);
+    rows = std::max<int64_t>(L->plan.asm_rows, 128);
   } else {
     a2a_dispatch(L, L->dfe_send.p, L->dfe_asm.p, s);  // moe.cpp:614
     if (L->dtd) {
@@ -651,7 +775,8 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   g.epi = EPI_STORE;
   g.N = h;
   g.K = L->fT;
-  g.C = L->fe_asm.p;  // Fe is dead after forward: reuse for dX
+  bf16* dx_asm = L->direct ? L->dx_asm.p : L->fe_asm.p;  // Fe is dead after forward
+  g.C = dx_asm;
   g.ldc = h;
   o = GemmOperands{};
   o.A = L->z.p;
@@ -692,6 +817,21 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     L->exp_done_on_side = true;
   }
   const bf16* dxh;
+  if (L->direct) {
+    L->mark("tp_allreduce_bwd", s);
+    if (L->T > 1 && L->plan.asm_rows > 0)  // parallel_linear.cpp:19
+      NC(ncclAllReduce(dx_asm, dx_asm, size_t(L->plan.asm_rows) * h, ncclBfloat16, ncclSum,
+                       L->tp_c, s));
+    L->mark("barrier", s);
+    plane_barrier(L, s);
+    L->mark("gate_dx", s);
+    // return trip of dX pulled from the expert ranks + da = dX + dl Wg^T (moe.cpp:660-685)
+    check(gate_backward_input(pull_src(L, 3), L->dlogits.p, L->fam_non.param.p, L->n, h, E, da,
+                              s),
+          "gate_backward_input");
+    L->mark("_end", s);
+    return;
+  }
   if (L->local) {
     dxh = L->fe_asm.p;
   } else {
@@ -710,8 +850,10 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   }
   L->mark("gate_dx", s);
   // da = da_dispatch + dinput_gate (moe.cpp:685)
-  check(gate_backward_input(dxh, L->pos_home.p, L->dlogits.p, L->fam_non.param.p, L->n, h, E,
-                            da, s),
+  RowSrc rs;
+  rs.local = dxh;
+  rs.pos_home = L->pos_home.p;
+  check(gate_backward_input(rs, L->dlogits.p, L->fam_non.param.p, L->n, h, E, da, s),
         "gate_backward_input");
   L->mark("_end", s);
 }
@@ -784,6 +926,45 @@ std::vector<std::string> local_param_names(ted_layer* L) {
   return v;
 }
 
+// Export the four exchange buffers with CUDA IPC, all-gather the handles over the plane
+// and map every peer's buffers (NVLink peer access), giving device tables of base pointers.
+void setup_peer_exchange(ted_layer* L) {
+  L->dx_asm.alloc(size_t(L->R_max) * L->h);
+  L->disp_base.alloc(size_t(L->E) * (1 + L->Tc));
+  L->h_tabs.alloc(size_t(L->E) * (1 + L->Tc));
+  L->bar.alloc(1);
+  L->bar.zero();
+  bf16* mine[4] = {L->x_asm.p, L->dfe_asm.p, L->fe_asm.p, L->dx_asm.p};
+  const int PS = L->plane_size;
+  const size_t HB = sizeof(cudaIpcMemHandle_t);
+  std::vector<char> hmine(4 * HB), hall(size_t(PS) * 4 * HB);
+  for (int b = 0; b < 4; ++b)
+    CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(hmine.data() + b * HB), mine[b]));
+  DevBuf<char> dh;
+  dh.alloc(hall.size());
+  CU(cudaMemcpy(dh.p + size_t(L->plane_rank) * 4 * HB, hmine.data(), 4 * HB,
+                cudaMemcpyHostToDevice));
+  NC(ncclAllGather(dh.p + size_t(L->plane_rank) * 4 * HB, dh.p, 4 * HB, ncclChar, L->plane_c,
+                   nullptr));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(hall.data(), dh.p, hall.size(), cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> tab(size_t(4) * PS);
+  for (int r = 0; r < PS; ++r)
+    for (int b = 0; b < 4; ++b) {
+      void* ptr = mine[b];
+      if (r != L->plane_rank) {
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, hall.data() + (size_t(r) * 4 + b) * HB, HB);
+        CU(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+        L->ipc_opened.push_back(ptr);
+      }
+      tab[size_t(b) * PS + r] = reinterpret_cast<unsigned long long>(ptr);
+    }
+  L->peer_tab.alloc(tab.size());
+  CU(cudaMemcpy(L->peer_tab.p, tab.data(), tab.size() * sizeof(unsigned long long),
+                cudaMemcpyHostToDevice));
+}
+
 void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* topo,
                   const ted_flags* flags, const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
                   double cf, int shard_opt, int rank, const void* uid) {
@@ -844,6 +1025,11 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     NC(ncclCommSplit(L->world_c, L->t + L->T * L->d, L->ep, &L->ep_c, nullptr));
     NC(ncclCommSplit(L->world_c, L->t + L->T * L->ep, L->d, &L->expdp_c, nullptr));
     NC(ncclCommSplit(L->world_c, L->t, L->ep + L->P * L->d, &L->nonexpdp_c, nullptr));
+    NC(ncclCommSplit(L->world_c, L->d, L->t + L->T * L->ep, &L->plane_c, nullptr));
+    const char* ex = std::getenv("TED_EXCHANGE");
+    L->direct = !L->local && !flags->corrupt_drop && !(ex && std::strcmp(ex, "nccl") == 0);
+    L->plane_rank = L->t + L->T * L->ep;
+    L->plane_size = L->T * L->P;
   }
 
   // flat families in enumerate_params order (moe.cpp:115-147, flatten_family :303-312)
@@ -875,12 +1061,12 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->blk_prefix.alloc(size_t(L->nblk) * E);
   L->chunk_prefix.alloc(size_t(L->Tc + 1) * E);
   L->kc.alloc(size_t(L->Tc) * E);
-  L->kc_all.alloc(size_t(L->Tc) * E * L->P);
+  L->kc_all.alloc(size_t(L->Tc) * E * L->P * L->T);
   L->send_base.alloc(E);
   L->home_base.alloc(size_t(L->Tc) * E);
   L->seg_off.alloc(size_t(2 * L->Eloc + 2));
   L->seg_off.zero();
-  L->h_kc_all.alloc(size_t(L->Tc) * E * L->P);
+  L->h_kc_all.alloc(size_t(L->Tc) * E * L->P * L->T);
   L->h_seg.alloc(size_t(2 * L->Eloc + 2));
   L->gate_part.alloc(gate_dw_part_floats(n, L->h, L->E));
   L->col_part.alloc(std::max(colsum_part_floats(L->fT, L->Eloc, int(L->R_max)),
@@ -900,6 +1086,7 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     L->dfe_send.alloc(size_t(n) * h);
     L->dx_home.alloc(size_t(n) * h);
   }
+  if (L->direct) setup_peer_exchange(L);
   if (L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 && (L->off_w2 % 4) == 0) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -961,7 +1148,10 @@ void ted_layer_destroy(ted_layer* L) {
     if (e) cudaEventDestroy(e);
   if (L->side) cudaStreamDestroy(L->side);
   if (L->hs) cudaStreamDestroy(L->hs);
-  for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->world_c})
+  for (void* ptr : L->ipc_opened) cudaIpcCloseMemHandle(ptr);
+  L->ipc_opened.clear();
+  for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->plane_c,
+                        &L->world_c})
     if (*c) {
       ncclCommDestroy(*c);
       *c = nullptr;

@@ -18,6 +18,7 @@
 #include <atomic>
 
 #include "ted_internal.h"
+#include "ted_vec.cuh"
 
 namespace ted {
 
@@ -27,48 +28,10 @@ void count_launch(int k) { g_launches += k; }
 
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
 constexpr int kThreads = 256;              // 8 warps
 constexpr int kWarpTok = kRouteBlock / 8;  // tokens per warp (8)
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
-
-__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
-  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
-  return __bfloat1622float2(v);
-}
-__device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
-  float2 t;
-  t = bf2_to_f2(u.x); f[0] = t.x; f[1] = t.y;
-  t = bf2_to_f2(u.y); f[2] = t.x; f[3] = t.y;
-  t = bf2_to_f2(u.z); f[4] = t.x; f[5] = t.y;
-  t = bf2_to_f2(u.w); f[6] = t.x; f[7] = t.y;
-}
-__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
-  uint4 u;
-  u.x = f2_to_bf2(f[0], f[1]);
-  u.y = f2_to_bf2(f[2], f[3]);
-  u.z = f2_to_bf2(f[4], f[5]);
-  u.w = f2_to_bf2(f[6], f[7]);
-  return u;
-}
-// streaming 16-byte load that does not allocate in L1
-__device__ __forceinline__ uint4 ldg_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
-}
 
 // Reduce-scatter of 32 per-lane partial values: afterwards lane l holds the warp total of
 // value index l.  31 shuffles instead of 32 x 5.
@@ -581,9 +544,23 @@ __global__ void __launch_bounds__(kThreads) combine_bwd_kernel(
 }
 
 // ------------------------------------------------------------------ gate backward
+__device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h) {
+  const int ph = R.pos_home ? R.pos_home[k] : -1;
+  if (ph < 0) return nullptr;
+  if (R.peers == nullptr) return R.local + int64_t(ph) * h;
+  const int e = R.expert[k];
+  int c = 0;
+  if (R.Tc > 1) {
+    c = int(k / R.chunk_len);
+    if (c >= R.Tc) c = R.Tc - 1;
+  }
+  const int64_t r = int64_t(ph) - R.home_base[c * R.E + e];
+  const bf16* base = reinterpret_cast<const bf16*>(R.peers[R.my_t + R.Tp * (e / R.Eloc)]);
+  return base + (R.pull_base[c * R.E + e] + r) * h;
+}
+
 template <int EMAX>
-__global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const bf16* __restrict__ dx_home,
-                                                               const int* __restrict__ pos_home,
+__global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
                                                                const float* __restrict__ dl,
                                                                const bf16* __restrict__ wg,
                                                                int64_t n, int h, int E, int HC,
@@ -602,8 +579,8 @@ __global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const bf16* __res
       if (k >= n) break;
       const float d0 = lane < E ? dl[k * E + lane] : 0.f;
       const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
-      const int ph = pos_home ? pos_home[k] : -1;
-      const bf16* src = ph >= 0 ? dx_home + int64_t(ph) * h + c0 : nullptr;
+      const bf16* row = src_row(R, k, h);
+      const bf16* src = row ? row + c0 : nullptr;
       for (int base = lane * 8; base < hc; base += 256 * 4) {
         uint4 xv[4];
 #pragma unroll
@@ -1037,9 +1014,8 @@ cudaError_t combine_backward(const bf16* fhome, const int* pos_home, const int* 
   return cudaGetLastError();
 }
 
-cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const float* dlogits,
-                                const bf16* wg, int64_t n, int h, int E, bf16* da,
-                                cudaStream_t s) {
+cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const bf16* wg,
+                                int64_t n, int h, int E, bf16* da, cudaStream_t s) {
   if (E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
@@ -1048,8 +1024,7 @@ cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const 
     const int HC = gate_hc<EM>(h);                                                             \
     const size_t sm = size_t(EM) * HC * 2;                                                     \
     smem_attr(gate_bwd_dx_kernel<EM>, sm);                                                     \
-    gate_bwd_dx_kernel<EM><<<grid, kThreads, sm, s>>>(dx_home, pos_home, dlogits, wg, n, h, E,  \
-                                                      HC, da);                                 \
+    gate_bwd_dx_kernel<EM><<<grid, kThreads, sm, s>>>(src, dlogits, wg, n, h, E, HC, da);     \
   }
   if (E <= 8) TED_GBX(8)
   else if (E <= 16) TED_GBX(16)

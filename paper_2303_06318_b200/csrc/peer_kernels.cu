@@ -1,0 +1,260 @@
+// peer_kernels.cu -- the EP all-to-all, the DTD all-gathers and the combine's return trip
+// done by the routing kernels themselves over NVLink peer memory (CUDA IPC mappings of
+// the expert ranks' assembled buffers), instead of staging + NCCL send/recv.
+//
+//   dispatch (moe.cpp:454-493):  every kept row of this rank's DTD chunk is stored
+//       straight into its expert's assembled buffer on replica my_t -- or, with DTD, on
+//       every TP replica (the all-gather folded into the scatter: one source per row).
+//   return + combine (moe.cpp:504-563): each token pulls its expert output row from the
+//       expert rank's (TP-reduced) buffer and scales it by p; the row is also kept in a
+//       token-ordered local copy for the backward (dchosen = <f_home, dy>).
+//   backward dispatch (moe.cpp:603-632): p * dy rows stored into the experts' dFe buffers
+//       exactly like the forward dispatch; the return of dX is a pull in gate backward.
+// Ordering across ranks is provided by stream-ordered NCCL barriers in layer.cu; every
+// writer kernel ends with a system-scope fence.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ted_internal.h"
+#include "ted_vec.cuh"
+
+namespace ted {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpTok = kRouteBlock / 8;
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// Row r of this token on replica t of expert e's EP rank.
+__device__ __forceinline__ bf16* dst_row(const PeerDst& D, int t, int e, int64_t r, int h) {
+  bf16* base = reinterpret_cast<bf16*>(D.peers[t + D.Tp * (e / D.Eloc)]);
+  return base + (D.disp_base[e] + r) * h;
+}
+
+__device__ __forceinline__ void scale8(uint4& u, float s) {
+  float f[8];
+  unpack8(u, f);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) f[q] *= s;
+  u = pack8(f);
+}
+
+__global__ void __launch_bounds__(kThreads) scatter_peer_kernel(const bf16* __restrict__ a,
+                                                                const int* __restrict__ pos_send,
+                                                                const int* __restrict__ expert,
+                                                                int64_t n, int h, PeerDst D,
+                                                                const float* __restrict__ scale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = h / 8;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + t;
+    if (k >= n) break;
+    const int ps = pos_send[k];
+    if (ps < 0) continue;
+    const int e = expert[k];
+    const int64_t r = int64_t(ps) - D.send_base[e];
+    const float sc = scale ? scale[k] : 1.f;
+    const uint4* src = reinterpret_cast<const uint4*>(a + k * h);
+    const int t0 = D.all_replicas ? 0 : D.my_t;
+    const int t1 = D.all_replicas ? D.Tp : D.my_t + 1;
+    for (int base = lane; base < vec; base += 32 * 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        if (i < vec) {
+          v[u] = ldg_stream(src + i);
+          if (scale) scale8(v[u], sc);
+        }
+      }
+      for (int tr = t0; tr < t1; ++tr) {
+        uint4* dst = reinterpret_cast<uint4*>(dst_row(D, tr, e, r, h));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = base + u * 32;
+          if (i < vec) dst[i] = v[u];
+        }
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+__device__ __forceinline__ const bf16* pull_row(const RowSrc& R, int64_t k, int h) {
+  const int ph = R.pos_home[k];
+  if (ph < 0) return nullptr;
+  const int e = R.expert[k];
+  int c = 0;
+  if (R.Tc > 1) {
+    c = int(k / R.chunk_len);
+    if (c >= R.Tc) c = R.Tc - 1;
+  }
+  const int64_t r = int64_t(ph) - R.home_base[c * R.E + e];
+  const bf16* base = reinterpret_cast<const bf16*>(R.peers[R.my_t + R.Tp * (e / R.Eloc)]);
+  return base + (R.pull_base[c * R.E + e] + r) * h;
+}
+
+__global__ void __launch_bounds__(kThreads) combine_pull_kernel(RowSrc R,
+                                                                const float* __restrict__ prob,
+                                                                int64_t n, int h,
+                                                                bf16* __restrict__ y,
+                                                                bf16* __restrict__ fhome,
+                                                                float* __restrict__ loss_part) {
+  __shared__ float s_red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = h / 8;
+  float sq = 0.f;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + t;
+    if (k >= n) break;
+    const bf16* src = pull_row(R, k, h);
+    const float pk = prob[k];
+    uint4* yd = reinterpret_cast<uint4*>(y + k * h);
+    uint4* fd = reinterpret_cast<uint4*>(fhome + k * h);
+    for (int base = lane; base < vec; base += 32 * 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (i < vec && src) v[u] = ldg_stream(reinterpret_cast<const uint4*>(src) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        if (i >= vec) continue;
+        fd[i] = v[u];
+        float f[8];
+        unpack8(v[u], f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          f[q] *= pk;
+          sq = fmaf(f[q], f[q], sq);
+        }
+        yd[i] = pack8(f);
+      }
+    }
+  }
+  sq = warp_sum(sq);
+  if (lane == 0) s_red[warp] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss_part) {
+    float tot = 0.f;
+    for (int w = 0; w < 8; ++w) tot += s_red[w];
+    loss_part[blockIdx.x] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) combine_bwd_peer_kernel(
+    const bf16* __restrict__ fhome, const int* __restrict__ pos_home,
+    const int* __restrict__ pos_send, const float* __restrict__ prob,
+    const float* __restrict__ probs, const int* __restrict__ expert, int64_t n, int h, int E,
+    const bf16* __restrict__ dy, const bf16* __restrict__ y, float dy_scale, PeerDst D,
+    float* __restrict__ dlogits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int vec = h / 8;
+  const bf16* dsrc_base = dy ? dy : y;
+  const float sc = dy ? 1.f : dy_scale;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int64_t k = tok0 + t;
+    if (k >= n) break;
+    const int ph = pos_home[k], ps = pos_send[k];
+    const int e = expert[k];
+    const float pk = prob[k];
+    const uint4* dsrc = reinterpret_cast<const uint4*>(dsrc_base + k * h);
+    const uint4* fsrc = reinterpret_cast<const uint4*>(fhome + k * h);
+    const int64_t r = ps >= 0 ? int64_t(ps) - D.send_base[e] : 0;
+    const int t0 = D.all_replicas ? 0 : D.my_t;
+    const int t1 = ps < 0 ? t0 : (D.all_replicas ? D.Tp : D.my_t + 1);
+    float dot = 0.f;
+    for (int base = lane; base < vec; base += 32 * 4) {
+      uint4 dv[4], fv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        dv[u] = make_uint4(0, 0, 0, 0);
+        fv[u] = make_uint4(0, 0, 0, 0);
+        if (i < vec) {
+          dv[u] = ldg_stream(dsrc + i);
+          if (ph >= 0) fv[u] = ldg_stream(fsrc + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * 32;
+        if (i >= vec) continue;
+        float d[8], f[8];
+        unpack8(dv[u], d);
+        unpack8(fv[u], f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d[q] *= sc;
+          dot = fmaf(f[q], d[q], dot);
+          d[q] *= pk;
+        }
+        dv[u] = pack8(d);
+      }
+      for (int tr = t0; tr < t1; ++tr) {
+        uint4* dst = reinterpret_cast<uint4*>(dst_row(D, tr, e, r, h));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = base + u * 32;
+          if (i < vec) dst[i] = dv[u];
+        }
+      }
+    }
+    const float dchosen = warp_sum(dot);
+    const float coef = dchosen * probs[k * E + e];
+    for (int j = lane; j < E; j += 32)
+      dlogits[k * E + j] = coef * ((j == e ? 1.f : 0.f) - probs[k * E + j]);
+  }
+  __threadfence_system();
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return int((a + b - 1) / b); }
+
+}  // namespace
+
+cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* expert, int64_t n,
+                              int h, const PeerDst& dst, const float* scale, bool scale_by_prob,
+                              cudaStream_t s) {
+  if (h % 8 != 0) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  scatter_peer_kernel<<<grid, kThreads, 0, s>>>(a, pos_send, expert, n, h, dst,
+                                                scale_by_prob ? scale : nullptr);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_pull(const RowSrc& src, const float* prob, int64_t n, int h, bf16* y,
+                         bf16* fhome, float* loss_part, cudaStream_t s) {
+  if (h % 8 != 0 || src.peers == nullptr) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  combine_pull_kernel<<<grid, kThreads, 0, s>>>(src, prob, n, h, y, fhome, loss_part);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+cudaError_t combine_backward_peer(const bf16* fhome, const int* pos_home, const int* pos_send,
+                                  const float* prob, const float* probs, const int* expert,
+                                  int64_t n, int h, int E, const bf16* dy, const bf16* y,
+                                  float dy_scale, const PeerDst& dst, float* dlogits,
+                                  cudaStream_t s) {
+  if (h % 8 != 0) return cudaErrorInvalidValue;
+  const int grid = ceil_div(n, kRouteBlock);
+  if (grid == 0) return cudaSuccess;
+  combine_bwd_peer_kernel<<<grid, kThreads, 0, s>>>(fhome, pos_home, pos_send, prob, probs,
+                                                    expert, n, h, E, dy, y, dy_scale, dst,
+                                                    dlogits);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+}  // namespace ted

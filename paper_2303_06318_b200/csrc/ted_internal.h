@@ -100,10 +100,46 @@ cudaError_t combine_backward(const bf16* fhome, const int* pos_home, const int* 
                              const float* prob, const float* probs, const int* expert,
                              int64_t n, int h, int E, const bf16* dy, const bf16* y,
                              float dy_scale, bf16* dfe, float* dlogits, cudaStream_t s);
-// da[k] = dx_home[pos_home[k]] + sum_j dlogits[k][j] Wg[:, j]
-cudaError_t gate_backward_input(const bf16* dx_home, const int* pos_home, const float* dlogits,
-                                const bf16* wg, int64_t n, int h, int E, bf16* da,
-                                cudaStream_t s);
+// Where token k's expert-side row lives: locally (home layout, pos_home) or, for the
+// peer-memory exchange, in the assembled buffer of replica my_t of expert e's EP rank:
+// peers[my_t + Tp * (e / Eloc)] + (pull_base[c][e] + pos_home[k] - home_base[c][e]) rows.
+struct RowSrc {
+  const bf16* local = nullptr;  // home-layout rows (local mode)
+  const int* pos_home = nullptr;
+  const unsigned long long* peers = nullptr;  // device table of peer buffer bases
+  const long long* pull_base = nullptr;       // [Tc][E]
+  const int* home_base = nullptr;             // [Tc][E]
+  const int* expert = nullptr;
+  int64_t chunk_len = 0;
+  int Tc = 1, E = 1, Eloc = 1, Tp = 1, my_t = 0;
+};
+// da[k] = row(k) + sum_j dlogits[k][j] Wg[:, j]
+cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const bf16* wg,
+                                int64_t n, int h, int E, bf16* da, cudaStream_t s);
+
+// ---- peer-memory exchange (CUDA IPC pointers over NVLink) -------------------------
+// Scatter every kept row of this rank's chunk straight into the assembled buffer of its
+// expert's EP rank: replica my_t, or every TP replica (DTD: one source per row).
+// Destination row = disp_base[e] + pos_send[k] - send_base[e].  Ends with a system fence.
+struct PeerDst {
+  const unsigned long long* peers = nullptr;  // plane rank -> buffer base
+  const long long* disp_base = nullptr;       // [E]
+  const int* send_base = nullptr;             // [E]
+  int Eloc = 1, Tp = 1, my_t = 0, all_replicas = 0;
+};
+cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* expert, int64_t n,
+                              int h, const PeerDst& dst, const float* scale, bool scale_by_prob,
+                              cudaStream_t s);
+// y[k] = prob[k] * row(k), fhome[k] = row(k) (token order, for the backward), loss partials
+cudaError_t combine_pull(const RowSrc& src, const float* prob, int64_t n, int h, bf16* y,
+                         bf16* fhome, float* loss_part, cudaStream_t s);
+// dchosen = <fhome[k], dy[k]> (token-order fhome), dlogits, and p*dy rows scattered to the
+// experts' dFe buffers like scatter_rows_peer.
+cudaError_t combine_backward_peer(const bf16* fhome, const int* pos_home, const int* pos_send,
+                                  const float* prob, const float* probs, const int* expert,
+                                  int64_t n, int h, int E, const bf16* dy, const bf16* y,
+                                  float dy_scale, const PeerDst& dst, float* dlogits,
+                                  cudaStream_t s);
 // dWg = a^T dlogits (deterministic two-stage reduction), written as bf16 (+ fp32 copy).
 cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n, int h, int E,
                                  float* part, bf16* dwg, cudaStream_t s);

@@ -1,0 +1,49 @@
+// ted_vec.cuh -- bf16 vector helpers shared by the HBM-bound kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ted {
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t u) {
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+  return __bfloat1622float2(v);
+}
+__device__ __forceinline__ uint32_t f2_to_bf2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  float2 t;
+  t = bf2_to_f2(u.x); f[0] = t.x; f[1] = t.y;
+  t = bf2_to_f2(u.y); f[2] = t.x; f[3] = t.y;
+  t = bf2_to_f2(u.z); f[4] = t.x; f[5] = t.y;
+  t = bf2_to_f2(u.w); f[6] = t.x; f[7] = t.y;
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  u.x = f2_to_bf2(f[0], f[1]);
+  u.y = f2_to_bf2(f[2], f[3]);
+  u.z = f2_to_bf2(f[4], f[5]);
+  u.w = f2_to_bf2(f[6], f[7]);
+  return u;
+}
+// streaming 16-byte load that does not allocate in L1
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+}  // namespace
+}  // namespace ted

@@ -21,28 +21,34 @@ def _port():
     return p
 
 
-def _run(nproc, *args):
+def _run(nproc, *args, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(HERE, "mgpu_layer_check.py"), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, **(env or {})))
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "MGPU-OK" in r.stdout, r.stdout[-4000:]
     return r.stdout
 
 
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
 @pytest.mark.parametrize("tp,ep,dtd", [(2, 1, 1), (2, 1, 0), (1, 2, 0)])
-def test_two_gpus(tp, ep, dtd):
+def test_two_gpus(tp, ep, dtd, exchange):
+    """exchange=peer: NVLink peer-memory scatter/pull kernels; nccl: grouped send/recv."""
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    _run(2, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd))
+    _run(2, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd),
+         env={"TED_EXCHANGE": exchange})
 
 
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
 @pytest.mark.parametrize("tp,ep,dtd,E", [(2, 2, 1, 8), (2, 2, 0, 8), (1, 4, 0, 16), (2, 1, 1, 4)])
-def test_four_gpus(tp, ep, dtd, E):
+def test_four_gpus(tp, ep, dtd, E, exchange):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
-    _run(4, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd), "--experts", str(E))
+    _run(4, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd), "--experts", str(E),
+         env={"TED_EXCHANGE": exchange})
 
 
 def test_four_gpus_corrupt_drop_is_detected():
