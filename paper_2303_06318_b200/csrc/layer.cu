@@ -579,15 +579,15 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   const bf16* fh;
   const double nglob = double(L->n) * L->P * L->D;
   if (L->direct) {
-    L->mark("tp_allreduce_fwd", s);
-    if (L->T > 1 && L->plan.asm_rows > 0)
-      NC(ncclAllReduce(L->fe_asm.p, L->fe_asm.p, size_t(L->plan.asm_rows) * h, ncclBfloat16,
-                       ncclSum, L->tp_c, s));
     L->mark("barrier", s);
     plane_barrier(L, s);
-    // return trip + DTD home gather + combine: pull each token's row from its expert rank
+    // return trip + DTD home gather + TP reduction (row-parallel GEMM2 partial sums,
+    // parallel_linear.cpp:28) + combine: every token pulls and sums its expert's T partial
+    // rows straight from the replicas' buffers
     L->mark("combine_pull", s);
-    check(combine_pull(pull_src(L, 2), L->prob.p, L->n, h, y, L->fhome.p, L->loss_part.p, s),
+    RowSrc src = pull_src(L, 2);
+    src.nsum = L->T;
+    check(combine_pull(src, L->prob.p, L->n, h, y, L->fhome.p, L->loss_part.p, s),
           "combine_pull");
     check(loss_finalize(L->loss_part.p, L->nblk, 1.0 / (2.0 * nglob), L->loss.p, s), "loss");
     L->mark("_end", s);
@@ -818,16 +818,14 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   }
   const bf16* dxh;
   if (L->direct) {
-    L->mark("tp_allreduce_bwd", s);
-    if (L->T > 1 && L->plan.asm_rows > 0)  // parallel_linear.cpp:19
-      NC(ncclAllReduce(dx_asm, dx_asm, size_t(L->plan.asm_rows) * h, ncclBfloat16, ncclSum,
-                       L->tp_c, s));
     L->mark("barrier", s);
     plane_barrier(L, s);
     L->mark("gate_dx", s);
-    // return trip of dX pulled from the expert ranks + da = dX + dl Wg^T (moe.cpp:660-685)
-    check(gate_backward_input(pull_src(L, 3), L->dlogits.p, L->fam_non.param.p, L->n, h, E, da,
-                              s),
+    // return trip of dX pulled from the expert ranks, TP partial sums of the
+    // column-parallel dgrad folded in (parallel_linear.cpp:19), + dl Wg^T (moe.cpp:660-685)
+    RowSrc src = pull_src(L, 3);
+    src.nsum = L->T;
+    check(gate_backward_input(src, L->dlogits.p, L->fam_non.param.p, L->n, h, E, da, s),
           "gate_backward_input");
     L->mark("_end", s);
     return;

@@ -544,7 +544,8 @@ __global__ void __launch_bounds__(kThreads) combine_bwd_kernel(
 }
 
 // ------------------------------------------------------------------ gate backward
-__device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h) {
+// replica `rep` (0 .. R.nsum-1) of token k's expert-side row, or nullptr if dropped
+__device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h, int rep = 0) {
   const int ph = R.pos_home ? R.pos_home[k] : -1;
   if (ph < 0) return nullptr;
   if (R.peers == nullptr) return R.local + int64_t(ph) * h;
@@ -555,7 +556,8 @@ __device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h
     if (c >= R.Tc) c = R.Tc - 1;
   }
   const int64_t r = int64_t(ph) - R.home_base[c * R.E + e];
-  const bf16* base = reinterpret_cast<const bf16*>(R.peers[R.my_t + R.Tp * (e / R.Eloc)]);
+  const int tr = R.nsum > 1 ? rep : R.my_t;
+  const bf16* base = reinterpret_cast<const bf16*>(R.peers[tr + R.Tp * (e / R.Eloc)]);
   return base + (R.pull_base[c * R.E + e] + r) * h;
 }
 
@@ -579,14 +581,17 @@ __global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
       if (k >= n) break;
       const float d0 = lane < E ? dl[k * E + lane] : 0.f;
       const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
-      const bf16* row = src_row(R, k, h);
+      const bf16* row = src_row(R, k, h, 0);
       const bf16* src = row ? row + c0 : nullptr;
+      const bf16* row1 = R.nsum > 1 && row ? src_row(R, k, h, 1) : nullptr;
+      const bf16* src1 = row1 ? row1 + c0 : nullptr;
       for (int base = lane * 8; base < hc; base += 256 * 4) {
-        uint4 xv[4];
+        uint4 xv[4], xv1[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i0 = base + u * 256;
           xv[u] = (src && i0 < hc) ? ldg_stream(src + i0) : make_uint4(0, 0, 0, 0);
+          xv1[u] = (src1 && i0 < hc) ? ldg_stream(src1 + i0) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -594,6 +599,17 @@ __global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
           if (i0 >= hc) continue;
           float acc[8];
           unpack8(xv[u], acc);
+          if (src1) {  // TP partial sums of the column-parallel dgrad (parallel_linear.cpp:19)
+            float p1[8];
+            unpack8(xv1[u], p1);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] += p1[q];
+            for (int rep = 2; rep < R.nsum; ++rep) {
+              unpack8(ldg_stream(src_row(R, k, h, rep) + c0 + i0), p1);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[q] += p1[q];
+            }
+          }
 #pragma unroll
           for (int j = 0; j < EMAX; ++j) {
             const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);

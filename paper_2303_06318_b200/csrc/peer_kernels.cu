@@ -5,11 +5,13 @@
 //   dispatch (moe.cpp:454-493):  every kept row of this rank's DTD chunk is stored
 //       straight into its expert's assembled buffer on replica my_t -- or, with DTD, on
 //       every TP replica (the all-gather folded into the scatter: one source per row).
-//   return + combine (moe.cpp:504-563): each token pulls its expert output row from the
-//       expert rank's (TP-reduced) buffer and scales it by p; the row is also kept in a
-//       token-ordered local copy for the backward (dchosen = <f_home, dy>).
+//   return + combine (moe.cpp:504-563): each token pulls its expert's output row from
+//       every TP replica and sums the partials in fp32 -- the row-parallel all-reduce
+//       (parallel_linear.cpp:28) folded into the consumer -- then scales by p; the row is
+//       also kept in a token-ordered local copy for the backward (dchosen = <f_home, dy>).
 //   backward dispatch (moe.cpp:603-632): p * dy rows stored into the experts' dFe buffers
-//       exactly like the forward dispatch; the return of dX is a pull in gate backward.
+//       exactly like the forward dispatch; the return of dX (with the column-parallel
+//       dgrad's TP partial sums, parallel_linear.cpp:19) is a pull in gate backward.
 // Ordering across ranks is provided by stream-ordered NCCL barriers in layer.cu; every
 // writer kernel ends with a system-scope fence.
 #include <cuda_bf16.h>
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) scatter_peer_kernel(const bf16* __re
   __threadfence_system();
 }
 
-__device__ __forceinline__ const bf16* pull_row(const RowSrc& R, int64_t k, int h) {
+__device__ __forceinline__ const bf16* pull_row(const RowSrc& R, int64_t k, int h, int rep) {
   const int ph = R.pos_home[k];
   if (ph < 0) return nullptr;
   const int e = R.expert[k];
@@ -93,7 +95,8 @@ __device__ __forceinline__ const bf16* pull_row(const RowSrc& R, int64_t k, int 
     if (c >= R.Tc) c = R.Tc - 1;
   }
   const int64_t r = int64_t(ph) - R.home_base[c * R.E + e];
-  const bf16* base = reinterpret_cast<const bf16*>(R.peers[R.my_t + R.Tp * (e / R.Eloc)]);
+  const int tr = R.nsum > 1 ? rep : R.my_t;
+  const bf16* base = reinterpret_cast<const bf16*>(R.peers[tr + R.Tp * (e / R.Eloc)]);
   return base + (R.pull_base[c * R.E + e] + r) * h;
 }
 
@@ -111,25 +114,41 @@ __global__ void __launch_bounds__(kThreads) combine_pull_kernel(RowSrc R,
   for (int t = 0; t < kWarpTok; ++t) {
     const int64_t k = tok0 + t;
     if (k >= n) break;
-    const bf16* src = pull_row(R, k, h);
+    const bf16* src = pull_row(R, k, h, 0);
+    // row-parallel GEMM2: sum the TP partial rows here instead of an all-reduce
+    const bf16* src1 = (R.nsum > 1 && src) ? pull_row(R, k, h, 1) : nullptr;
     const float pk = prob[k];
     uint4* yd = reinterpret_cast<uint4*>(y + k * h);
     uint4* fd = reinterpret_cast<uint4*>(fhome + k * h);
     for (int base = lane; base < vec; base += 32 * 4) {
-      uint4 v[4];
+      uint4 v[4], v1[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = base + u * 32;
         v[u] = make_uint4(0, 0, 0, 0);
+        v1[u] = make_uint4(0, 0, 0, 0);
         if (i < vec && src) v[u] = ldg_stream(reinterpret_cast<const uint4*>(src) + i);
+        if (i < vec && src1) v1[u] = ldg_stream(reinterpret_cast<const uint4*>(src1) + i);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = base + u * 32;
         if (i >= vec) continue;
-        fd[i] = v[u];
         float f[8];
         unpack8(v[u], f);
+        if (src1) {
+          float g[8];
+          unpack8(v1[u], g);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) f[q] += g[q];
+          for (int rep = 2; rep < R.nsum; ++rep) {
+            unpack8(ldg_stream(reinterpret_cast<const uint4*>(pull_row(R, k, h, rep)) + i), g);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) f[q] += g[q];
+          }
+          v[u] = pack8(f);
+        }
+        fd[i] = v[u];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           f[q] *= pk;

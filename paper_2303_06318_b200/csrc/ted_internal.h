@@ -112,6 +112,9 @@ struct RowSrc {
   const int* expert = nullptr;
   int64_t chunk_len = 0;
   int Tc = 1, E = 1, Eloc = 1, Tp = 1, my_t = 0;
+  // 1: read replica my_t (already TP-reduced);  Tp: sum the row over every TP replica
+  // (the row-parallel all-reduce of parallel_linear.cpp:28 folded into the consumer)
+  int nsum = 1;
 };
 // da[k] = row(k) + sum_j dlogits[k][j] Wg[:, j]
 cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const bf16* wg,
