@@ -153,19 +153,22 @@ __global__ void __launch_bounds__(kThreads) gate_fwd_kernel(const bf16* __restri
       float acc[TPW * EMAX];
 #pragma unroll
       for (int i = 0; i < TPW * EMAX; ++i) acc[i] = 0.f;
+      // next slice's loads are issued before the current slice's FMAs
+      uint4 nx[TPW];
+      auto load_slice = [&](int i0, uint4 (&dst)[TPW]) {
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          const int64_t k = tok0 + warp * kWarpTok + tg + t;
+          dst[t] = (k < n && i0 < hc) ? ldg_stream(a + k * h + c0 + i0) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      load_slice(lane * 8, nx);
 #pragma unroll 1
       for (int i0 = lane * 8; i0 < hc; i0 += 256) {
         float av[TPW][8];
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          const int64_t k = tok0 + warp * kWarpTok + tg + t;
-          if (k < n) {
-            unpack8(ldg_stream(a + k * h + c0 + i0), av[t]);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) av[t][q] = 0.f;
-          }
-        }
+        for (int t = 0; t < TPW; ++t) unpack8(nx[t], av[t]);
+        load_slice(i0 + 256, nx);
 #pragma unroll
         for (int j = 0; j < EMAX; ++j) {
           float wv[8];
@@ -625,7 +628,7 @@ __global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
   }
 }
 
-constexpr int kDwTok = 64;  // tokens per dWg partial
+constexpr int kDwTok = 32;  // tokens per dWg partial
 
 // dWg partials: thread owns CPT consecutive columns for all EMAX experts.
 template <int EMAX, int CPT>
@@ -648,29 +651,41 @@ __global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict
 #pragma unroll
     for (int j = 0; j < EMAX; ++j) acc[c][j] = 0.f;
   const int tn = int(lmin(kDwTok, n - k0));
-#pragma unroll 4
-  for (int t = 0; t < tn; ++t) {
-    float x[CPT];
-    const bf16* src = a + (k0 + t) * h + i0;
-    if constexpr (CPT == 8) {
-      float f[8];
-      unpack8(ldg_stream(src), f);
+  // 8 token rows in flight per thread: loads first, then the FMAs
+  for (int t0 = 0; t0 < tn; t0 += 8) {
+    float xb[8][CPT];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) x[c] = f[c];
-    } else if constexpr (CPT == 4) {
-      const uint2 u = *reinterpret_cast<const uint2*>(src);
-      const float2 f0 = bf2_to_f2(u.x), f1 = bf2_to_f2(u.y);
-      x[0] = f0.x; x[1] = f0.y; x[2] = f1.x; x[3] = f1.y;
-    } else if constexpr (CPT == 2) {
-      const float2 f0 = bf2_to_f2(*reinterpret_cast<const uint32_t*>(src));
-      x[0] = f0.x; x[1] = f0.y;
-    } else {
-      x[0] = __bfloat162float(src[0]);
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u;
+      const bf16* src = a + (k0 + t) * h + i0;
+      if (t >= tn) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) xb[u][c] = 0.f;
+      } else if constexpr (CPT == 8) {
+        float f[8];
+        unpack8(ldg_stream(src), f);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xb[u][c] = f[c];
+      } else if constexpr (CPT == 4) {
+        const uint2 uu = *reinterpret_cast<const uint2*>(src);
+        const float2 f0 = bf2_to_f2(uu.x), f1 = bf2_to_f2(uu.y);
+        xb[u][0] = f0.x; xb[u][1] = f0.y; xb[u][2] = f1.x; xb[u][3] = f1.y;
+      } else if constexpr (CPT == 2) {
+        const float2 f0 = bf2_to_f2(*reinterpret_cast<const uint32_t*>(src));
+        xb[u][0] = f0.x; xb[u][1] = f0.y;
+      } else {
+        xb[u][0] = __bfloat162float(src[0]);
+      }
     }
 #pragma unroll
-    for (int c = 0; c < CPT; ++c)
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u >= tn) break;
 #pragma unroll
-      for (int j = 0; j < EMAX; ++j) acc[c][j] = fmaf(x[c], s_dl[t * EMAX + j], acc[c][j]);
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int j = 0; j < EMAX; ++j)
+          acc[c][j] = fmaf(xb[u][c], s_dl[(t0 + u) * EMAX + j], acc[c][j]);
+    }
   }
   float* out = part + (int64_t(blockIdx.x) * h + i0) * E;
 #pragma unroll
@@ -721,7 +736,7 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restri
 }
 
 // ------------------------------------------------------------------ bias-grad column sums
-constexpr int kColRows = 64;  // rows per partial
+constexpr int kColRows = 32;  // rows per partial
 
 // thread = 8 columns (one 16 B vector per row), block = 128 threads = 1024 columns
 __global__ void __launch_bounds__(128) colsum_part_kernel(const bf16* __restrict__ D, int64_t ld,
@@ -735,12 +750,12 @@ __global__ void __launch_bounds__(128) colsum_part_kernel(const bf16* __restrict
   if (col >= w || r0 >= r1) return;
   float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    uint4 v[4];
+  for (; r + 8 <= r1; r += 8) {
+    uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = ldg_stream(D + (r + u) * ld + col);
+    for (int u = 0; u < 8; ++u) v[u] = ldg_stream(D + (r + u) * ld + col);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       float f[8];
       unpack8(v[u], f);
 #pragma unroll

@@ -22,11 +22,14 @@ def _port():
 
 
 def _run(nproc, *args, env=None):
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-           os.path.join(HERE, "mgpu_layer_check.py"), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                       env=dict(os.environ, **(env or {})))
+    for _attempt in range(3):  # a freshly probed port can be taken before torchrun binds it
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               os.path.join(HERE, "mgpu_layer_check.py"), *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env=dict(os.environ, **(env or {})))
+        if "EADDRINUSE" not in r.stderr + r.stdout:
+            break
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "MGPU-OK" in r.stdout, r.stdout[-4000:]
     return r.stdout
