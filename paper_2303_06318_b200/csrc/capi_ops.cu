@@ -252,7 +252,8 @@ int ted_adam_step(float* master, float* m1, float* m2, uint16_t* param, const ui
                       reinterpret_cast<const bf16*>(grad), begin, end, tile, float(adam->lr),
                       float(adam->beta1), float(adam->beta2), float(1.0 - adam->beta1),
                       float(1.0 - adam->beta2), float(adam->eps),
-                      float(adam->weight_decay), float(1.0 / c1), float(1.0 / c2), S(stream)),
+                      float(adam->weight_decay), float(1.0 / c1), float(1.0 / c2), nullptr,
+                      S(stream)),
             "adam_step");
   });
 }

@@ -92,6 +92,8 @@ struct Family {
   int64_t chunk = 0;  // completion all-gather chunk
   DevBuf<bf16> param, grad, gather;
   DevBuf<float> master, m1, m2;
+  DevBuf<long long> dstep;  // steps_done on the device (graph-safe)
+  DevBuf<float> dcoef;      // {1/(1-b1^steps), 1/(1-b2^steps)}
   int64_t steps = 0;
   bool reset = false;
   uint64_t upcast_peak = 0;
@@ -164,7 +166,18 @@ struct ted_layer {
   cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr, ev_fork = nullptr,
               ev_join = nullptr;
   bool overlap_opt = false, exp_done_on_side = false;
-  double side_c1 = 1.0, side_c2 = 1.0;  // bias corrections of the in-flight side step
+
+  // CUDA graph of the whole single-rank training step (ted_layer_step): the step has no
+  // host synchronisation, so it is captured once and replayed (removes ~45 launches and
+  // 24 tensor-map encodes of host work per step).
+  bool use_graph = true, capturing = false;
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    const void *a = nullptr, *y = nullptr, *da = nullptr;
+    unsigned long long launches = 0;
+    std::vector<cudaEvent_t> evs;  // timing event nodes (timed graph only)
+    std::vector<const char*> names;
+  } g_plain, g_timed;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
   size_t side_used = 0;
 
@@ -190,7 +203,7 @@ struct ted_layer {
   }
   // interval on the side stream: call with begin=true before, false after the work
   void side_mark(bool begin, cudaStream_t s) {
-    if (!timing) return;
+    if (!timing || capturing) return;
     if (begin) {
       if (side_used == side_evs.size()) {
         cudaEvent_t a, b;
@@ -205,6 +218,10 @@ struct ted_layer {
     }
   }
 };
+
+namespace {
+void graph_reset(ted_layer::Graph& g);
+}
 
 namespace ted {
 thread_local std::string g_err;
@@ -339,6 +356,9 @@ void setup_family(ted_layer* L, Family& F, int64_t elems, ncclComm_t dp, int gro
   F.m2.alloc(owned + 4);
   F.m2.zero();
   if (F.group > 1) F.gather.alloc(size_t(F.chunk) * F.group + 8);
+  F.dstep.alloc(1);
+  F.dstep.zero();
+  F.dcoef.alloc(2);
 }
 
 // --------------------------------------------------------------- NCCL helpers
@@ -622,17 +642,21 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
 
 namespace {
 
-// reset (set_param) + step count + bias corrections for one family step, on stream s
-void family_begin(ted_layer* L, Family& F, cudaStream_t s, double& c1, double& c2) {
-  if (F.reset) {
-    CU(cudaMemsetAsync(F.m1.p, 0, sizeof(float) * F.m1.n, s));
-    CU(cudaMemsetAsync(F.m2.p, 0, sizeof(float) * F.m2.n, s));
-    F.steps = 0;
-    F.reset = false;
-  }
-  F.steps += 1;
-  c1 = 1.0 - std::pow(L->adam.beta1, double(F.steps));
-  c2 = 1.0 - std::pow(L->adam.beta2, double(F.steps));
+// set_param resets the family's optimizer state (reset_master, optimizer.cpp:46-56)
+void family_reset_if_needed(Family& F, cudaStream_t s) {
+  if (!F.reset) return;
+  CU(cudaMemsetAsync(F.m1.p, 0, sizeof(float) * F.m1.n, s));
+  CU(cudaMemsetAsync(F.m2.p, 0, sizeof(float) * F.m2.n, s));
+  CU(cudaMemsetAsync(F.dstep.p, 0, sizeof(long long), s));
+  F.steps = 0;
+  F.reset = false;
+}
+
+// steps_done += 1 and the bias corrections, both on the device (optimizer.cpp:68-70)
+void family_begin(ted_layer* L, Family& F, cudaStream_t s) {
+  family_reset_if_needed(F, s);
+  if (!L->capturing) F.steps += 1;  // host mirror (replays add it themselves)
+  check(adam_prep(F.dstep.p, F.dcoef.p, L->adam.beta1, L->adam.beta2, s), "adam_prep");
 }
 
 // AdamW of one tensor kind of every local expert (W1+b1 or W2+b2, contiguous per expert)
@@ -642,9 +666,7 @@ void side_adam(ted_layer* L, cudaEvent_t ready, int64_t off, int64_t len, cudaSt
   Family& F = L->fam_exp;
   CU(cudaEventRecord(ready, s));
   CU(cudaStreamWaitEvent(L->side, ready, 0));
-  double& c1 = L->side_c1;
-  double& c2 = L->side_c2;
-  if (first) family_begin(L, F, L->side, c1, c2);
+  if (first) family_begin(L, F, L->side);
   const int64_t owned = F.end - F.begin;
   const int64_t one = std::max<int64_t>(owned, 1);
   const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
@@ -654,8 +676,8 @@ void side_adam(ted_layer* L, cudaEvent_t ready, int64_t off, int64_t len, cudaSt
   check(adam_segments(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, L->Eloc, L->per_expert,
                       off, len, float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
                       float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2),
-                      float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
-                      float(1.0 / c2), sm_count(), L->side),
+                      float(L->adam.eps), float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p,
+                      sm_count(), L->side),
         "adam_segments");
   L->side_mark(false, L->side);
 }
@@ -859,16 +881,15 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
 // --------------------------------------------------------------- optimizer
 void family_step(ted_layer* L, Family& F, cudaStream_t s) {
   if (F.elems == 0) return;
-  double c1, c2;
-  family_begin(L, F, s, c1, c2);
+  family_begin(L, F, s);
   const int64_t owned = F.end - F.begin;
   const int64_t one = std::max<int64_t>(owned, 1);
   const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
   F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
   check(adam_step(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, F.begin, F.end, tile,
                   float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
-                  float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps), float(L->adam.weight_decay), float(1.0 / c1),
-                  float(1.0 / c2), s),
+                  float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps),
+                  float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p, s),
         "adam_step");
   if (F.group > 1) {  // ZeRO-1 completion (moe.cpp:718-732), zero-padded equal chunks
     bf16* gbuf = F.gather.p;
@@ -1085,6 +1106,10 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     L->dx_home.alloc(size_t(n) * h);
   }
   if (L->direct) setup_peer_exchange(L);
+  {
+    const char* gv = std::getenv("TED_GRAPH");
+    L->use_graph = !(gv && std::strcmp(gv, "0") == 0);
+  }
   if (L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 && (L->off_w2 % 4) == 0) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1137,6 +1162,8 @@ int ted_layer_create(const ted_model_cfg* model, const ted_topo_cfg* topo,
 void ted_layer_destroy(ted_layer* L) {
   if (!L) return;
   cudaDeviceSynchronize();
+  graph_reset(L->g_plain);
+  graph_reset(L->g_timed);
   for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
   for (auto& pr : L->side_evs) {
     cudaEventDestroy(pr.first);
@@ -1251,6 +1278,71 @@ int ted_layer_optimizer_step(ted_layer* L, void* stream) {
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// forward + synthetic loss + backward (AdamW overlapped) + optimizer on stream ms
+void step_body(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, cudaStream_t ms) {
+  layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), ms);
+  L->overlap_opt = L->hs != nullptr;  // the optimizer follows: overlap it with the backward
+  try {
+    layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), ms);
+  } catch (...) {
+    L->overlap_opt = false;
+    throw;
+  }
+  L->overlap_opt = false;
+  layer_optimizer(L, ms);
+}
+
+void graph_reset(ted_layer::Graph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (cudaEvent_t e : g.evs) cudaEventDestroy(e);
+  g = ted_layer::Graph{};
+}
+
+// Capture the single-rank step once per (a, y, da); timing variants carry event nodes.
+void graph_capture(ted_layer* L, ted_layer::Graph& g, const uint16_t* a, uint16_t* y,
+                   uint16_t* da) {
+  graph_reset(g);
+  const size_t ev0 = L->ev_used;
+  const unsigned long long before = launches();
+  L->capturing = true;
+  CU(cudaStreamBeginCapture(L->hs, cudaStreamCaptureModeThreadLocal));
+  try {
+    step_body(L, a, y, da, L->hs);
+  } catch (...) {
+    cudaGraph_t broken = nullptr;
+    cudaStreamEndCapture(L->hs, &broken);
+    if (broken) cudaGraphDestroy(broken);
+    L->capturing = false;
+    throw;
+  }
+  cudaGraph_t graph = nullptr;
+  CU(cudaStreamEndCapture(L->hs, &graph));
+  L->capturing = false;
+  cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CU(e);
+  g.launches = launches() - before;
+  count_launch(-int(g.launches));  // counted again on every replay
+  if (L->timing) {  // the graph owns these event nodes now
+    g.evs.assign(L->evs.begin() + ev0, L->evs.begin() + L->ev_used);
+    g.names.assign(L->ev_names.begin() + ev0, L->ev_names.begin() + L->ev_used);
+    L->evs.resize(ev0);
+    L->ev_names.resize(ev0);
+    L->ev_used = ev0;
+  }
+  g.a = a;
+  g.y = y;
+  g.da = da;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, void* stream) {
   return guard([&] {
     require(L && a && y && da, "null argument");
@@ -1261,16 +1353,32 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
       CU(cudaStreamWaitEvent(L->hs, L->ev_fork, 0));
       ms = L->hs;
     }
-    layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), ms);
-    L->overlap_opt = L->hs != nullptr;  // the optimizer follows: overlap it with the backward
-    try {
-      layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), ms);
-    } catch (...) {
-      L->overlap_opt = false;
-      throw;
+    if (L->local && L->hs && L->use_graph) {
+      family_reset_if_needed(L->fam_non, ms);  // set_param resets stay outside the graph
+      family_reset_if_needed(L->fam_exp, ms);
+      ted_layer::Graph& g = L->timing ? L->g_timed : L->g_plain;
+      if (!g.exec || g.a != a || g.y != y || g.da != da) graph_capture(L, g, a, y, da);
+      CU(cudaGraphLaunch(g.exec, L->hs));
+      count_launch(int(g.launches));
+      L->fam_non.steps += 1;
+      L->fam_exp.steps += 1;
+      L->have_forward = true;
+      L->last_a = reinterpret_cast<const bf16*>(a);
+      L->last_y = reinterpret_cast<const bf16*>(y);
+      if (L->timing) {  // read this replay's event nodes
+        CU(cudaStreamSynchronize(L->hs));
+        for (size_t i = 0; i + 1 < g.evs.size(); ++i) {
+          const char* nm = g.names[i];
+          if (!nm || nm[0] == '_') continue;
+          float ms_ = 0.f;
+          CU(cudaEventElapsedTime(&ms_, g.evs[i], g.evs[i + 1]));
+          L->stage_ms[nm] += ms_;
+          L->stage_cnt[nm] += 1;
+        }
+      }
+    } else {
+      step_body(L, a, y, da, ms);
     }
-    L->overlap_opt = false;
-    layer_optimizer(L, ms);
     if (L->hs) {  // join back into the caller's stream
       CU(cudaEventRecord(L->ev_join, L->hs));
       CU(cudaStreamWaitEvent(cs, L->ev_join, 0));

@@ -781,8 +781,13 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ master,
                                                    const bf16* __restrict__ grad, int64_t begin,
                                                    int64_t len, float lr, float b1, float b2,
                                                    float omb1, float omb2, float eps, float wd,
-                                                   float inv_c1, float inv_c2) {
+                                                   float inv_c1, float inv_c2,
+                                                   const float* __restrict__ coef) {
   // master/m1/m2 are indexed over the owned range; param/grad over the whole family.
+  if (coef) {
+    inv_c1 = coef[0];
+    inv_c2 = coef[1];
+  }
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
     const float g = __bfloat162float(grad[begin + i]);
@@ -806,7 +811,11 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
                                                       int64_t begin, int64_t len4, float lr,
                                                       float b1, float b2, float omb1, float omb2,
                                                       float eps, float wd, float inv_c1,
-                                                      float inv_c2) {
+                                                      float inv_c2, const float* __restrict__ coef) {
+  if (coef) {
+    inv_c1 = coef[0];
+    inv_c2 = coef[1];
+  }
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len4; i += stride) {
     const uint2 gu = reinterpret_cast<const uint2*>(grad + begin)[i];
@@ -842,7 +851,11 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
     float* __restrict__ master, float* __restrict__ m1, float* __restrict__ m2,
     bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride4,
     int64_t seg_off4, int64_t seg_len4, float lr, float b1, float b2, float omb1, float omb2,
-    float eps, float wd, float inv_c1, float inv_c2) {
+    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef) {
+  if (coef) {
+    inv_c1 = coef[0];
+    inv_c2 = coef[1];
+  }
   constexpr int U = 4;  // independent 4-element vectors in flight per thread
   const int64_t total = int64_t(nseg) * seg_len4;
   // short-lived CTAs (U*256 vectors each) so a concurrently launched persistent GEMM on a
@@ -889,6 +902,15 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
       reinterpret_cast<uint2*>(param)[idx[u]] = po;
     }
   }
+}
+
+// steps_done += 1 and the bias corrections 1 / (1 - beta^steps_done) on the device, so a
+// captured CUDA graph of the training step stays correct on every replay.
+__global__ void adam_prep_kernel(long long* step, float* coef, double b1, double b2) {
+  const long long st = *step + 1;
+  *step = st;
+  coef[0] = float(1.0 / (1.0 - pow(b1, double(st))));
+  coef[1] = float(1.0 / (1.0 - pow(b2, double(st))));
 }
 
 __global__ void expert_hist_kernel(const int* __restrict__ expert, int64_t n, int E,
@@ -1138,10 +1160,17 @@ cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const fl
   return cudaGetLastError();
 }
 
+cudaError_t adam_prep(long long* step, float* coef, double b1, double b2, cudaStream_t s) {
+  adam_prep_kernel<<<1, 1, 0, s>>>(step, coef, b1, b2);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                           int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
                           float b1, float b2, float omb1, float omb2, float eps, float wd,
-                          float inv_c1, float inv_c2, int grid, cudaStream_t s) {
+                          float inv_c1, float inv_c2, const float* coef, int grid,
+                          cudaStream_t s) {
   if (seg_stride % 4 || seg_off % 4 || seg_len % 4 || nseg < 1) return cudaErrorInvalidValue;
   if (seg_len == 0) return cudaSuccess;
   (void)grid;
@@ -1149,7 +1178,7 @@ cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, cons
   const int ctas = int((items + 256 * 4 - 1) / (256 * 4));
   adam_segments_kernel<<<ctas, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
                                             seg_off / 4, seg_len / 4, lr, b1, b2, omb1, omb2,
-                                            eps, wd, inv_c1, inv_c2);
+                                            eps, wd, inv_c1, inv_c2, coef);
   count_launch(1);
   return cudaGetLastError();
 }
@@ -1157,7 +1186,7 @@ cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, cons
 cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                       int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
                       float omb1, float omb2, float eps, float wd, float inv_c1, float inv_c2,
-                      cudaStream_t s) {
+                      const float* coef, cudaStream_t s) {
   (void)tile;  // the tile only bounds the reference's up-cast buffer; none exists here
   const int64_t len = end - begin;
   if (len <= 0) return cudaSuccess;
@@ -1170,10 +1199,10 @@ cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf
                   (reinterpret_cast<uintptr_t>(grad) % 8 == 0);
   if (v4)
     adam_kernel_v4<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len / 4, lr, b1, b2,
-                                        omb1, omb2, eps, wd, inv_c1, inv_c2);
+                                        omb1, omb2, eps, wd, inv_c1, inv_c2, coef);
   else
     adam_kernel<<<grid, 256, 0, s>>>(master, m1, m2, param, grad, begin, len, lr, b1, b2, omb1,
-                                     omb2, eps, wd, inv_c1, inv_c2);
+                                     omb2, eps, wd, inv_c1, inv_c2, coef);
   count_launch(1);
   return cudaGetLastError();
 }

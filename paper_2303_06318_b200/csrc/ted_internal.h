@@ -164,12 +164,16 @@ cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const fl
 cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                       int64_t begin, int64_t end, int64_t tile, float lr, float b1, float b2,
                       float omb1, float omb2, float eps, float wd, float inv_c1, float inv_c2,
-                      cudaStream_t s);
+                      const float* coef, cudaStream_t s);
+// device-side step counter += 1 and coef = {1/(1-b1^step), 1/(1-b2^step)} (graph-safe);
+// a non-null coef passed to the Adam launchers overrides inv_c1 / inv_c2.
+cudaError_t adam_prep(long long* step, float* coef, double b1, double b2, cudaStream_t s);
 
 // AdamW over nseg equal, equally strided segments of an unsharded family (side stream).
 cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                           int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
                           float b1, float b2, float omb1, float omb2, float eps, float wd,
-                          float inv_c1, float inv_c2, int grid, cudaStream_t s);
+                          float inv_c1, float inv_c2, const float* coef, int grid,
+                          cudaStream_t s);
 
 }  // namespace ted
