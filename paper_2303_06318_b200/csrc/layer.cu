@@ -177,7 +177,7 @@ struct ted_layer {
     unsigned long long launches = 0;
     std::vector<cudaEvent_t> evs;  // timing event nodes (timed graph only)
     std::vector<const char*> names;
-  } g_plain, g_timed;
+  } g_plain;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
   size_t side_used = 0;
 
@@ -1163,7 +1163,6 @@ void ted_layer_destroy(ted_layer* L) {
   if (!L) return;
   cudaDeviceSynchronize();
   graph_reset(L->g_plain);
-  graph_reset(L->g_timed);
   for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
   for (auto& pr : L->side_evs) {
     cudaEventDestroy(pr.first);
@@ -1302,7 +1301,7 @@ void graph_reset(ted_layer::Graph& g) {
   g = ted_layer::Graph{};
 }
 
-// Capture the single-rank step once per (a, y, da); timing variants carry event nodes.
+// Capture the single-rank step once per (a, y, da).
 void graph_capture(ted_layer* L, ted_layer::Graph& g, const uint16_t* a, uint16_t* y,
                    uint16_t* da) {
   graph_reset(g);
@@ -1327,13 +1326,7 @@ void graph_capture(ted_layer* L, ted_layer::Graph& g, const uint16_t* a, uint16_
   CU(e);
   g.launches = launches() - before;
   count_launch(-int(g.launches));  // counted again on every replay
-  if (L->timing) {  // the graph owns these event nodes now
-    g.evs.assign(L->evs.begin() + ev0, L->evs.begin() + L->ev_used);
-    g.names.assign(L->ev_names.begin() + ev0, L->ev_names.begin() + L->ev_used);
-    L->evs.resize(ev0);
-    L->ev_names.resize(ev0);
-    L->ev_used = ev0;
-  }
+  (void)ev0;
   g.a = a;
   g.y = y;
   g.da = da;
@@ -1353,10 +1346,12 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
       CU(cudaStreamWaitEvent(L->hs, L->ev_fork, 0));
       ms = L->hs;
     }
-    if (L->local && L->hs && L->use_graph) {
+    // stage timing runs eagerly (event pairs around every stage; the host enqueues faster
+    // than the GPU drains, so the intervals are kernel time)
+    if (L->local && L->hs && L->use_graph && !L->timing) {
       family_reset_if_needed(L->fam_non, ms);  // set_param resets stay outside the graph
       family_reset_if_needed(L->fam_exp, ms);
-      ted_layer::Graph& g = L->timing ? L->g_timed : L->g_plain;
+      ted_layer::Graph& g = L->g_plain;
       if (!g.exec || g.a != a || g.y != y || g.da != da) graph_capture(L, g, a, y, da);
       CU(cudaGraphLaunch(g.exec, L->hs));
       count_launch(int(g.launches));
@@ -1365,17 +1360,6 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
       L->have_forward = true;
       L->last_a = reinterpret_cast<const bf16*>(a);
       L->last_y = reinterpret_cast<const bf16*>(y);
-      if (L->timing) {  // read this replay's event nodes
-        CU(cudaStreamSynchronize(L->hs));
-        for (size_t i = 0; i + 1 < g.evs.size(); ++i) {
-          const char* nm = g.names[i];
-          if (!nm || nm[0] == '_') continue;
-          float ms_ = 0.f;
-          CU(cudaEventElapsedTime(&ms_, g.evs[i], g.evs[i + 1]));
-          L->stage_ms[nm] += ms_;
-          L->stage_cnt[nm] += 1;
-        }
-      }
     } else {
       step_body(L, a, y, da, ms);
     }
