@@ -43,11 +43,16 @@ constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + 8 epilog
 constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
 constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
 
+constexpr int F32_BLOCK_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging block (AdamW state)
+
 template <int EPI>
 struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : 4;
-  static constexpr size_t STAGING = size_t(EPI_WARPS) * NOUT * EPI_BLOCK_BYTES;
+  // the fused-AdamW epilogue is HBM-bound: 2 stages leave room for 3 fp32 blocks per warp
+  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : (EPI == EPI_ADAM ? 2 : 4);
+  static constexpr size_t PER_WARP =
+      EPI == EPI_ADAM ? 3 * F32_BLOCK_BYTES + EPI_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
+  static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
 };
@@ -115,7 +120,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
-                        const __grid_constant__ CUtensorMap tmAux, const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tmAux,
+                        const __grid_constant__ CUtensorMap tmMaster,
+                        const __grid_constant__ CUtensorMap tmM1,
+                        const __grid_constant__ CUtensorMap tmM2, const GemmParams p) {
   using CF = Cfg<EPI>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -153,6 +161,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmC);
     if (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU) ptx::prefetch_tmap(&tmAux);
+    if (EPI == EPI_ADAM) {
+      ptx::prefetch_tmap(&tmMaster);
+      ptx::prefetch_tmap(&tmM1);
+      ptx::prefetch_tmap(&tmM2);
+    }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -261,8 +274,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;
     const int sp = ew & 3;      // TMEM sub-partition: lanes 32*(warp%4)..+31
     const int chalf = ew >> 2;  // column half of the 256-wide tile
-    uint8_t* blk0 = sEpi + size_t(ew) * CF::NOUT * EPI_BLOCK_BYTES;
+    uint8_t* blk0 = sEpi + size_t(ew) * CF::PER_WARP;
     uint8_t* blk1 = blk0 + EPI_BLOCK_BYTES;  // H (bias+GELU only)
+    // AdamW state blocks (EPI_ADAM): master, m1, m2 fp32 after the bf16 parameter block
+    uint8_t* fblk = blk0 + EPI_BLOCK_BYTES;
+    float inv_c1 = 1.f, inv_c2 = 1.f;
+    if (EPI == EPI_ADAM) {
+      inv_c1 = p.adam_coef[0];
+      inv_c2 = p.adam_coef[1];
+    }
     int acc = 0;
     uint32_t acc_phase = 0, zphase = 0;
     TileInfo ti;
@@ -310,6 +330,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
+        if (EPI == EPI_ADAM) {
+          // bring the 32x32 master / m / v blocks in by TMA (SWIZZLE_128B: 16 B chunk j of
+          // row r at j ^ (r & 7)), update in place, store them and the bf16 parameters back
+          if (lane == 0) {
+            ptx::mbar_arrive_expect_tx(&zbar[ew], 3 * F32_BLOCK_BYTES);
+            ptx::tma_load_3d(fblk, &tmMaster, &zbar[ew], col, row0, gz);
+            ptx::tma_load_3d(fblk + F32_BLOCK_BYTES, &tmM1, &zbar[ew], col, row0, gz);
+            ptx::tma_load_3d(fblk + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[ew], col, row0, gz);
+          }
+          ptx::mbar_wait(&zbar[ew], zphase);
+          zphase ^= 1;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int off = lane * 128 + ((j ^ (lane & 7)) << 4);
+            float4* pm = reinterpret_cast<float4*>(fblk + off);
+            float4* p1 = reinterpret_cast<float4*>(fblk + F32_BLOCK_BYTES + off);
+            float4* p2 = reinterpret_cast<float4*>(fblk + 2 * F32_BLOCK_BYTES + off);
+            float4 mm = *pm, a1 = *p1, a2 = *p2;
+            float* mq = &mm.x;
+            float* q1 = &a1.x;
+            float* q2 = &a2.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              // the gradient as the unfused path stores it (bf16), optimizer.cpp:91-100
+              const float g = __bfloat162float(__float2bfloat16(v[4 * j + q]));
+              q1[q] = p.b1 * q1[q] + p.omb1 * g;
+              q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
+              mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) + p.wd * mq[q]);
+              v[4 * j + q] = mq[q];  // the new parameter value goes to C below
+            }
+            *pm = mm;
+            *p1 = a1;
+            *p2 = a2;
+          }
+        }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
             const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride + col;
@@ -351,6 +406,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           ptx::tma_store_3d(&tmC, blk0, col, row0, gz);
           if (EPI == EPI_BIAS_GELU) ptx::tma_store_3d(&tmAux, blk1, col, row0, gz);
+          if (EPI == EPI_ADAM) {
+            ptx::tma_store_3d(&tmMaster, fblk, col, row0, gz);
+            ptx::tma_store_3d(&tmM1, fblk + F32_BLOCK_BYTES, col, row0, gz);
+            ptx::tma_store_3d(&tmM2, fblk + 2 * F32_BLOCK_BYTES, col, row0, gz);
+          }
           ptx::bulk_commit();
         }
       }
@@ -386,13 +446,14 @@ bool get_encoder() {
 // 3-D bf16 tensor map: dims {d0 (contiguous), d1, d2}, byte strides {s1, s2}, box {b0, b1, 1}.
 bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
               uint64_t s1, uint64_t s2, uint32_t b0, uint32_t b1,
-              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+              CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B,
+              CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   if (!get_encoder()) return false;
   cuuint64_t dims[3] = {d0, d1, d2 == 0 ? 1 : d2};
   cuuint64_t strides[2] = {s1, s2 == 0 ? s1 * d1 : s2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+  CUresult r = g_encode(m, dt, 3, const_cast<void*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -400,7 +461,8 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
 
 template <bool A_MN, bool B_MN, int EPI>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                     const CUtensorMap& mx, const GemmParams& p, int grid, cudaStream_t s) {
+                     const CUtensorMap& mx, const CUtensorMap& m0, const CUtensorMap& m1,
+                     const CUtensorMap& m2, const GemmParams& p, int grid, cudaStream_t s) {
   auto k = grouped_gemm_kernel<A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -409,7 +471,7 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k<<<grid, NUM_THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, p);
+  k<<<grid, NUM_THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
   count_launch(1);
   return cudaGetLastError();
 }
@@ -447,12 +509,15 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   } else {
     if (!o.a_mn || !o.b_mn) return fail("gemm: KDIM mode needs MN-major A and B");
     if (p.M % BM != 0) return fail("gemm: M must be a multiple of 128");
-    if (p.epi != EPI_STORE) return fail("gemm: KDIM mode supports the plain store epilogue");
+    if (p.epi != EPI_STORE && p.epi != EPI_ADAM)
+      return fail("gemm: KDIM mode supports the store and AdamW epilogues");
+    if (p.epi == EPI_ADAM && !(p.adam_master && p.adam_m1 && p.adam_m2 && p.adam_coef))
+      return fail("gemm: AdamW epilogue needs master / m1 / m2 / coef");
   }
   if ((p.epi == EPI_BIAS_GELU || p.epi == EPI_DGELU) && p.aux == nullptr)
     return fail("gemm: epilogue needs the aux tensor");
   const uint64_t rows = uint64_t(max_rows > 0 ? max_rows : 1);
-  CUtensorMap ma, mb, mc, mx;
+  CUtensorMap ma, mb, mc, mx, f0, f1, f2;
   bool ok;
   const auto SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
   if (p.mode == GEMM_ROWS) {
@@ -470,21 +535,31 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
          make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2,
                   (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 2, 32, 32, SW64);
     mx = mc;
+    if (p.epi == EPI_ADAM) {
+      const uint64_t gs = (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 4;
+      const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+      const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B;
+      ok = ok && make_map(&f0, p.adam_master, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32) &&
+           make_map(&f1, p.adam_m1, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32) &&
+           make_map(&f2, p.adam_m2, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32);
+    }
   }
+  if (p.epi != EPI_ADAM) f0 = f1 = f2 = mc;
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
   if (p.mode == GEMM_ROWS) {
     if (o.b_mn) {
       if (p.epi == EPI_BIAS_GELU)
-        return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, mc, mx, p, grid, s);
-      if (p.epi == EPI_BIAS) return launch_t<false, true, EPI_BIAS>(ma, mb, mc, mx, p, grid, s);
-      return launch_t<false, true, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
+        return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      if (p.epi == EPI_BIAS) return launch_t<false, true, EPI_BIAS>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      return launch_t<false, true, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
     }
-    if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, mc, mx, p, grid, s);
-    if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, mc, mx, p, grid, s);
-    return launch_t<false, false, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
+    if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    return launch_t<false, false, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
   }
-  return launch_t<true, true, EPI_STORE>(ma, mb, mc, mx, p, grid, s);
+  if (p.epi == EPI_ADAM) return launch_t<true, true, EPI_ADAM>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+  return launch_t<true, true, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
 }
 
 }  // namespace ted

@@ -165,7 +165,8 @@ struct ted_layer {
   cudaStream_t hs = nullptr;    // highest priority: the step's main work in ted_layer_step
   cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr, ev_fork = nullptr,
               ev_join = nullptr;
-  bool overlap_opt = false, exp_done_on_side = false;
+  bool overlap_opt = false, exp_done_fused = false;
+  bool fuse_ok = false;  // expert family unsharded, no DP sync: AdamW may fuse into wgrad
 
   // CUDA graph of the whole single-rank training step (ted_layer_step): the step has no
   // host synchronisation, so it is captured once and replayed (removes ~45 launches and
@@ -659,27 +660,34 @@ void family_begin(ted_layer* L, Family& F, cudaStream_t s) {
   check(adam_prep(F.dstep.p, F.dcoef.p, L->adam.beta1, L->adam.beta2, s), "adam_prep");
 }
 
-// AdamW of one tensor kind of every local expert (W1+b1 or W2+b2, contiguous per expert)
-// on the side stream once the main stream has produced its final gradient.
-void side_adam(ted_layer* L, cudaEvent_t ready, int64_t off, int64_t len, cudaStream_t s,
-               bool first) {
+// AdamW over one bias kind (b1 or b2) of every local expert, after its column sum.
+void bias_adam(ted_layer* L, int64_t off, int64_t len, cudaStream_t s) {
   Family& F = L->fam_exp;
-  CU(cudaEventRecord(ready, s));
-  CU(cudaStreamWaitEvent(L->side, ready, 0));
-  if (first) family_begin(L, F, L->side);
-  const int64_t owned = F.end - F.begin;
-  const int64_t one = std::max<int64_t>(owned, 1);
-  const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
-  F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
-  L->side_mark(true, L->side);
-  // one CTA per SM: fits beside the persistent GEMM CTA (registers / threads)
   check(adam_segments(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, L->Eloc, L->per_expert,
                       off, len, float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
                       float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2),
                       float(L->adam.eps), float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p,
-                      sm_count(), L->side),
+                      sm_count(), s),
         "adam_segments");
-  L->side_mark(false, L->side);
+}
+
+// wgrad GEMM params for the fused-AdamW epilogue (the gradient tile updates the parameter
+// block in place; the bf16 parameter is the GEMM output)
+void set_adam_epilogue(ted_layer* L, GemmParams& g, int64_t off) {
+  Family& F = L->fam_exp;
+  g.epi = EPI_ADAM;
+  g.C = F.param.p + off;
+  g.adam_master = F.master.p + off;
+  g.adam_m1 = F.m1.p + off;
+  g.adam_m2 = F.m2.p + off;
+  g.adam_coef = F.dcoef.p;
+  g.lr = float(L->adam.lr);
+  g.b1 = float(L->adam.beta1);
+  g.b2 = float(L->adam.beta2);
+  g.omb1 = float(1.0 - L->adam.beta1);
+  g.omb2 = float(1.0 - L->adam.beta2);
+  g.eps = float(L->adam.eps);
+  g.wd = float(L->adam.weight_decay);
 }
 
 // --------------------------------------------------------------- backward
@@ -772,6 +780,13 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   g.C = G + L->off_w2;
   g.ldc = h;
   g.c_group_stride = L->per_expert;
+  // the optimizer follows this backward and the expert family needs no data-parallel sync:
+  // AdamW runs inside the wgrad epilogues (W2 is no longer read: dgrad2 ran before)
+  const bool fuse_adam = L->overlap_opt && L->fuse_ok;
+  if (fuse_adam) {
+    family_begin(L, L->fam_exp, s);
+    set_adam_epilogue(L, g, L->off_w2);
+  }
   o = GemmOperands{};
   o.A = L->hbuf.p;
   o.lda = L->fT;
@@ -785,9 +800,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   check(colsum_groups(L->dfe_asm.p, h, h, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
                       G + L->off_b2, L->per_expert, s),
         "colsum db2");
-  const bool side_opt = L->overlap_opt && L->side != nullptr;
-  if (side_opt)  // W2 and b2 are final: update them while dgrad1 / wgrad1 run
-    side_adam(L, L->ev_w2, L->off_w2, int64_t(L->fT) * h + h, s, true);
+  if (fuse_adam) bias_adam(L, L->off_b2, h, s);
   L->mark("dgrad1", s);
   // dgrad of GEMM1: dX = dZ W1^T  (column_parallel_backward :16)
   g = GemmParams{};
@@ -821,6 +834,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   g.C = G + L->off_w1;
   g.ldc = L->fT;
   g.c_group_stride = L->per_expert;
+  if (fuse_adam) set_adam_epilogue(L, g, L->off_w1);  // dgrad1 (reads W1) ran before
   o = GemmOperands{};
   o.A = L->x_asm.p;
   o.lda = h;
@@ -833,10 +847,9 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   check(colsum_groups(L->z.p, L->fT, L->fT, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
                       G + L->off_b1, L->per_expert, s),
         "colsum db1");
-  if (side_opt) {
-    side_adam(L, L->ev_w1, L->off_w1, int64_t(h) * L->fT + L->fT, s, false);
-    CU(cudaEventRecord(L->ev_side_done, L->side));
-    L->exp_done_on_side = true;
+  if (fuse_adam) {
+    bias_adam(L, L->off_b1, L->fT, s);
+    L->exp_done_fused = true;
   }
   const bf16* dxh;
   if (L->direct) {
@@ -918,9 +931,8 @@ void layer_optimizer(ted_layer* L, cudaStream_t s) {
                      ncclBfloat16, ncclSum, L->nonexpdp_c, s));
   L->mark("adam", s);
   family_step(L, L->fam_non, s);
-  if (L->exp_done_on_side) {  // already updated on the side stream: join it
-    CU(cudaStreamWaitEvent(s, L->ev_side_done, 0));
-    L->exp_done_on_side = false;
+  if (L->exp_done_fused) {  // already updated inside the backward's wgrad epilogues
+    L->exp_done_fused = false;
   } else {
     family_step(L, L->fam_exp, s);
   }
@@ -1110,7 +1122,9 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     const char* gv = std::getenv("TED_GRAPH");
     L->use_graph = !(gv && std::strcmp(gv, "0") == 0);
   }
-  if (L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 && (L->off_w2 % 4) == 0) {
+  L->fuse_ok = L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 &&
+               (L->off_w2 % 4) == 0 && (L->off_b1 % 4) == 0 && (L->off_b2 % 4) == 0;
+  if (L->fuse_ok) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     CU(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, least));

@@ -18,7 +18,7 @@ const char* last_error();
 
 // ------------------------------------------------------------------ grouped GEMM
 enum GemmMode { GEMM_ROWS = 0, GEMM_KDIM = 1 };
-enum EpiKind { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2, EPI_DGELU = 3 };
+enum EpiKind { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2, EPI_DGELU = 3, EPI_ADAM = 4 };
 
 struct GemmParams {
   int mode;  // GemmMode
@@ -33,6 +33,14 @@ struct GemmParams {
   int64_t bias_group_stride;
   bf16* aux;  // EPI_BIAS_GELU: H output; EPI_DGELU: Z input (may alias C)
   int64_t ld_aux;
+  // EPI_ADAM (KDIM only): the wgrad tile is the gradient of the parameter block at the
+  // same [g][row][col] of these arrays (all laid out like C); AdamW is applied in the
+  // epilogue and C (the bf16 gradient) is never written.  C is the bf16 parameter output.
+  float* adam_master = nullptr;
+  float* adam_m1 = nullptr;
+  float* adam_m2 = nullptr;
+  const float* adam_coef = nullptr;  // device {1/(1-b1^t), 1/(1-b2^t)}
+  float lr = 0.f, b1 = 0.f, b2 = 0.f, omb1 = 0.f, omb2 = 0.f, eps = 0.f, wd = 0.f;
 };
 
 struct GemmOperands {

@@ -128,3 +128,28 @@ def test_full_size_c2_sampled_tokens():
         assert rel_l2(yd[k], ref) < TOL
     assert np.isfinite(from_dev(da)).all()
     L.close()
+
+
+def test_fused_adam_step_matches_unfused_path():
+    """ted_layer_step fuses AdamW into the wgrad epilogues (and runs as a CUDA graph);
+    forward + backward + optimizer_step as separate calls use the standalone kernels.  Both
+    must give the same parameters (same gradient rounding, same update formula)."""
+    n, h, E = 1024, 256, 4
+    La, inp = _make(n, h, E, 1.25, 3)
+    Lb, _ = _make(n, h, E, 1.25, 3)
+    a = to_dev_bf16(inp["a"])
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    for _ in range(3):
+        La.step(a, y, da)
+        Lb.forward(a, y)
+        Lb.backward(None, da)
+        Lb.optimizer_step()
+    torch.cuda.synchronize()
+    for e in range(E):
+        for k in ("w1", "b1", "w2", "b2"):
+            pa = La.get_param(f"layer0.expert{e}.{k}")
+            pb = Lb.get_param(f"layer0.expert{e}.{k}")
+            assert rel_l2(pa, pb) < 1e-3, (e, k)
+    assert rel_l2(La.get_param("layer0.gate.w"), Lb.get_param("layer0.gate.w")) < 1e-3
+    La.close()
+    Lb.close()
