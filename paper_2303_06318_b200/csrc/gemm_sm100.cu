@@ -43,15 +43,17 @@ constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + 8 epilog
 constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
 constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
 
-constexpr int F32_BLOCK_BYTES = 32 * 32 * 4;  // one 32x32 fp32 staging block (AdamW state)
+// fused AdamW works on 32x16 half blocks: fp32 master/m/v (64 B rows, SWIZZLE_64B) and
+// the bf16 parameter (32 B rows, SWIZZLE_32B)
+constexpr int F32_BLOCK_BYTES = 32 * 16 * 4;
+constexpr int P16_BLOCK_BYTES = 32 * 16 * 2;
 
 template <int EPI>
 struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  // the fused-AdamW epilogue is HBM-bound: 2 stages leave room for 3 fp32 blocks per warp
-  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : (EPI == EPI_ADAM ? 2 : 4);
+  static constexpr int STAGES = EPI == EPI_BIAS_GELU || EPI == EPI_ADAM ? 3 : 4;
   static constexpr size_t PER_WARP =
-      EPI == EPI_ADAM ? 3 * F32_BLOCK_BYTES + EPI_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
+      EPI == EPI_ADAM ? 3 * F32_BLOCK_BYTES + 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -276,8 +278,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int chalf = ew >> 2;  // column half of the 256-wide tile
     uint8_t* blk0 = sEpi + size_t(ew) * CF::PER_WARP;
     uint8_t* blk1 = blk0 + EPI_BLOCK_BYTES;  // H (bias+GELU only)
-    // AdamW state blocks (EPI_ADAM): master, m1, m2 fp32 after the bf16 parameter block
-    uint8_t* fblk = blk0 + EPI_BLOCK_BYTES;
+    // AdamW half blocks (EPI_ADAM): master, m1, m2 fp32 (2 KB each), then the bf16 params
+    uint8_t* fblk = blk0;
+    uint8_t* pblk = blk0 + 3 * F32_BLOCK_BYTES;
     float inv_c1 = 1.f, inv_c2 = 1.f;
     if (EPI == EPI_ADAM) {
       inv_c1 = p.adam_coef[0];
@@ -331,39 +334,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         if (EPI == EPI_ADAM) {
-          // bring the 32x32 master / m / v blocks in by TMA (SWIZZLE_128B: 16 B chunk j of
-          // row r at j ^ (r & 7)), update in place, store them and the bf16 parameters back
-          if (lane == 0) {
-            ptx::mbar_arrive_expect_tx(&zbar[ew], 3 * F32_BLOCK_BYTES);
-            ptx::tma_load_3d(fblk, &tmMaster, &zbar[ew], col, row0, gz);
-            ptx::tma_load_3d(fblk + F32_BLOCK_BYTES, &tmM1, &zbar[ew], col, row0, gz);
-            ptx::tma_load_3d(fblk + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[ew], col, row0, gz);
-          }
-          ptx::mbar_wait(&zbar[ew], zphase);
-          zphase ^= 1;
+          // two 32x16 halves: TMA-load master/m/v, update in place, TMA-store them and the
+          // bf16 parameters (the bf16-rounded gradient is what the unfused path stores)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int off = lane * 128 + ((j ^ (lane & 7)) << 4);
-            float4* pm = reinterpret_cast<float4*>(fblk + off);
-            float4* p1 = reinterpret_cast<float4*>(fblk + F32_BLOCK_BYTES + off);
-            float4* p2 = reinterpret_cast<float4*>(fblk + 2 * F32_BLOCK_BYTES + off);
-            float4 mm = *pm, a1 = *p1, a2 = *p2;
-            float* mq = &mm.x;
-            float* q1 = &a1.x;
-            float* q2 = &a2.x;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              // the gradient as the unfused path stores it (bf16), optimizer.cpp:91-100
-              const float g = __bfloat162float(__float2bfloat16(v[4 * j + q]));
-              q1[q] = p.b1 * q1[q] + p.omb1 * g;
-              q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
-              mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) + p.wd * mq[q]);
-              v[4 * j + q] = mq[q];  // the new parameter value goes to C below
+          for (int hf = 0; hf < 2; ++hf) {
+            if (hf == 1) {
+              if (lane == 0) ptx::bulk_wait_read0();
+              __syncwarp();
             }
-            *pm = mm;
-            *p1 = a1;
-            *p2 = a2;
+            if (lane == 0) {
+              ptx::mbar_arrive_expect_tx(&zbar[ew], 3 * F32_BLOCK_BYTES);
+              ptx::tma_load_3d(fblk, &tmMaster, &zbar[ew], col + 16 * hf, row0, gz);
+              ptx::tma_load_3d(fblk + F32_BLOCK_BYTES, &tmM1, &zbar[ew], col + 16 * hf, row0, gz);
+              ptx::tma_load_3d(fblk + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[ew], col + 16 * hf, row0,
+                               gz);
+            }
+            ptx::mbar_wait(&zbar[ew], zphase);
+            zphase ^= 1;
+            float nv[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+              float4* pm = reinterpret_cast<float4*>(fblk + off);
+              float4* p1 = reinterpret_cast<float4*>(fblk + F32_BLOCK_BYTES + off);
+              float4* p2 = reinterpret_cast<float4*>(fblk + 2 * F32_BLOCK_BYTES + off);
+              float4 mm = *pm, a1 = *p1, a2 = *p2;
+              float* mq = &mm.x;
+              float* q1 = &a1.x;
+              float* q2 = &a2.x;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float g = __bfloat162float(__float2bfloat16(v[16 * hf + 4 * j + q]));
+                q1[q] = p.b1 * q1[q] + p.omb1 * g;
+                q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
+                mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
+                                 p.wd * mq[q]);
+                nv[4 * j + q] = mq[q];
+              }
+              *pm = mm;
+              *p1 = a1;
+              *p2 = a2;
+            }
+            // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              uint4 o;
+              o.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
+              o.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
+              o.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
+              o.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
+              *reinterpret_cast<uint4*>(pblk + hf * P16_BLOCK_BYTES + lane * 32 +
+                                        ((j ^ ((lane >> 2) & 1)) << 4)) = o;
+            }
+            ptx::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_3d(&tmMaster, fblk, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmM1, fblk + F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmM2, fblk + 2 * F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmC, pblk + hf * P16_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::bulk_commit();
+            }
           }
+          continue;  // parameters and state written; nothing else to stage
         }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
@@ -406,11 +439,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) {
           ptx::tma_store_3d(&tmC, blk0, col, row0, gz);
           if (EPI == EPI_BIAS_GELU) ptx::tma_store_3d(&tmAux, blk1, col, row0, gz);
-          if (EPI == EPI_ADAM) {
-            ptx::tma_store_3d(&tmMaster, fblk, col, row0, gz);
-            ptx::tma_store_3d(&tmM1, fblk + F32_BLOCK_BYTES, col, row0, gz);
-            ptx::tma_store_3d(&tmM2, fblk + 2 * F32_BLOCK_BYTES, col, row0, gz);
-          }
           ptx::bulk_commit();
         }
       }
@@ -538,10 +566,11 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
     if (p.epi == EPI_ADAM) {
       const uint64_t gs = (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 4;
       const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-      const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B;
-      ok = ok && make_map(&f0, p.adam_master, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32) &&
-           make_map(&f1, p.adam_m1, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32) &&
-           make_map(&f2, p.adam_m2, p.N, p.M, p.groups, p.ldc * 4, gs, 32, 32, SW128, F32);
+      ok = ok && make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2, gs / 2, 16, 32,
+                          CU_TENSOR_MAP_SWIZZLE_32B) &&
+           make_map(&f0, p.adam_master, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32) &&
+           make_map(&f1, p.adam_m1, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32) &&
+           make_map(&f2, p.adam_m2, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32);
     }
   }
   if (p.epi != EPI_ADAM) f0 = f1 = f2 = mc;
