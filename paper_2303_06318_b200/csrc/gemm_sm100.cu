@@ -334,6 +334,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         if (EPI == EPI_ADAM) {
+          // pull the next 32x32 block's optimizer state into L2 while this one is processed
+          if (lane == 0 && c0 + 32 < (chalf + 1) * (BN / 2)) {
+            ptx::tma_prefetch_3d(&tmMaster, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmMaster, col + 48, row0, gz);
+            ptx::tma_prefetch_3d(&tmM1, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmM1, col + 48, row0, gz);
+            ptx::tma_prefetch_3d(&tmM2, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmM2, col + 48, row0, gz);
+          }
           // two 32x16 halves: TMA-load master/m/v, update in place, TMA-store them and the
           // bf16 parameters (the bf16-rounded gradient is what the unfused path stores)
 #pragma unroll

@@ -60,6 +60,14 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// TMA prefetch of a tensor box into L2 (no smem, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+
 // TMA store (smem -> global), bulk-group completion tracking
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* smem_src, int x,
                                              int y, int z) {
