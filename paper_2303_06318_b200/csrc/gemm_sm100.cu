@@ -51,11 +51,9 @@ constexpr int P16_BLOCK_BYTES = 32 * 16 * 2;
 template <int EPI>
 struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  // the fused-AdamW wgrad is HBM-bound: its epilogue gets a double-buffered job ring and
-  // the (hidden) mainloop 2 stages
-  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : (EPI == EPI_ADAM ? 2 : 4);
+  static constexpr int STAGES = EPI == EPI_BIAS_GELU || EPI == EPI_ADAM ? 3 : 4;
   static constexpr size_t PER_WARP =
-      EPI == EPI_ADAM ? 2 * (3 * F32_BLOCK_BYTES + P16_BLOCK_BYTES) : NOUT * EPI_BLOCK_BYTES;
+      EPI == EPI_ADAM ? 3 * F32_BLOCK_BYTES + 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -140,8 +138,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* zbar = tempty + 2;  // per epilogue warp x 2 slots (dGELU Z / AdamW state loads)
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(zbar + 2 * EPI_WARPS);
+  uint64_t* zbar = tempty + 2;  // per epilogue warp (dGELU Z loads)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(zbar + EPI_WARPS);
   int* s_off = reinterpret_cast<int*>(smem + CF::BAR_OFF + 512);
   int* s_tstart = s_off + (MAX_GROUPS + 1);
 
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], EPI_WARPS);
     }
-    for (int w = 0; w < 2 * EPI_WARPS; ++w) ptx::mbar_init(&zbar[w], 1);
+    for (int w = 0; w < EPI_WARPS; ++w) ptx::mbar_init(&zbar[w], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
@@ -273,135 +271,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (EPI == EPI_ADAM && warp >= 4) {
-    // -------------------------------------------------------------- fused AdamW epilogue
-    // Each warp owns 32 rows x 128 columns of every tile = 8 jobs of 32x16.  A job TMA-loads
-    // the parameter block's fp32 master / m / v, applies AdamW with the bf16-rounded
-    // gradient (optimizer.cpp:91-100), and TMA-stores master / m / v and the bf16 parameter.
-    // Two smem slots per warp: job i+1's loads are in flight while job i is processed.
-    const int ew = warp - 4;
-    const int sp = ew & 3, chalf = ew >> 2;
-    constexpr int SLOT = 3 * F32_BLOCK_BYTES + P16_BLOCK_BYTES;
-    uint8_t* slots = sEpi + size_t(ew) * CF::PER_WARP;
-    const float inv_c1 = p.adam_coef[0], inv_c2 = p.adam_coef[1];
-    auto coords = [&](const TileInfo& tt, int jb, int& col, int& row, int& gz) {
-      col = tt.n_blk * BN + chalf * (BN / 2) + (jb >> 1) * 32 + (jb & 1) * 16;
-      row = tt.m_blk * BM + sp * 32;
-      gz = tt.g;
-    };
-    auto issue_loads = [&](int slot, int col, int row, int gz) {
-      uint8_t* b = slots + slot * SLOT;
-      ptx::mbar_arrive_expect_tx(&zbar[2 * ew + slot], 3 * F32_BLOCK_BYTES);
-      ptx::tma_load_3d(b, &tmMaster, &zbar[2 * ew + slot], col, row, gz);
-      ptx::tma_load_3d(b + F32_BLOCK_BYTES, &tmM1, &zbar[2 * ew + slot], col, row, gz);
-      ptx::tma_load_3d(b + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[2 * ew + slot], col, row, gz);
-    };
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    uint32_t zph0 = 0, zph1 = 0;
-    unsigned jglob = 0;
-    TileInfo ti;
-    int t = blockIdx.x;
-    if (decode_tile(p, s_off, s_tstart, total, t, ti) && lane == 0) {
-      int c_, r_, g_;
-      coords(ti, 0, c_, r_, g_);
-      issue_loads(0, c_, r_, g_);
-    }
-    for (; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
-      TileInfo tn;
-      const bool has_next = decode_tile(p, s_off, s_tstart, total, t + gridDim.x, tn);
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      const bool zero = ti.k_len == 0;
-      const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        ptx::tmem_ld32(tbase + chalf * (BN / 2) + c * 32, v);
-        if (zero) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-        }
-        if (c == 3) {  // accumulator fully read: release TMEM to the next tile's MMAs
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        }
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          const int jb = c * 2 + hf;
-          const int slot = int(jglob & 1);
-          // the other slot's previous stores must have read smem before it is refilled
-          if (lane == 0) ptx::bulk_wait_read0();
-          __syncwarp();
-          if (lane == 0) {
-            int c_, r_, g_;
-            if (jb < 7) {
-              coords(ti, jb + 1, c_, r_, g_);
-              issue_loads(slot ^ 1, c_, r_, g_);
-            } else if (has_next) {
-              coords(tn, 0, c_, r_, g_);
-              issue_loads(slot ^ 1, c_, r_, g_);
-            }
-          }
-          ptx::mbar_wait(&zbar[2 * ew + slot], slot ? zph1 : zph0);
-          if (slot) zph1 ^= 1;
-          else zph0 ^= 1;
-          uint8_t* b = slots + slot * SLOT;
-          uint8_t* pb = b + 3 * F32_BLOCK_BYTES;
-          float nv[16];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
-            float4* pm = reinterpret_cast<float4*>(b + off);
-            float4* p1 = reinterpret_cast<float4*>(b + F32_BLOCK_BYTES + off);
-            float4* p2 = reinterpret_cast<float4*>(b + 2 * F32_BLOCK_BYTES + off);
-            float4 mm = *pm, a1 = *p1, a2 = *p2;
-            float* mq = &mm.x;
-            float* q1 = &a1.x;
-            float* q2 = &a2.x;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float g = __bfloat162float(__float2bfloat16(v[16 * hf + 4 * j + q]));
-              q1[q] = p.b1 * q1[q] + p.omb1 * g;
-              q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
-              mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
-                               p.wd * mq[q]);
-              nv[4 * j + q] = mq[q];
-            }
-            *pm = mm;
-            *p1 = a1;
-            *p2 = a2;
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {  // bf16 params: 32 B rows, SWIZZLE_32B
-            uint4 o;
-            o.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
-            o.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
-            o.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
-            o.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
-            *reinterpret_cast<uint4*>(pb + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) = o;
-          }
-          ptx::fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            int c_, r_, g_;
-            coords(ti, jb, c_, r_, g_);
-            ptx::tma_store_3d(&tmMaster, b, c_, r_, g_);
-            ptx::tma_store_3d(&tmM1, b + F32_BLOCK_BYTES, c_, r_, g_);
-            ptx::tma_store_3d(&tmM2, b + 2 * F32_BLOCK_BYTES, c_, r_, g_);
-            ptx::tma_store_3d(&tmC, pb, c_, r_, g_);
-            ptx::bulk_commit();
-          }
-          ++jglob;
-        }
-      }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
-      }
-    }
-    if (lane == 0) ptx::bulk_wait0();
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
@@ -463,6 +332,80 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v[8 * j + 2 * q + 1] *= gelu_grad_f(f.y);
             }
           }
+        }
+        if (EPI == EPI_ADAM) {
+          // pull the next 32x32 block's optimizer state into L2 while this one is processed
+          if (lane == 0 && c0 + 32 < (chalf + 1) * (BN / 2)) {
+            ptx::tma_prefetch_3d(&tmMaster, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmMaster, col + 48, row0, gz);
+            ptx::tma_prefetch_3d(&tmM1, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmM1, col + 48, row0, gz);
+            ptx::tma_prefetch_3d(&tmM2, col + 32, row0, gz);
+            ptx::tma_prefetch_3d(&tmM2, col + 48, row0, gz);
+          }
+          // two 32x16 halves: TMA-load master/m/v, update in place, TMA-store them and the
+          // bf16 parameters (the bf16-rounded gradient is what the unfused path stores)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            if (hf == 1) {
+              if (lane == 0) ptx::bulk_wait_read0();
+              __syncwarp();
+            }
+            if (lane == 0) {
+              ptx::mbar_arrive_expect_tx(&zbar[ew], 3 * F32_BLOCK_BYTES);
+              ptx::tma_load_3d(fblk, &tmMaster, &zbar[ew], col + 16 * hf, row0, gz);
+              ptx::tma_load_3d(fblk + F32_BLOCK_BYTES, &tmM1, &zbar[ew], col + 16 * hf, row0, gz);
+              ptx::tma_load_3d(fblk + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[ew], col + 16 * hf, row0,
+                               gz);
+            }
+            ptx::mbar_wait(&zbar[ew], zphase);
+            zphase ^= 1;
+            float nv[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
+              float4* pm = reinterpret_cast<float4*>(fblk + off);
+              float4* p1 = reinterpret_cast<float4*>(fblk + F32_BLOCK_BYTES + off);
+              float4* p2 = reinterpret_cast<float4*>(fblk + 2 * F32_BLOCK_BYTES + off);
+              float4 mm = *pm, a1 = *p1, a2 = *p2;
+              float* mq = &mm.x;
+              float* q1 = &a1.x;
+              float* q2 = &a2.x;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float g = __bfloat162float(__float2bfloat16(v[16 * hf + 4 * j + q]));
+                q1[q] = p.b1 * q1[q] + p.omb1 * g;
+                q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
+                mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
+                                 p.wd * mq[q]);
+                nv[4 * j + q] = mq[q];
+              }
+              *pm = mm;
+              *p1 = a1;
+              *p2 = a2;
+            }
+            // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              uint4 o;
+              o.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
+              o.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
+              o.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
+              o.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
+              *reinterpret_cast<uint4*>(pblk + hf * P16_BLOCK_BYTES + lane * 32 +
+                                        ((j ^ ((lane >> 2) & 1)) << 4)) = o;
+            }
+            ptx::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_3d(&tmMaster, fblk, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmM1, fblk + F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmM2, fblk + 2 * F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::tma_store_3d(&tmC, pblk + hf * P16_BLOCK_BYTES, col + 16 * hf, row0, gz);
+              ptx::bulk_commit();
+            }
+          }
+          continue;  // parameters and state written; nothing else to stage
         }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
