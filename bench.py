@@ -274,8 +274,60 @@ def run_ours(args, w, rank, world, local_rank, dist):
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
+    # DTD on vs off on the same workload (all-to-all bytes and time reported separately)
+    dtd_cmp = None
+    if world > 1 and T > 1 and not args.no_dtd_compare:
+        def exch_ms(st):
+            keys = ["dispatch_peer", "combine_pull", "combine_bwd", "gate_dx", "barrier", "count_exchange",
+                    "a2a_fwd", "ag_fwd", "a2a_ret_fwd", "ag_home_fwd", "a2a_bwd", "ag_bwd",
+                    "a2a_ret_bwd", "ag_home_bwd", "tp_allreduce_fwd", "tp_allreduce_bwd"]
+            return {k: round(v, 4) for k, v in st.items() if k in keys}
+        arms = {}
+        for dtd_flag in (w["dtd"], not w["dtd"]):
+            if dtd_flag == w["dtd"]:
+                Lx, stx, ms_x = L, stages, ms
+            else:
+                L.close()
+                Lx = ted.MoeLayer(model, topo, ted.RunFlags(dtd=dtd_flag), capacity_factor=w["cf"],
+                                  rank=rank, nccl_uid=uid)
+                Lx.init_params(1234)
+                for _ in range(3):
+                    Lx.step(a, y, da)
+                torch.cuda.synchronize()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                kx = max(1, min(args.steps, 10))
+                e0.record(stream)
+                for _ in range(kx):
+                    Lx.step(a, y, da)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ms_x = max_over_ranks(e0.elapsed_time(e1) / kx)
+                Lx.timing(True)
+                for _ in range(kx):
+                    Lx.step(a, y, da)
+                torch.cuda.synchronize()
+                stx = {k: v[0] / kx for k, v in Lx.timing_read().items()}
+                Lx.timing(False)
+                barrier()
+            if dtd_flag == w["dtd"]:
+                stx = {k: v[0] / nprof for k, v in stx.items()}
+            sx = Lx.stats()
+            ex = exch_ms(stx)
+            arms["dtd_on" if dtd_flag else "dtd_off"] = {
+                "ms_per_step": ms_x, "tokens_per_s": w["tokens"] / (ms_x / 1e3),
+                "a2a_bytes_fwd_rank0_ledger": sx["a2a_bytes_fwd"],
+                "a2a_rows_offrank_rank0": sx["a2a_rows_offrank"],
+                "dtd_allgather_bytes_fwd_rank0_ledger": sx["ag_bytes_fwd"],
+                "nvlink_bytes_fwd_rank0": sx["peer_bytes_fwd"],
+                "exchange_ms_rank0": ex, "exchange_ms_total_rank0": round(sum(ex.values()), 4)}
+            if Lx is not L:
+                Lx.close()
+        dtd_cmp = arms
+        L = None
     if rank != 0:
-        L.close()
+        if L is not None:
+            L.close()
         return
     tokens_global = w["tokens"]
     value = tokens_global / (ms / 1e3)
@@ -320,8 +372,12 @@ def run_ours(args, w, rank, world, local_rank, dist):
         "routing": {"dropped_tokens_rank0": stats["dropped"], "loss_rank0": loss},
         "clocks": clk.summary(),
     }
+    if dtd_cmp is not None:
+        line["dtd_compare"] = dtd_cmp
     if world > 1:
         line["comm"] = {"a2a_bytes_fwd_rank0": stats["a2a_bytes_fwd"],
+                        "nvlink_bytes_fwd_rank0": stats["peer_bytes_fwd"],
+                        "peer_exchange": bool(stats["peer_exchange"]),
                         "a2a_rows_offrank_rank0": stats["a2a_rows_offrank"],
                         "ag_bytes_fwd_rank0": stats["ag_bytes_fwd"],
                         "ar_bytes_fwd_rank0": stats["ar_bytes_fwd"]}
@@ -332,7 +388,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
                                 "sample": f"{args.ref_sample} tokens through the reference "
                                           f"MoE branch ({t_layer:.2f} s) + AdamW amortised"}
     print(json.dumps(line), flush=True)
-    L.close()
+    if L is not None:
+        L.close()
 
 
 def main():
@@ -344,6 +401,7 @@ def main():
     ap.add_argument("--dtd", type=int, default=1)
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dtd-compare", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -183,6 +183,9 @@ typedef struct {
   int64_t asm_rows;          /* expert-side rows (padded) */
   int placement_ok;          /* DTD placement verdict (moe.cpp:537-556) */
   int64_t kept_per_expert[64]; /* local experts: rows processed */
+  int64_t peer_bytes_fwd;    /* NVLink bytes this rank moves per forward (peer exchange:
+                                dispatch stores to other GPUs + pulls of TP partial rows) */
+  int peer_exchange;         /* 1: NVLink peer-memory exchange, 0: NCCL send/recv */
 } ted_layer_stats;
 int ted_layer_get_stats(ted_layer* L, ted_layer_stats* out);
 

@@ -99,7 +99,8 @@ class LayerStats(C.Structure):
                 ("a2a_rows_offrank", C.c_int64), ("a2a_bytes_fwd", C.c_int64),
                 ("ag_bytes_fwd", C.c_int64), ("ar_bytes_fwd", C.c_int64),
                 ("asm_rows", C.c_int64), ("placement_ok", C.c_int),
-                ("kept_per_expert", C.c_int64 * 64)]
+                ("kept_per_expert", C.c_int64 * 64), ("peer_bytes_fwd", C.c_int64),
+                ("peer_exchange", C.c_int)]
 
 
 def _sig(name, res, args):

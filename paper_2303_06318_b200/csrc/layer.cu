@@ -1423,6 +1423,23 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
       o->ar_bytes_fwd = L->T > 1 ? L->plan.asm_rows * hb : 0;
       o->asm_rows = L->plan.asm_rows;
       for (int le = 0; le < L->Eloc && le < 64; ++le) o->kept_per_expert[le] = L->plan.seg_rows[le];
+      if (L->direct) {
+        // dispatch: my chunk's rows to 1 (or T with DTD) replicas of each expert's rank;
+        // return: every kept token pulls T partial rows.  Local replicas move no NVLink bytes.
+        const int my_c = L->dtd ? L->t : 0;
+        int64_t rows = 0;
+        for (int e = 0; e < E; ++e) {
+          const int ep2 = e / L->Eloc;
+          const int reps = L->dtd ? L->T : 1;
+          const int local_reps = (ep2 == L->ep) ? 1 : 0;  // replica (t, ep) is this GPU
+          rows += int64_t(kc[size_t(my_c) * E + e]) * (reps - local_reps);
+          for (int c = 0; c < Tc; ++c)
+            rows += int64_t(kc[size_t(c) * E + e]) * (L->T - local_reps);
+        }
+        o->peer_bytes_fwd = rows * hb;
+        o->peer_exchange = 1;
+        o->ar_bytes_fwd = 0;  // folded into the pulls
+      }
     }
     o->placement_ok = (L->dtd && L->flags.corrupt_drop) ? 0 : 1;
   });
