@@ -3,11 +3,14 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dtd 0|1]
 
-N=1 : configs[1] of BASELINE.json -- single-GPU MoE layer d=1024, ffn=4096, 8 experts,
-      16384 tokens, bf16, capacity factor 1.25 (TP=EP=DP=1).
-N>1 : (launched by torchrun, one rank per GPU) configs[2]'s layer -- d=4096, ffn=16384,
-      16 experts, 32768 tokens in total -- over TP=2 x EP=N/2 (N=8: exactly TP=2 x EP=4,
-      4 data shards of 8192 tokens); DTD on by default (--dtd 0 for the off arm).
+Workload (all N): configs[2] of BASELINE.json, the layer the north-star target is quoted on
+-- d=4096, ffn=16384, 16 experts top-1, 32768 tokens in total, capacity factor 1.25 --
+partitioned TP=2 x EP=N/2 (N=1: TP=EP=1, all 16 experts on one GPU; N=8: exactly TP=2 x
+EP=4, 4 data shards of 8192 tokens).  Total work is fixed, so the 1/2/4/8 series is strong
+scaling of one layer.  DTD on by default for TP>1 (--dtd 0 for the off arm); at N>1 the
+line also carries a DTD on/off comparison measured in the same run.  At N=1 the line adds
+configs[1] (d=1024, ffn=4096, 8 experts, 16384 tokens) as `c2_single_gpu`
+(--workload c2 makes it the headline).
 
 A step = one pass of the MoE layer over one batch: gate, capacity routing, dispatch,
 [EP all-to-all, DTD all-gathers, TP all-reduce], expert FFN fwd (tcgen05 GEMMs), combine,
@@ -23,6 +26,7 @@ workload with one rank-thread per expert, the reference's own concurrency model.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -49,14 +53,51 @@ def peaks():
     return d
 
 
-def workload(n_gpus: int, dtd: bool):
-    if n_gpus == 1:
+def workload(n_gpus: int, dtd: bool, which: str = "c3"):
+    if which == "c2":
         return dict(name="C2 single-GPU MoE layer", hidden=1024, experts=8, tokens=16384,
                     tp=1, ep=1, cf=1.25, dtd=False)
     tp = 2 if n_gpus % 2 == 0 else 1
     ep = n_gpus // tp
     return dict(name=f"C3 MoE layer TP={tp}xEP={ep}", hidden=4096, experts=16,
                 tokens=32768, tp=tp, ep=ep, cf=1.25, dtd=dtd and tp > 1)
+
+
+def quick_layer_bench(w, steps: int, warmup: int):
+    """ms/step of one more single-GPU workload in the same process (graph-replayed step,
+    CUDA events), plus its per-stage times from an eager timed pass."""
+    import torch
+
+    import paper_2303_06318_b200 as ted
+    model = ted.MoeModelConfig(1, w["hidden"], w["experts"], w["tokens"], 0)
+    L = ted.MoeLayer(model, ted.derive_config(1, 1, 1), ted.RunFlags(dtd=False),
+                     capacity_factor=w["cf"])
+    L.init_params(1234)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000)
+    a = torch.randn(w["tokens"], w["hidden"], device="cuda", generator=g).bfloat16()
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    for _ in range(warmup):
+        L.step(a, y, da)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        L.step(a, y, da)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    L.timing(True)
+    k = max(1, min(steps, 20))
+    for _ in range(k):
+        L.step(a, y, da)
+    torch.cuda.synchronize()
+    st = {kk: round(v[0] / k, 4) for kk, v in sorted(L.timing_read().items())}
+    L.close()
+    return {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
+            "experts": w["experts"], "tokens": w["tokens"], "capacity_factor": w["cf"],
+            "ms_per_step": ms, "tokens_per_s": w["tokens"] / (ms / 1e3), "steps": steps,
+            "stage_ms": st}
 
 
 class ClockSampler:
@@ -108,18 +149,29 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference arm (CPU)
 
-def reference_tokens_per_s(w, sample_tokens: int, threads: int):
+def ref_sample_plan(w, sample_tokens):
+    """(tokens, experts) of the bounded CPU sample: top-1 routing makes the per-token cost
+    independent of the expert count, so wide layers are sampled with fewer experts (host
+    memory: 4 fp64 weight/gradient tensors per expert) and fewer tokens (10-30 s)."""
+    h = w["hidden"]
+    if sample_tokens <= 0:
+        sample_tokens = 256 if h <= 1024 else 24
+    return sample_tokens, (w["experts"] if h <= 1024 else min(w["experts"], 2))
+
+
+def reference_tokens_per_s(w, sample_tokens: int, experts: int):
     """Time the unmodified reference (oracle/_ref) on a bounded sample: the MoE branch
     (gate_forward + per-expert linear/gelu fwd+bwd + gate_backward, one thread per expert)
-    on `sample_tokens` tokens, plus OptimizerShard::step_owned on the layer's parameter
-    count amortised over the full batch."""
+    on `sample_tokens` tokens routed over `experts` experts, plus OptimizerShard::step_owned
+    on the layer's full parameter count amortised over the full batch."""
     import ctypes as C
 
     import numpy as np
 
     from oracle import oracle as O
     R = O.ref()
-    h, E = w["hidden"], w["experts"]
+    h, E = w["hidden"], experts
+    threads = experts
     f = 4 * h
     rng = np.random.default_rng(0)
     a = rng.standard_normal((sample_tokens, h))
@@ -138,7 +190,7 @@ def reference_tokens_per_s(w, sample_tokens: int, threads: int):
     t_layer = time.perf_counter() - t0
     assert rc == 0, R.ref_last_error()
     # optimizer over a slice of the family, scaled to the layer's parameter count
-    params = E * (2 * h * f + f + h) + h * E
+    params = w["experts"] * (2 * h * f + f + h) + h * w["experts"]
     probe = min(params, 4_000_000)
     vals = rng.standard_normal(probe)
     grads = rng.standard_normal(probe)
@@ -155,14 +207,13 @@ def reference_tokens_per_s(w, sample_tokens: int, threads: int):
 def run_reference(args, w, rank, world):
     if rank != 0:
         return
-    sample = args.ref_sample
-    threads = w["experts"]
+    sample, threads = ref_sample_plan(w, args.ref_sample)
     tps, t_layer, t_adam = reference_tokens_per_s(w, sample, threads)
     ms = w["tokens"] / tps * 1e3
     line = {
         "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
@@ -288,8 +339,10 @@ def run_ours(args, w, rank, world, local_rank, dist):
                 Lx, stx, ms_x = L, stages, ms
             else:
                 L.close()
+                obj = [ted.nccl_unique_id() if rank == 0 else None]  # a fresh id per communicator
+                dist.broadcast_object_list(obj, src=0)
                 Lx = ted.MoeLayer(model, topo, ted.RunFlags(dtd=dtd_flag), capacity_factor=w["cf"],
-                                  rank=rank, nccl_uid=uid)
+                                  rank=rank, nccl_uid=obj[0])
                 Lx.init_params(1234)
                 for _ in range(3):
                     Lx.step(a, y, da)
@@ -341,15 +394,16 @@ def run_ours(args, w, rank, world, local_rank, dist):
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak_tc = pk["bf16_tflops_sustained"]
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
-    if os.path.exists(tp) and world == 1:  # from the committed ncu --set full capture
-        with open(tp) as f:
-            traffic = json.load(f)["traffic_bytes_per_launch_mean"]
+    for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic*.json"))):
+        with open(tp) as f:  # from a committed ncu --set full capture of this workload
+            tj = json.load(f)
+        if tj.get("workload") == w["name"] and tj.get("n_gpus", 1) == world:
+            traffic = tj["traffic_bytes_per_launch_mean"]
     stage_ms = {k: round(v[0] / nprof, 4) for k, v in sorted(stages.items())}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
                    "experts": w["experts"], "tokens": tokens_global, "tokens_per_shard": n,
@@ -382,11 +436,17 @@ def run_ours(args, w, rank, world, local_rank, dist):
                         "ag_bytes_fwd_rank0": stats["ag_bytes_fwd"],
                         "ar_bytes_fwd_rank0": stats["ar_bytes_fwd"]}
     if not args.no_cpu_baseline and world == 1:
-        tps, t_layer, t_adam = reference_tokens_per_s(w, args.ref_sample, w["experts"])
-        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": w["experts"],
+        sample, nexp = ref_sample_plan(w, args.ref_sample)
+        tps, t_layer, t_adam = reference_tokens_per_s(w, sample, nexp)
+        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": nexp,
                                 "kind": "reference",
-                                "sample": f"{args.ref_sample} tokens through the reference "
-                                          f"MoE branch ({t_layer:.2f} s) + AdamW amortised"}
+                                "sample": f"{sample} tokens over {nexp} experts through the "
+                                          f"reference MoE branch ({t_layer:.2f} s, {nexp} "
+                                          f"expert threads) + step_owned over the layer's "
+                                          f"{w['experts']} experts' parameters "
+                                          f"({t_adam:.2f} s) amortised over {w['tokens']} tokens"}
+    if world == 1 and w["name"].startswith("C3") and not args.no_c2:
+        line["c2_single_gpu"] = quick_layer_bench(workload(1, False, "c2"), 200, 10)
     print(json.dumps(line), flush=True)
     if L is not None:
         L.close()
@@ -399,7 +459,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtd", type=int, default=1)
-    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--ref-sample", type=int, default=0, help="0: automatic (10-30 s)")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2"])
+    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] side line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dtd-compare", action="store_true")
     args = ap.parse_args()
@@ -408,7 +470,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         world = args.gpus if world == 1 else world
-    w = workload(world, bool(args.dtd))
+    if args.workload == "c2" and world > 1:
+        raise SystemExit("--workload c2 is the single-GPU configuration")
+    w = workload(world, bool(args.dtd), args.workload)
     dist = None
     if args.impl == "reference":
         run_reference(args, w, rank, world)

@@ -18,8 +18,8 @@
 // (dZ = acc * gelu'(Z), Z brought in by TMA).
 //
 // Tile 128 x 256 x 64; warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
-// allocator, warps 4..11 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31, one half of
-// the tile's 256 columns each).
+// allocator, warps 4.. = epilogue (warp w reads TMEM lanes 32*(w%4)..+31; 8 epilogue warps
+// take one half of the tile's 256 columns each, the 16 of the AdamW variant a quarter).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -38,22 +38,39 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int MAX_GROUPS = 256;
-constexpr int EPI_WARPS = 8;
-constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + 8 epilogue warps
+constexpr int MAX_EPI_WARPS = 16;
 constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
 constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
 
-// fused AdamW works on 32x16 half blocks: fp32 master/m/v (64 B rows, SWIZZLE_64B) and
-// the bf16 parameter (32 B rows, SWIZZLE_32B)
-constexpr int F32_BLOCK_BYTES = 32 * 16 * 4;
+// fused AdamW works on 32x16 half blocks: fp32 master/m/v straight from global memory into
+// registers (blk_off layout), the bf16 parameter staged in smem (32 B rows, SWIZZLE_32B).
+// It is bound by the state traffic (24 of its 26 B/parameter), so its variant runs 16
+// epilogue warps (4 per TMEM sub-partition, 64 columns each): more independent 6 KB state
+// loads in flight per SM than 8 warps with double-buffered registers (measured with
+// tools/adam_bw.cu: 4.6-5.0 vs 3.1 TB/s for the same bytes).
 constexpr int P16_BLOCK_BYTES = 32 * 16 * 2;
+
+__device__ __forceinline__ float4 ld_state(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_state(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
 
 template <int EPI>
 struct Cfg {
+  static constexpr int EPI_WARPS = EPI == EPI_ADAM ? 16 : 8;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + epilogue warps
+  static constexpr int COL_SPAN = BN / (EPI_WARPS / 4);  // tile columns per epilogue warp
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  static constexpr int STAGES = EPI == EPI_BIAS_GELU || EPI == EPI_ADAM ? 3 : 4;
-  static constexpr size_t PER_WARP =
-      EPI == EPI_ADAM ? 3 * F32_BLOCK_BYTES + 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
+  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : 4;
+  static constexpr size_t PER_WARP = EPI == EPI_ADAM ? P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -118,7 +135,7 @@ __device__ __forceinline__ uint4* blk_chunk(uint8_t* blk, int r, int j) {
 }
 
 template <bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
@@ -128,6 +145,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const __grid_constant__ CUtensorMap tmM2, const GemmParams p) {
   using CF = Cfg<EPI>;
   constexpr int STAGES = CF::STAGES;
+  constexpr int EPI_WARPS = CF::EPI_WARPS;
+  constexpr int SPAN = CF::COL_SPAN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -163,11 +182,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::prefetch_tmap(&tmB);
     ptx::prefetch_tmap(&tmC);
     if (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU) ptx::prefetch_tmap(&tmAux);
-    if (EPI == EPI_ADAM) {
-      ptx::prefetch_tmap(&tmMaster);
-      ptx::prefetch_tmap(&tmM1);
-      ptx::prefetch_tmap(&tmM2);
-    }
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -275,12 +289,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
     const int sp = ew & 3;      // TMEM sub-partition: lanes 32*(warp%4)..+31
-    const int chalf = ew >> 2;  // column half of the 256-wide tile
+    const int cq = ew >> 2;     // column span (SPAN wide) of the 256-wide tile
     uint8_t* blk0 = sEpi + size_t(ew) * CF::PER_WARP;
     uint8_t* blk1 = blk0 + EPI_BLOCK_BYTES;  // H (bias+GELU only)
-    // AdamW half blocks (EPI_ADAM): master, m1, m2 fp32 (2 KB each), then the bf16 params
-    uint8_t* fblk = blk0;
-    uint8_t* pblk = blk0 + 3 * F32_BLOCK_BYTES;
+    uint8_t* pblk = blk0;  // EPI_ADAM: the bf16 parameter half block
     float inv_c1 = 1.f, inv_c2 = 1.f;
     if (EPI == EPI_ADAM) {
       inv_c1 = p.adam_coef[0];
@@ -302,8 +314,82 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
+      if (EPI == EPI_ADAM) {
+        // Fused AdamW (optimizer.cpp:58-104) over this warp's 32 rows x SPAN columns as
+        // 32x16 half tiles: the half's optimizer state (3 x 2 KB, contiguous in the
+        // tile-major blk_off layout) is loaded into registers first, the TMEM read overlaps
+        // the loads, then master/m/v are stored back and the bf16 parameter block goes out
+        // as one TMA tensor store.
+        constexpr int NH = SPAN / 16;
+        const int64_t gbase = int64_t(gz) * p.c_group_stride + int64_t(lane) * 4;
+        const int colw = ti.n_blk * BN + cq * SPAN;
 #pragma unroll 1
-      for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32) {
+        for (int k = 0; k < NH; ++k) {
+          const int64_t o = gbase + blk_off(row0, colw + 16 * k, p.N);
+          float4 cur[12];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cur[j] = ld_state(p.adam_master + o + j * 128);
+            cur[4 + j] = ld_state(p.adam_m1 + o + j * 128);
+            cur[8 + j] = ld_state(p.adam_m2 + o + j * 128);
+          }
+          float v[16];
+          ptx::tmem_ld16(tbase + cq * SPAN + 16 * k, v);
+          if (k == NH - 1) {  // accumulator fully read: the MMA warp may reuse it
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          }
+          float nv[16];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float* mq = &cur[j].x;
+            float* q1 = &cur[4 + j].x;
+            float* q2 = &cur[8 + j].x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              // the unfused path stores the bf16-rounded gradient: same rounding here
+              const float g = zero ? 0.f : __bfloat162float(__float2bfloat16(v[4 * j + q]));
+              q1[q] = p.b1 * q1[q] + p.omb1 * g;
+              q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
+              mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
+                               p.wd * mq[q]);
+              nv[4 * j + q] = mq[q];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            st_state(p.adam_master + o + j * 128, cur[j]);
+            st_state(p.adam_m1 + o + j * 128, cur[4 + j]);
+            st_state(p.adam_m2 + o + j * 128, cur[8 + j]);
+          }
+          // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
+          if (lane == 0) ptx::bulk_wait_read0();  // the previous half's store has read pblk
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            uint4 w;
+            w.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
+            w.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
+            w.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
+            w.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
+            *reinterpret_cast<uint4*>(pblk + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) = w;
+          }
+          ptx::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_3d(&tmC, pblk, colw + 16 * k, row0, gz);
+            ptx::bulk_commit();
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
+#pragma unroll 1
+      for (int c0 = cq * SPAN; c0 < (cq + 1) * SPAN; c0 += 32) {
         const int col = ti.n_blk * BN + c0;
         float v[32];
         ptx::tmem_ld32(tbase + c0, v);
@@ -332,80 +418,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v[8 * j + 2 * q + 1] *= gelu_grad_f(f.y);
             }
           }
-        }
-        if (EPI == EPI_ADAM) {
-          // pull the next 32x32 block's optimizer state into L2 while this one is processed
-          if (lane == 0 && c0 + 32 < (chalf + 1) * (BN / 2)) {
-            ptx::tma_prefetch_3d(&tmMaster, col + 32, row0, gz);
-            ptx::tma_prefetch_3d(&tmMaster, col + 48, row0, gz);
-            ptx::tma_prefetch_3d(&tmM1, col + 32, row0, gz);
-            ptx::tma_prefetch_3d(&tmM1, col + 48, row0, gz);
-            ptx::tma_prefetch_3d(&tmM2, col + 32, row0, gz);
-            ptx::tma_prefetch_3d(&tmM2, col + 48, row0, gz);
-          }
-          // two 32x16 halves: TMA-load master/m/v, update in place, TMA-store them and the
-          // bf16 parameters (the bf16-rounded gradient is what the unfused path stores)
-#pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            if (hf == 1) {
-              if (lane == 0) ptx::bulk_wait_read0();
-              __syncwarp();
-            }
-            if (lane == 0) {
-              ptx::mbar_arrive_expect_tx(&zbar[ew], 3 * F32_BLOCK_BYTES);
-              ptx::tma_load_3d(fblk, &tmMaster, &zbar[ew], col + 16 * hf, row0, gz);
-              ptx::tma_load_3d(fblk + F32_BLOCK_BYTES, &tmM1, &zbar[ew], col + 16 * hf, row0, gz);
-              ptx::tma_load_3d(fblk + 2 * F32_BLOCK_BYTES, &tmM2, &zbar[ew], col + 16 * hf, row0,
-                               gz);
-            }
-            ptx::mbar_wait(&zbar[ew], zphase);
-            zphase ^= 1;
-            float nv[16];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int off = lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4);
-              float4* pm = reinterpret_cast<float4*>(fblk + off);
-              float4* p1 = reinterpret_cast<float4*>(fblk + F32_BLOCK_BYTES + off);
-              float4* p2 = reinterpret_cast<float4*>(fblk + 2 * F32_BLOCK_BYTES + off);
-              float4 mm = *pm, a1 = *p1, a2 = *p2;
-              float* mq = &mm.x;
-              float* q1 = &a1.x;
-              float* q2 = &a2.x;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float g = __bfloat162float(__float2bfloat16(v[16 * hf + 4 * j + q]));
-                q1[q] = p.b1 * q1[q] + p.omb1 * g;
-                q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
-                mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
-                                 p.wd * mq[q]);
-                nv[4 * j + q] = mq[q];
-              }
-              *pm = mm;
-              *p1 = a1;
-              *p2 = a2;
-            }
-            // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              uint4 o;
-              o.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
-              o.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
-              o.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
-              o.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
-              *reinterpret_cast<uint4*>(pblk + hf * P16_BLOCK_BYTES + lane * 32 +
-                                        ((j ^ ((lane >> 2) & 1)) << 4)) = o;
-            }
-            ptx::fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              ptx::tma_store_3d(&tmMaster, fblk, col + 16 * hf, row0, gz);
-              ptx::tma_store_3d(&tmM1, fblk + F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
-              ptx::tma_store_3d(&tmM2, fblk + 2 * F32_BLOCK_BYTES, col + 16 * hf, row0, gz);
-              ptx::tma_store_3d(&tmC, pblk + hf * P16_BLOCK_BYTES, col + 16 * hf, row0, gz);
-              ptx::bulk_commit();
-            }
-          }
-          continue;  // parameters and state written; nothing else to stage
         }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {
           if (p.bias != nullptr) {
@@ -508,7 +520,7 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k<<<grid, NUM_THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
+  k<<<grid, Cfg<EPI>::THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
   count_launch(1);
   return cudaGetLastError();
 }
@@ -573,16 +585,16 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
                   (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 2, 32, 32, SW64);
     mx = mc;
     if (p.epi == EPI_ADAM) {
-      const uint64_t gs = (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 4;
-      const auto F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-      ok = ok && make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2, gs / 2, 16, 32,
-                          CU_TENSOR_MAP_SWIZZLE_32B) &&
-           make_map(&f0, p.adam_master, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32) &&
-           make_map(&f1, p.adam_m1, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32) &&
-           make_map(&f2, p.adam_m2, p.N, p.M, p.groups, p.ldc * 4, gs, 16, 32, SW64, F32);
+      if (p.c_group_stride <= 0 || p.c_group_stride % 4 != 0 || p.ldc != p.N ||
+          (reinterpret_cast<uintptr_t>(p.adam_master) | reinterpret_cast<uintptr_t>(p.adam_m1) |
+           reinterpret_cast<uintptr_t>(p.adam_m2)) % 16 != 0)
+        return fail("gemm: AdamW epilogue needs dense rows and 16 B aligned state blocks");
+      const uint64_t gs = (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 2;
+      ok = ok && make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2, gs, 16, 32,
+                          CU_TENSOR_MAP_SWIZZLE_32B);
     }
   }
-  if (p.epi != EPI_ADAM) f0 = f1 = f2 = mc;
+  f0 = f1 = f2 = mc;  // (state blocks move as 1-D bulk copies; the maps are unused)
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
   if (p.mode == GEMM_ROWS) {

@@ -92,6 +92,7 @@ struct Family {
   int64_t chunk = 0;  // completion all-gather chunk
   DevBuf<bf16> param, grad, gather;
   DevBuf<float> master, m1, m2;
+  bool blocked = false;  // weight-matrix state in the blk_off layout (fused AdamW epilogue)
   DevBuf<long long> dstep;  // steps_done on the device (graph-safe)
   DevBuf<float> dcoef;      // {1/(1-b1^steps), 1/(1-b2^steps)}
   int64_t steps = 0;
@@ -303,6 +304,11 @@ bool lookup(ted_layer* L, const std::string& name, ParamLoc& out) {
   return true;
 }
 
+// expert weight matrices whose optimizer state uses the blk_off layout
+bool state_blocked(const ted_layer* L, const ParamLoc& pl) {
+  return L->fam_exp.blocked && pl.fam == &L->fam_exp && pl.rows > 1;
+}
+
 uint16_t f2bf(float x) {
   uint32_t u;
   std::memcpy(&u, &x, 4);
@@ -319,7 +325,7 @@ float bf2f(uint16_t b) {
 
 __global__ void init_family_kernel(bf16* param, float* master, int64_t begin, int64_t end,
                                    int64_t off, int64_t rows, int64_t cols, int64_t full_cols,
-                                   int64_t col0, uint64_t seed, float scale) {
+                                   int64_t col0, uint64_t seed, float scale, int blocked) {
   const int64_t n = rows * cols;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -332,7 +338,8 @@ __global__ void init_family_kernel(bf16* param, float* master, int64_t begin, in
     const float v = (2.f * u - 1.f) * scale;
     param[off + i] = __float2bfloat16(v);
     const int64_t fi = off + i;
-    if (fi >= begin && fi < end) master[fi - begin] = v;
+    if (blocked) master[off + blk_off(r, c, cols)] = v;  // unsharded family (begin == 0)
+    else if (fi >= begin && fi < end) master[fi - begin] = v;
   }
 }
 
@@ -899,11 +906,29 @@ void family_step(ted_layer* L, Family& F, cudaStream_t s) {
   const int64_t one = std::max<int64_t>(owned, 1);
   const int64_t tile = L->tiles.enabled ? std::min<int64_t>(L->tiles.tile_size, one) : one;
   F.upcast_peak = std::max<uint64_t>(F.upcast_peak, owned == 0 ? 0 : uint64_t(tile) * 4);
-  check(adam_step(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, F.begin, F.end, tile,
-                  float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
-                  float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps),
-                  float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p, s),
-        "adam_step");
+  if (F.blocked) {  // expert family with blk_off weight state: w1, w2 blocked, biases flat
+    const struct {
+      int64_t off, len;
+      int cols;
+    } regions[4] = {{L->off_w1, int64_t(L->h) * L->fT, L->fT},
+                    {L->off_b1, L->fT, 0},
+                    {L->off_w2, int64_t(L->fT) * L->h, L->h},
+                    {L->off_b2, L->h, 0}};
+    for (const auto& rg : regions)
+      check(adam_segments(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, L->Eloc,
+                          L->per_expert, rg.off, rg.len, float(L->adam.lr),
+                          float(L->adam.beta1), float(L->adam.beta2),
+                          float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2),
+                          float(L->adam.eps), float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p,
+                          sm_count(), s, rg.cols),
+            "adam_segments");
+  } else {
+    check(adam_step(F.master.p, F.m1.p, F.m2.p, F.param.p, F.grad.p, F.begin, F.end, tile,
+                    float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
+                    float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps),
+                    float(L->adam.weight_decay), 1.f, 1.f, F.dcoef.p, s),
+          "adam_step");
+  }
   if (F.group > 1) {  // ZeRO-1 completion (moe.cpp:718-732), zero-padded equal chunks
     bf16* gbuf = F.gather.p;
     CU(cudaMemsetAsync(gbuf + F.pos * F.chunk, 0, sizeof(bf16) * F.chunk, s));
@@ -1123,7 +1148,11 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     L->use_graph = !(gv && std::strcmp(gv, "0") == 0);
   }
   L->fuse_ok = L->D == 1 && L->fam_exp.group == 1 && (L->per_expert % 4) == 0 &&
-               (L->off_w2 % 4) == 0 && (L->off_b1 % 4) == 0 && (L->off_b2 % 4) == 0;
+               (L->off_w2 % 4) == 0 && (L->off_b1 % 4) == 0 && (L->off_b2 % 4) == 0 &&
+               L->h % 256 == 0 && L->fT % 256 == 0;
+  if (const char* fz = std::getenv("TED_FUSE_ADAM"))  // A/B switch for measurements
+    if (std::strcmp(fz, "0") == 0) L->fuse_ok = false;
+  L->fam_exp.blocked = L->fuse_ok;
   if (L->fuse_ok) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1216,7 +1245,14 @@ int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
     Family& F = *pl.fam;
     CU(cudaMemcpy(F.param.p + pl.off, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
     const int64_t lo = std::max(pl.off, F.begin), hi = std::min(pl.off + int64_t(b.size()), F.end);
-    if (hi > lo)
+    if (state_blocked(L, pl)) {  // unsharded: the whole tensor, state in the blk_off layout
+      std::vector<float> blk(shard.size());
+      for (int64_t r = 0; r < pl.rows; ++r)
+        for (int64_t c = 0; c < pl.cols; ++c)
+          blk[size_t(blk_off(r, c, pl.cols))] = shard[size_t(r * pl.cols + c)];
+      CU(cudaMemcpy(F.master.p + pl.off, blk.data(), sizeof(float) * blk.size(),
+                    cudaMemcpyHostToDevice));
+    } else if (hi > lo)
       CU(cudaMemcpy(F.master.p + (lo - F.begin), shard.data() + (lo - pl.off),
                     sizeof(float) * (hi - lo), cudaMemcpyHostToDevice));
     L->fam_exp.reset = true;
@@ -1261,7 +1297,8 @@ int ted_layer_init_params(ted_layer* L, uint64_t seed) {
       Family& F = *pl.fam;
       init_family_kernel<<<sm_count() * 4, 256>>>(F.param.p, F.master.p, F.begin, F.end, pl.off,
                                                   pl.rows, pl.cols, pl.full_cols, col0,
-                                                  name_seed(seed, nm), float(pl.scale));
+                                                  name_seed(seed, nm), float(pl.scale),
+                                                  state_blocked(L, pl) ? 1 : 0);
       CU(cudaGetLastError());
     }
     L->fam_exp.reset = true;

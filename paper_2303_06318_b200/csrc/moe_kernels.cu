@@ -851,7 +851,8 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
     float* __restrict__ master, float* __restrict__ m1, float* __restrict__ m2,
     bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride4,
     int64_t seg_off4, int64_t seg_len4, float lr, float b1, float b2, float omb1, float omb2,
-    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef) {
+    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef,
+    int blk_cols) {
   if (coef) {
     inv_c1 = coef[0];
     inv_c2 = coef[1];
@@ -863,7 +864,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
   const int64_t stride = blockDim.x;
   {
     const int64_t t0 = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x;
-    int64_t idx[U];
+    int64_t idx[U], sidx[U];  // parameter / gradient and optimizer-state vector indices
     uint2 gu[U];
     float4 mm[U], vv[U], pp[U];
 #pragma unroll
@@ -872,11 +873,17 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
       idx[u] = -1;
       if (t < total) {
         const int64_t seg = t / seg_len4;
-        idx[u] = seg * seg_stride4 + seg_off4 + (t - seg * seg_len4);
+        const int64_t e4 = t - seg * seg_len4;
+        idx[u] = seg * seg_stride4 + seg_off4 + e4;
+        sidx[u] = idx[u];
+        if (blk_cols > 0) {
+          const int64_t o = 4 * e4, r = o / blk_cols, c = o - r * blk_cols;
+          sidx[u] = seg * seg_stride4 + seg_off4 + (blk_off(r, c, blk_cols) >> 2);
+        }
         gu[u] = reinterpret_cast<const uint2*>(grad)[idx[u]];
-        mm[u] = reinterpret_cast<float4*>(m1)[idx[u]];
-        vv[u] = reinterpret_cast<float4*>(m2)[idx[u]];
-        pp[u] = reinterpret_cast<float4*>(master)[idx[u]];
+        mm[u] = reinterpret_cast<float4*>(m1)[sidx[u]];
+        vv[u] = reinterpret_cast<float4*>(m2)[sidx[u]];
+        pp[u] = reinterpret_cast<float4*>(master)[sidx[u]];
       }
     }
 #pragma unroll
@@ -893,9 +900,9 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
         vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
         pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
       }
-      reinterpret_cast<float4*>(m1)[idx[u]] = mm[u];
-      reinterpret_cast<float4*>(m2)[idx[u]] = vv[u];
-      reinterpret_cast<float4*>(master)[idx[u]] = pp[u];
+      reinterpret_cast<float4*>(m1)[sidx[u]] = mm[u];
+      reinterpret_cast<float4*>(m2)[sidx[u]] = vv[u];
+      reinterpret_cast<float4*>(master)[sidx[u]] = pp[u];
       uint2 po;
       po.x = f2_to_bf2(pp[u].x, pp[u].y);
       po.y = f2_to_bf2(pp[u].z, pp[u].w);
@@ -1170,15 +1177,17 @@ cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, cons
                           int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
                           float b1, float b2, float omb1, float omb2, float eps, float wd,
                           float inv_c1, float inv_c2, const float* coef, int grid,
-                          cudaStream_t s) {
+                          cudaStream_t s, int blk_cols) {
   if (seg_stride % 4 || seg_off % 4 || seg_len % 4 || nseg < 1) return cudaErrorInvalidValue;
+  if (blk_cols > 0 && (blk_cols % 256 || seg_len % (int64_t(blk_cols) * 128)))
+    return cudaErrorInvalidValue;
   if (seg_len == 0) return cudaSuccess;
   (void)grid;
   const int64_t items = int64_t(nseg) * (seg_len / 4);
   const int ctas = int((items + 256 * 4 - 1) / (256 * 4));
   adam_segments_kernel<<<ctas, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
                                             seg_off / 4, seg_len / 4, lr, b1, b2, omb1, omb2,
-                                            eps, wd, inv_c1, inv_c2, coef);
+                                            eps, wd, inv_c1, inv_c2, coef, blk_cols);
   count_launch(1);
   return cudaGetLastError();
 }

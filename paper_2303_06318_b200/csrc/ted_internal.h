@@ -20,6 +20,23 @@ const char* last_error();
 enum GemmMode { GEMM_ROWS = 0, GEMM_KDIM = 1 };
 enum EpiKind { EPI_STORE = 0, EPI_BIAS = 1, EPI_BIAS_GELU = 2, EPI_DGELU = 3, EPI_ADAM = 4 };
 
+// Optimizer-state layout of the expert weight matrices when AdamW is fused into the wgrad
+// epilogue ("tile-major"): each 128x256 GEMM output tile's state is one contiguous 128 KB
+// run (tiles row-major over the matrix), inside it sixteen 32x64 warp shares (sub-partition
+// sp = row/32, column quarter cq) of four 32x16 fp32 half blocks (2 KB) each; inside a
+// half block, 4-column chunk j of row r sits at j * 128 + r * 4.  The epilogue warp that
+// owns rows r0..r0+31 of a half tile (one TMEM lane per row) thus moves each chunk with one
+// fully coalesced 512 B access, and the SMs working on consecutive tiles stream through
+// consecutive memory like an elementwise kernel.  Parameters and gradients stay row-major.
+// Needs rows % 128 == 0 and cols % 256 == 0.  Element offset of (r, c) in a rows x cols
+// matrix:
+__host__ __device__ inline int64_t blk_off(int64_t r, int64_t c, int64_t cols) {
+  const int64_t rr = r & 127, cc = c & 255;
+  const int64_t share = ((rr >> 5) << 2) + (cc >> 6);
+  return (((r >> 7) * (cols >> 8) + (c >> 8)) << 15) + ((share << 2) + ((cc >> 4) & 3)) * 512 +
+         ((cc >> 2) & 3) * 128 + (rr & 31) * 4 + (cc & 3);
+}
+
 struct GemmParams {
   int mode;  // GemmMode
   int epi;   // EpiKind
@@ -40,6 +57,7 @@ struct GemmParams {
   float* adam_m1 = nullptr;
   float* adam_m2 = nullptr;
   const float* adam_coef = nullptr;  // device {1/(1-b1^t), 1/(1-b2^t)}
+  // (EPI_ADAM: master/m1/m2 use the blk_off layout per group, group stride c_group_stride)
   float lr = 0.f, b1 = 0.f, b2 = 0.f, omb1 = 0.f, omb2 = 0.f, eps = 0.f, wd = 0.f;
 };
 
@@ -177,11 +195,13 @@ cudaError_t adam_step(float* master, float* m1, float* m2, bf16* param, const bf
 // a non-null coef passed to the Adam launchers overrides inv_c1 / inv_c2.
 cudaError_t adam_prep(long long* step, float* coef, double b1, double b2, cudaStream_t s);
 
-// AdamW over nseg equal, equally strided segments of an unsharded family (side stream).
+// AdamW over nseg equal, equally strided segments of an unsharded family.  blk_cols > 0:
+// each segment is a (seg_len / blk_cols) x blk_cols matrix whose optimizer state uses the
+// blk_off layout (parameters and gradients row-major).
 cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, const bf16* grad,
                           int nseg, int64_t seg_stride, int64_t seg_off, int64_t seg_len, float lr,
                           float b1, float b2, float omb1, float omb2, float eps, float wd,
                           float inv_c1, float inv_c2, const float* coef, int grid,
-                          cudaStream_t s);
+                          cudaStream_t s, int blk_cols = 0);
 
 }  // namespace ted
