@@ -851,8 +851,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
     float* __restrict__ master, float* __restrict__ m1, float* __restrict__ m2,
     bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride4,
     int64_t seg_off4, int64_t seg_len4, float lr, float b1, float b2, float omb1, float omb2,
-    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef,
-    int blk_cols) {
+    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef) {
   if (coef) {
     inv_c1 = coef[0];
     inv_c2 = coef[1];
@@ -864,7 +863,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
   const int64_t stride = blockDim.x;
   {
     const int64_t t0 = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x;
-    int64_t idx[U], sidx[U];  // parameter / gradient and optimizer-state vector indices
+    int64_t idx[U];
     uint2 gu[U];
     float4 mm[U], vv[U], pp[U];
 #pragma unroll
@@ -873,17 +872,11 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
       idx[u] = -1;
       if (t < total) {
         const int64_t seg = t / seg_len4;
-        const int64_t e4 = t - seg * seg_len4;
-        idx[u] = seg * seg_stride4 + seg_off4 + e4;
-        sidx[u] = idx[u];
-        if (blk_cols > 0) {
-          const int64_t o = 4 * e4, r = o / blk_cols, c = o - r * blk_cols;
-          sidx[u] = seg * seg_stride4 + seg_off4 + (blk_off(r, c, blk_cols) >> 2);
-        }
+        idx[u] = seg * seg_stride4 + seg_off4 + (t - seg * seg_len4);
         gu[u] = reinterpret_cast<const uint2*>(grad)[idx[u]];
-        mm[u] = reinterpret_cast<float4*>(m1)[sidx[u]];
-        vv[u] = reinterpret_cast<float4*>(m2)[sidx[u]];
-        pp[u] = reinterpret_cast<float4*>(master)[sidx[u]];
+        mm[u] = reinterpret_cast<float4*>(m1)[idx[u]];
+        vv[u] = reinterpret_cast<float4*>(m2)[idx[u]];
+        pp[u] = reinterpret_cast<float4*>(master)[idx[u]];
       }
     }
 #pragma unroll
@@ -900,14 +893,78 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
         vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
         pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
       }
-      reinterpret_cast<float4*>(m1)[sidx[u]] = mm[u];
-      reinterpret_cast<float4*>(m2)[sidx[u]] = vv[u];
-      reinterpret_cast<float4*>(master)[sidx[u]] = pp[u];
+      reinterpret_cast<float4*>(m1)[idx[u]] = mm[u];
+      reinterpret_cast<float4*>(m2)[idx[u]] = vv[u];
+      reinterpret_cast<float4*>(master)[idx[u]] = pp[u];
       uint2 po;
       po.x = f2_to_bf2(pp[u].x, pp[u].y);
       po.y = f2_to_bf2(pp[u].z, pp[u].w);
       reinterpret_cast<uint2*>(param)[idx[u]] = po;
     }
+  }
+}
+
+// AdamW over expert weight matrices whose optimizer state uses the tile-major blk_off
+// layout (the unfused path of a family whose state the fused wgrad epilogue owns): one warp
+// per 32x16 half block, lane = row, so both the state (contiguous 2 KB per array) and the
+// row-major bf16 gradient / parameter (32 B per row) move in full sectors.
+__global__ void __launch_bounds__(256) adam_tiles_kernel(
+    float* __restrict__ master, float* __restrict__ m1, float* __restrict__ m2,
+    bf16* __restrict__ param, const bf16* __restrict__ grad, int nseg, int64_t seg_stride,
+    int64_t seg_off, int rows, int cols, float lr, float b1, float b2, float omb1, float omb2,
+    float eps, float wd, float inv_c1, float inv_c2, const float* __restrict__ coef) {
+  if (coef) {
+    inv_c1 = coef[0];
+    inv_c2 = coef[1];
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t per_seg = int64_t(rows) * cols / 512;
+  const int64_t nblk = per_seg * nseg;
+  const int ntn = cols / 256;
+  for (int64_t b = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; b < nblk;
+       b += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const int64_t seg = b / per_seg, lb = b - seg * per_seg;
+    const int64_t tile = lb >> 6;
+    const int share = int(lb >> 2) & 15, hf = int(lb) & 3;
+    const int64_t row = (tile / ntn) * 128 + (share >> 2) * 32 + lane;
+    const int64_t col = (tile % ntn) * 256 + (share & 3) * 64 + hf * 16;
+    const int64_t base = seg * seg_stride + seg_off;
+    float* sm = master + base + lb * 512 + lane * 4;
+    float* s1 = m1 + base + lb * 512 + lane * 4;
+    float* s2 = m2 + base + lb * 512 + lane * 4;
+    const int64_t pi = base + row * cols + col;
+    const uint4 g0 = *reinterpret_cast<const uint4*>(grad + pi);
+    const uint4 g1 = *reinterpret_cast<const uint4*>(grad + pi + 8);
+    float4 w[4], a[4], c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      w[j] = *reinterpret_cast<const float4*>(sm + j * 128);
+      a[j] = *reinterpret_cast<const float4*>(s1 + j * 128);
+      c[j] = *reinterpret_cast<const float4*>(s2 + j * 128);
+    }
+    const uint32_t gw[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    uint32_t pw[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 ga = bf2_to_f2(gw[2 * j]), gb = bf2_to_f2(gw[2 * j + 1]);
+      const float g[4] = {ga.x, ga.y, gb.x, gb.y};
+      float* pw_ = &w[j].x;
+      float* pa = &a[j].x;
+      float* pc = &c[j].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pa[q] = b1 * pa[q] + omb1 * g[q];
+        pc[q] = b2 * pc[q] + omb2 * g[q] * g[q];
+        pw_[q] -= lr * ((pa[q] * inv_c1) / (sqrtf(pc[q] * inv_c2) + eps) + wd * pw_[q]);
+      }
+      pw[2 * j] = f2_to_bf2(w[j].x, w[j].y);
+      pw[2 * j + 1] = f2_to_bf2(w[j].z, w[j].w);
+      *reinterpret_cast<float4*>(sm + j * 128) = w[j];
+      *reinterpret_cast<float4*>(s1 + j * 128) = a[j];
+      *reinterpret_cast<float4*>(s2 + j * 128) = c[j];
+    }
+    *reinterpret_cast<uint4*>(param + pi) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+    *reinterpret_cast<uint4*>(param + pi + 8) = make_uint4(pw[4], pw[5], pw[6], pw[7]);
   }
 }
 
@@ -1179,15 +1236,24 @@ cudaError_t adam_segments(float* master, float* m1, float* m2, bf16* param, cons
                           float inv_c1, float inv_c2, const float* coef, int grid,
                           cudaStream_t s, int blk_cols) {
   if (seg_stride % 4 || seg_off % 4 || seg_len % 4 || nseg < 1) return cudaErrorInvalidValue;
-  if (blk_cols > 0 && (blk_cols % 256 || seg_len % (int64_t(blk_cols) * 128)))
-    return cudaErrorInvalidValue;
+  if (blk_cols > 0) {
+    if (blk_cols % 256 || seg_len % (int64_t(blk_cols) * 128)) return cudaErrorInvalidValue;
+    if ((seg_stride | seg_off) % 8) return cudaErrorInvalidValue;  // 16 B rows of bf16
+    const int64_t blocks = int64_t(nseg) * (seg_len / 512);
+    const int ctas = int(std::min<int64_t>((blocks + 7) / 8, int64_t(sm_count()) * 16));
+    adam_tiles_kernel<<<ctas, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride,
+                                           seg_off, int(seg_len / blk_cols), blk_cols, lr, b1,
+                                           b2, omb1, omb2, eps, wd, inv_c1, inv_c2, coef);
+    count_launch(1);
+    return cudaGetLastError();
+  }
   if (seg_len == 0) return cudaSuccess;
   (void)grid;
   const int64_t items = int64_t(nseg) * (seg_len / 4);
   const int ctas = int((items + 256 * 4 - 1) / (256 * 4));
   adam_segments_kernel<<<ctas, 256, 0, s>>>(master, m1, m2, param, grad, nseg, seg_stride / 4,
                                             seg_off / 4, seg_len / 4, lr, b1, b2, omb1, omb2,
-                                            eps, wd, inv_c1, inv_c2, coef, blk_cols);
+                                            eps, wd, inv_c1, inv_c2, coef);
   count_launch(1);
   return cudaGetLastError();
 }
