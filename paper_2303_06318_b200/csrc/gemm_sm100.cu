@@ -37,7 +37,7 @@ constexpr int BM = 128, BN = 256, BK = 64;
 constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int MAX_GROUPS = 256;
+constexpr int MAX_GROUPS = 128;  // local experts per launch
 constexpr int MAX_EPI_WARPS = 16;
 constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
 constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
@@ -69,7 +69,7 @@ struct Cfg {
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + epilogue warps
   static constexpr int COL_SPAN = BN / (EPI_WARPS / 4);  // tile columns per epilogue warp
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  static constexpr int STAGES = EPI == EPI_BIAS_GELU ? 3 : 4;
+  static constexpr int STAGES = 4;
   static constexpr size_t PER_WARP = EPI == EPI_ADAM ? P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
@@ -80,6 +80,19 @@ struct TileInfo {
   int g, m_blk, n_blk, k_len;  // k_len = number of K elements (multiple of 64)
 };
 
+// Tile order inside a group: bands of kBand row blocks, walked column block by column
+// block, so the ~148 tiles in flight cover about kBand x 18 blocks and share their A and B
+// k-slices in L2 (row-major order would cover ~2 row blocks x every column block and
+// stream a wide B from HBM once per two row blocks).
+constexpr int kBand = 8;
+__device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, int& n_blk) {
+  const int band = local / (kBand * nt);
+  const int idx = local - band * (kBand * nt);
+  const int rows = min(kBand, mt - band * kBand);
+  n_blk = idx / rows;
+  m_blk = band * kBand + (idx - n_blk * rows);
+}
+
 __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_off,
                                             const int* s_tstart, int total, int t, TileInfo& ti) {
   if (t >= total) return false;
@@ -87,17 +100,14 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
   if (p.mode == GEMM_ROWS) {
     int g = 0;
     while (g + 1 < p.groups && s_tstart[g + 1] <= t) ++g;
-    const int local = t - s_tstart[g];
     ti.g = g;
-    ti.m_blk = local / nt;
-    ti.n_blk = local % nt;
+    raster(t - s_tstart[g], (s_off[g + 1] - s_off[g]) / BM, nt, ti.m_blk, ti.n_blk);
     ti.k_len = p.K;
   } else {
-    const int per = (p.M / BM) * nt;
+    const int mt = p.M / BM;
+    const int per = mt * nt;
     ti.g = t / per;
-    const int local = t % per;
-    ti.m_blk = local / nt;
-    ti.n_blk = local % nt;
+    raster(t % per, mt, nt, ti.m_blk, ti.n_blk);
     ti.k_len = s_off[ti.g + 1] - s_off[ti.g];
   }
   return true;
