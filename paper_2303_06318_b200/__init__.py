@@ -18,7 +18,8 @@ import os
 from dataclasses import dataclass, field
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libted_b200.so")
+# TED_LIB: load another build of the same library (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("TED_LIB") or os.path.join(HERE, "libted_b200.so")
 PLAN_PATH = os.path.join(HERE, "libted_plan.so")
 
 TED_OK, TED_ERR_RUNTIME, TED_ERR_CONFIG = 0, 1, 2

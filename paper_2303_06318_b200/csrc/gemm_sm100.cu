@@ -50,16 +50,24 @@ constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging blo
 // tools/adam_bw.cu: 4.6-5.0 vs 3.1 TB/s for the same bytes).
 constexpr int P16_BLOCK_BYTES = 32 * 16 * 2;
 
-__device__ __forceinline__ float4 ld_state(const float* p) {
+// optimizer state is touched once per step: evict-first in L2 so it does not push out the
+// wgrad operand slices the neighbouring tiles are about to re-read
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ld_state(const float* p, uint64_t pol) {
   float4 v;
-  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ void st_state(float* p, float4 v) {
-  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
-               "f"(v.y), "f"(v.z), "f"(v.w)
+__device__ __forceinline__ void st_state(float* p, float4 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::
+                   "l"(p),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
 }
 
@@ -332,6 +340,7 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
         // as one TMA tensor store.
         constexpr int NH = SPAN / 16;
         const int64_t gbase = int64_t(gz) * p.c_group_stride + int64_t(lane) * 4;
+        const uint64_t pol = evict_first_policy();
         const int colw = ti.n_blk * BN + cq * SPAN;
 #pragma unroll 1
         for (int k = 0; k < NH; ++k) {
@@ -339,9 +348,9 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           float4 cur[12];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            cur[j] = ld_state(p.adam_master + o + j * 128);
-            cur[4 + j] = ld_state(p.adam_m1 + o + j * 128);
-            cur[8 + j] = ld_state(p.adam_m2 + o + j * 128);
+            cur[j] = ld_state(p.adam_master + o + j * 128, pol);
+            cur[4 + j] = ld_state(p.adam_m1 + o + j * 128, pol);
+            cur[8 + j] = ld_state(p.adam_m2 + o + j * 128, pol);
           }
           float v[16];
           ptx::tmem_ld16(tbase + cq * SPAN + 16 * k, v);
@@ -369,9 +378,9 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            st_state(p.adam_master + o + j * 128, cur[j]);
-            st_state(p.adam_m1 + o + j * 128, cur[4 + j]);
-            st_state(p.adam_m2 + o + j * 128, cur[8 + j]);
+            st_state(p.adam_master + o + j * 128, cur[j], pol);
+            st_state(p.adam_m1 + o + j * 128, cur[4 + j], pol);
+            st_state(p.adam_m2 + o + j * 128, cur[8 + j], pol);
           }
           // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
           if (lane == 0) ptx::bulk_wait_read0();  // the previous half's store has read pblk
