@@ -123,80 +123,114 @@ __device__ __forceinline__ void stage_wg(const bf16* __restrict__ wg, int E, int
   }
 }
 
-// TPW tokens of a warp are processed together so each Wg slice read from smem feeds
-// TPW * 8 FMAs; TPW * EMAX = 32 accumulators (64 for EMAX = 64) keeps 2 CTAs / SM.
-template <int EMAX, int TPW>
-__global__ void __launch_bounds__(kThreads) gate_fwd_kernel(const bf16* __restrict__ a,
-                                                            const bf16* __restrict__ wg,
-                                                            int64_t n, int h, int E, int HC,
-                                                            float* __restrict__ logits,
-                                                            float* __restrict__ probs,
-                                                            int* __restrict__ expert,
-                                                            float* __restrict__ prob,
-                                                            int* __restrict__ blk_hist) {
+// Gate logits on the tensor cores: logits[16 tokens x 8 experts] per mma.sync.m16n8k16
+// (bf16 x bf16 products exact, fp32 accumulation -- the same arithmetic class as the FMA
+// path, 12 warp instructions per token instead of ~1000, so the kernel is HBM-bound).
+// The K order inside each 32-element step is permuted identically for A and B (a dot
+// product is order-free up to fp32 rounding): quad lane c loads 16 contiguous bytes
+// (elements 8c..8c+7) of its two token rows g and g+8, and MMA m in {0,1} takes elements
+// 8c+4m..8c+4m+3 of the token rows and of the staged Wg^T rows.  CTA = 64 tokens (one
+// routing block), warp = 16 tokens x one half of every 64-element K pair; the two K halves
+// are summed in a fixed order (bit-identical logits on every TP replica).
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1,
+                                               uint32_t a2, uint32_t a3, uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+constexpr int kGatePad = 8;  // bf16 padding per staged Wg^T row (spreads the B loads' banks)
+
+template <int EMAX, int U>
+__global__ void __launch_bounds__(kThreads, 2) gate_fwd_mma_kernel(
+    const bf16* __restrict__ a, const bf16* __restrict__ wg, int64_t n, int h, int E, int HC,
+    float* __restrict__ logits, float* __restrict__ probs, int* __restrict__ expert,
+    float* __restrict__ prob, int* __restrict__ blk_hist) {
+  constexpr int NT = EMAX / 8;
   extern __shared__ __align__(16) uint8_t smem[];
-  float* s_part = reinterpret_cast<float*>(smem);  // [kRouteBlock][EMAX]
-  bf16* s_wg = reinterpret_cast<bf16*>(smem + kRouteBlock * EMAX * sizeof(float));
+  float* s_part = reinterpret_cast<float*>(smem);  // [2][kRouteBlock][EMAX]
+  bf16* s_wg = reinterpret_cast<bf16*>(smem + 2 * kRouteBlock * EMAX * sizeof(float));
   __shared__ int s_hist[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int tt = warp & 3, ks = warp >> 2;
   const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
-  for (int i = threadIdx.x; i < kRouteBlock * EMAX; i += blockDim.x) s_part[i] = 0.f;
+  const int64_t ta = tok0 + tt * 16 + g, tb = ta + 8;
+  const bf16* pa = a + (ta < n ? ta : 0) * int64_t(h) + 8 * c;
+  const bf16* pb = a + (tb < n ? tb : 0) * int64_t(h) + 8 * c;
+  const bool va = ta < n, vb = tb < n;
   if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+  const int HCP = HC + kGatePad;
+  float acc[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
   for (int c0 = 0; c0 < h; c0 += HC) {
     const int hc = min(HC, h - c0);
     __syncthreads();
-    stage_wg<EMAX>(wg, E, c0, hc, HC, s_wg);
+    stage_wg<EMAX>(wg, E, c0, hc, HCP, s_wg);  // s_wg[e][i] = Wg[c0 + i][e], zero e >= E
     __syncthreads();
-#pragma unroll 1
-    for (int tg = 0; tg < kWarpTok; tg += TPW) {
-      float acc[TPW * EMAX];
+    const int steps = hc / 32;  // 32-element K steps; this warp takes ks, ks + 2, ...
+    uint4 cur[U][2], nxt[U][2];
+    auto load = [&](int s0, uint4 (&d)[U][2]) {
 #pragma unroll
-      for (int i = 0; i < TPW * EMAX; ++i) acc[i] = 0.f;
-      // next slice's loads are issued before the current slice's FMAs
-      uint4 nx[TPW];
-      auto load_slice = [&](int i0, uint4 (&dst)[TPW]) {
+      for (int u = 0; u < U; ++u) {
+        const int st = s0 + 2 * u;
+        const int64_t off = c0 + int64_t(st) * 32;
+        const bool in = st < steps;
+        d[u][0] = (in && va) ? ldg_stream(pa + off) : make_uint4(0, 0, 0, 0);
+        d[u][1] = (in && vb) ? ldg_stream(pb + off) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    load(ks, cur);
+    for (int s0 = ks; s0 < steps; s0 += 2 * U) {
+      load(s0 + 2 * U, nxt);
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) {
-          const int64_t k = tok0 + warp * kWarpTok + tg + t;
-          dst[t] = (k < n && i0 < hc) ? ldg_stream(a + k * h + c0 + i0) : make_uint4(0, 0, 0, 0);
-        }
-      };
-      load_slice(lane * 8, nx);
-#pragma unroll 1
-      for (int i0 = lane * 8; i0 < hc; i0 += 256) {
-        float av[TPW][8];
+      for (int u = 0; u < U; ++u) {
+        const int st = s0 + 2 * u;
+        if (st >= steps) break;
+        const uint32_t* xa = reinterpret_cast<const uint32_t*>(&cur[u][0]);
+        const uint32_t* xb = reinterpret_cast<const uint32_t*>(&cur[u][1]);
+        const bf16* wrow = s_wg + g * HCP + st * 32 + 8 * c;
 #pragma unroll
-        for (int t = 0; t < TPW; ++t) unpack8(nx[t], av[t]);
-        load_slice(i0 + 256, nx);
+        for (int m = 0; m < 2; ++m) {
 #pragma unroll
-        for (int j = 0; j < EMAX; ++j) {
-          float wv[8];
-          unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
-#pragma unroll
-          for (int t = 0; t < TPW; ++t)
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[t * EMAX + j] = fmaf(av[t][q], wv[q], acc[t * EMAX + j]);
+          for (int nt = 0; nt < NT; ++nt) {
+            const uint2 bw = *reinterpret_cast<const uint2*>(wrow + nt * 8 * HCP + 4 * m);
+            mma_bf16_16816(acc[nt], xa[2 * m], xb[2 * m], xa[2 * m + 1], xb[2 * m + 1], bw.x,
+                           bw.y);
+          }
         }
       }
 #pragma unroll
-      for (int half = 0; half < (TPW * EMAX) / 32; ++half) {
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = acc[half * 32 + i];
-        const float tot = reduce_scatter32(v, lane);
-        const int vi = half * 32 + lane;
-        s_part[(warp * kWarpTok + tg + vi / EMAX) * EMAX + (vi % EMAX)] += tot;
+      for (int u = 0; u < U; ++u) {
+        cur[u][0] = nxt[u][0];
+        cur[u][1] = nxt[u][1];
       }
     }
   }
-  __syncwarp();
+  // partial logits of this K half: token rows g / g+8, experts nt*8 + 2c (+1)
+  float* sp = s_part + ks * (kRouteBlock * EMAX);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int e = nt * 8 + 2 * c;
+    sp[(tt * 16 + g) * EMAX + e] = acc[nt][0];
+    sp[(tt * 16 + g) * EMAX + e + 1] = acc[nt][1];
+    sp[(tt * 16 + g + 8) * EMAX + e] = acc[nt][2];
+    sp[(tt * 16 + g + 8) * EMAX + e + 1] = acc[nt][3];
+  }
+  __syncthreads();
   for (int t = 0; t < kWarpTok; ++t) {
-    const int64_t k = tok0 + warp * kWarpTok + t;
+    const int lt = warp * kWarpTok + t;
+    const int64_t k = tok0 + lt;
     if (k >= n) break;
-    const float* lp = s_part + (warp * kWarpTok + t) * EMAX;
-    const float l0v = lane < EMAX ? lp[lane] : 0.f;
-    const float l1v = lane + 32 < EMAX ? lp[lane + 32] : 0.f;
+    const float* l0 = s_part + lt * EMAX;
+    const float* l1 = l0 + kRouteBlock * EMAX;
+    const float l0v = lane < E ? l0[lane] + l1[lane] : 0.f;
+    const float l1v = lane + 32 < E ? l0[lane + 32] + l1[lane + 32] : 0.f;
     const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
     if (lane == 0) atomicAdd(&s_hist[best], 1);
   }
@@ -1046,18 +1080,18 @@ cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E,
   if (E < 1 || E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-#define TED_GATE(EM, TP)                                                                      \
+#define TED_GATE(EM, U)                                                                       \
   {                                                                                           \
-    const int HC = gate_hc<EM>(h);                                                            \
-    const size_t sm = kRouteBlock * EM * sizeof(float) + size_t(EM) * HC * 2;                 \
-    smem_attr(gate_fwd_kernel<EM, TP>, sm);                                                   \
-    gate_fwd_kernel<EM, TP><<<grid, kThreads, sm, s>>>(a, wg, n, h, E, HC, logits, probs,     \
-                                                       expert, prob, blk_hist);               \
+    const int HC = std::min(((h + 255) / 256) * 256, EM <= 16 ? 2048 : (EM <= 32 ? 1024 : 512)); \
+    const size_t sm = 2 * kRouteBlock * EM * sizeof(float) + size_t(EM) * (HC + kGatePad) * 2; \
+    smem_attr(gate_fwd_mma_kernel<EM, U>, sm);                                                \
+    gate_fwd_mma_kernel<EM, U><<<grid, kThreads, sm, s>>>(a, wg, n, h, E, HC, logits, probs,  \
+                                                          expert, prob, blk_hist);            \
   }
   if (E <= 8) TED_GATE(8, 4)
-  else if (E <= 16) TED_GATE(16, 2)
-  else if (E <= 32) TED_GATE(32, 1)
-  else TED_GATE(64, 1)
+  else if (E <= 16) TED_GATE(16, 4)
+  else if (E <= 32) TED_GATE(32, 2)
+  else TED_GATE(64, 2)
 #undef TED_GATE
   count_launch(1);
   return cudaGetLastError();
