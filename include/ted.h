@@ -205,6 +205,37 @@ int ted_set_device(int device);
 int ted_layer_get_routing(ted_layer* L, int32_t* expert, float* prob, int32_t* slot,
                           int32_t* pos_home, float* probs, float* logits);
 
+/* ---------------------------------------------------------------- whole model (stack)
+ * The reference's Trainer / MoeRank over model.layers layers (moe.cpp:334-415): every
+ * layer = attention stand-in block (column -> GELU -> row + TP all-reduce,
+ * moe.cpp:418-426 / :688-696, parallel_linear.cpp:8-40), then the MoE branch on even
+ * layers (layer_has_experts) or a dense FFN block on odd layers (moe.cpp:428-433 /
+ * :571-580).  Parameters by the reference's names (enumerate_params, moe.cpp:115-147):
+ * layer{l}.attn.{w1,b1,w2,b2}, layer{l}.gate.w, layer{l}.expert{e}.*, layer{l}.ffn.*.
+ * `batch` is this rank's shard (tokens_per_shard x hidden bf16, device), shard index
+ * d*EP + e replicated over the TP group (moe.cpp:229, :266-267).  Loss of this rank =
+ * sum(y^2) / (2 N_global) over the last layer's output (moe.cpp:379-381); the Trainer's
+ * loss is the sum over data shards (moe.cpp:822-831). */
+typedef struct ted_model ted_model;
+
+int ted_model_create(const ted_model_cfg* model, const ted_topo_cfg* topo, const ted_flags* flags,
+                     const ted_adam_cfg* adam, const ted_tile_cfg* tiles, double capacity_factor,
+                     int shard_optimizer, int rank, const void* nccl_uid, ted_model** out);
+void ted_model_destroy(ted_model* M);
+int ted_model_set_param(ted_model* M, const char* name, const float* full);
+int ted_model_get_param(ted_model* M, const char* name, float* out, int64_t* numel);
+int ted_model_get_grad(ted_model* M, const char* name, float* out, int64_t* numel);
+int ted_model_init_params(ted_model* M, uint64_t seed);
+/* Trainer::step (moe.cpp:838-844): run_forward, run_backward, run_grad_sync,
+ * run_optimizer_step */
+int ted_model_step(ted_model* M, const uint16_t* batch, void* stream);
+int ted_model_forward(ted_model* M, const uint16_t* batch, void* stream);
+int ted_model_backward(ted_model* M, void* stream);
+int ted_model_optimizer_step(ted_model* M, void* stream);
+int ted_model_loss(ted_model* M, double* loss, void* stream);
+/* last layer's output (tokens_per_shard x hidden bf16, device) */
+int ted_model_output(ted_model* M, uint16_t* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -146,6 +146,20 @@ _sig("ted_layer_get_routing", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp])
 _sig("ted_layer_timing", _i32, [_vp, _i32])
 _sig("ted_layer_timing_read", _i32, [_vp, C.c_char_p, _i32])
 _sig("ted_kernel_launches", C.c_ulonglong, [])
+_sig("ted_model_create", _i32, [C.POINTER(ModelCfg), C.POINTER(TopoCfg), C.POINTER(FlagsC),
+                                C.POINTER(AdamC), C.POINTER(TileC), _dbl, _i32, _i32,
+                                C.c_char_p, C.POINTER(_vp)])
+_sig("ted_model_destroy", None, [_vp])
+_sig("ted_model_set_param", _i32, [_vp, C.c_char_p, _vp])
+_sig("ted_model_get_param", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
+_sig("ted_model_get_grad", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
+_sig("ted_model_init_params", _i32, [_vp, _u64])
+_sig("ted_model_step", _i32, [_vp, _vp, _vp])
+_sig("ted_model_forward", _i32, [_vp, _vp, _vp])
+_sig("ted_model_backward", _i32, [_vp, _vp])
+_sig("ted_model_optimizer_step", _i32, [_vp, _vp])
+_sig("ted_model_loss", _i32, [_vp, C.POINTER(_dbl), _vp])
+_sig("ted_model_output", _i32, [_vp, _vp, _vp])
 
 EXPORTED = [
     "ted_default_configs", "ted_last_error", "ted_version", "ted_derive_config",
@@ -155,7 +169,10 @@ EXPORTED = [
     "ted_layer_get_grad", "ted_layer_init_params", "ted_layer_forward", "ted_layer_backward",
     "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_get_stats",
     "ted_layer_get_routing", "ted_layer_timing", "ted_layer_timing_read", "ted_kernel_launches",
-    "ted_set_device"]
+    "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
+    "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_step",
+    "ted_model_forward", "ted_model_backward", "ted_model_optimizer_step", "ted_model_loss",
+    "ted_model_output"]
 
 
 def lib():
@@ -459,3 +476,102 @@ class MoeLayer:
         _check(_lib.ted_layer_get_routing(self._h, *(x.ctypes.data_as(_vp)
                                                      for x in (ex, pr, sl, ph, ps, lg))))
         return dict(expert=ex, prob=pr, slot=sl, pos_home=ph, probs=ps, logits=lg)
+
+
+# ------------------------------------------------------------------ the model (Trainer)
+
+def param_names(model: MoeModelConfig) -> list:
+    """enumerate_params order (moe.cpp:115-147): attention block, then the gate and experts
+    on even layers or the dense FFN block on odd layers."""
+    out = []
+    for l in range(model.layers):
+        out += [f"layer{l}.attn.{k}" for k in ("w1", "b1", "w2", "b2")]
+        if l % 2 == 0:
+            out.append(f"layer{l}.gate.w")
+            for e in range(model.experts):
+                out += [f"layer{l}.expert{e}.{k}" for k in ("w1", "b1", "w2", "b2")]
+        else:
+            out += [f"layer{l}.ffn.{k}" for k in ("w1", "b1", "w2", "b2")]
+    return out
+
+
+def param_shape(model: MoeModelConfig, name: str) -> tuple:
+    h = model.hidden
+    leaf = name.rsplit(".", 1)[1]
+    if name.endswith("gate.w"):
+        return (h, model.experts)
+    return {"w1": (h, 4 * h), "b1": (4 * h,), "w2": (4 * h, h), "b2": (h,)}[leaf]
+
+
+class TedModel:
+    """One rank of the reference's Trainer over a layer stack (MoeRank, moe.cpp:334-415):
+    attention stand-in block + MoE branch (even layers) or dense FFN (odd layers)."""
+
+    def __init__(self, model: MoeModelConfig, topo: TedConfig, flags: RunFlags | None = None,
+                 adam: AdamConfig | None = None, tiles: TileConfig | None = None,
+                 capacity_factor: float = 0.0, shard_optimizer: bool = True, rank: int = 0,
+                 nccl_uid: bytes | None = None):
+        self.model, self.topo = model, topo
+        self.flags = flags or RunFlags()
+        self.adam = adam or AdamConfig()
+        self.tiles = tiles or TileConfig()
+        h = _vp()
+        m, t, f, a, ti = model.c(), topo.c(), self.flags.c(), self.adam.c(), self.tiles.c()
+        _check(_lib.ted_model_create(C.byref(m), C.byref(t), C.byref(f), C.byref(a),
+                                     C.byref(ti), capacity_factor, int(shard_optimizer), rank,
+                                     nccl_uid, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ted_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_param(self, name: str, full):
+        import numpy as np
+        arr = np.ascontiguousarray(full, dtype=np.float32)
+        _check(_lib.ted_model_set_param(self._h, name.encode(), arr.ctypes.data_as(_vp)))
+
+    def _get(self, name, grad):
+        import numpy as np
+        n = _i64()
+        fn = _lib.ted_model_get_grad if grad else _lib.ted_model_get_param
+        _check(fn(self._h, name.encode(), None, C.byref(n)))
+        out = np.empty(n.value, np.float32)
+        _check(fn(self._h, name.encode(), out.ctypes.data_as(_vp), C.byref(n)))
+        return out
+
+    def get_param(self, name):
+        return self._get(name, False)
+
+    def get_grad(self, name):
+        return self._get(name, True)
+
+    def init_params(self, seed: int = 0):
+        _check(_lib.ted_model_init_params(self._h, seed))
+
+    def step(self, batch, stream=None):
+        _check(_lib.ted_model_step(self._h, _p(batch), _stream(stream)))
+
+    def forward(self, batch, stream=None):
+        _check(_lib.ted_model_forward(self._h, _p(batch), _stream(stream)))
+
+    def backward(self, stream=None):
+        _check(_lib.ted_model_backward(self._h, _stream(stream)))
+
+    def optimizer_step(self, stream=None):
+        _check(_lib.ted_model_optimizer_step(self._h, _stream(stream)))
+
+    def loss(self, stream=None) -> float:
+        v = _dbl()
+        _check(_lib.ted_model_loss(self._h, C.byref(v), _stream(stream)))
+        return v.value
+
+    def output(self, y, stream=None):
+        _check(_lib.ted_model_output(self._h, _p(y), _stream(stream)))

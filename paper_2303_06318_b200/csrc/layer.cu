@@ -25,86 +25,12 @@
 #include <vector>
 
 #include "../../include/ted.h"
+#include "ted_host.h"
 #include "ted_internal.h"
 #include "ted_plan.h"
 
 namespace ted {
 
-struct ConfigError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct RuntimeError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-#define CU(x)                                                                              \
-  do {                                                                                     \
-    cudaError_t e_ = (x);                                                                  \
-    if (e_ != cudaSuccess)                                                                 \
-      throw ::ted::RuntimeError(std::string("CUDA: ") + cudaGetErrorString(e_) + " at " + \
-                                __FILE__ + ":" + std::to_string(__LINE__) + " (" #x ")");  \
-  } while (0)
-#define NC(x)                                                                                 \
-  do {                                                                                        \
-    ncclResult_t r_ = (x);                                                                    \
-    if (r_ != ncclSuccess)                                                                    \
-      throw ::ted::RuntimeError(std::string("NCCL: ") + ncclGetErrorString(r_) + " at " +    \
-                                __FILE__ + ":" + std::to_string(__LINE__));                   \
-  } while (0)
-
-template <class T>
-struct DevBuf {
-  T* p = nullptr;
-  size_t n = 0;
-  void alloc(size_t count) {
-    free();
-    n = count;
-    if (count) CU(cudaMalloc(&p, sizeof(T) * count));
-  }
-  void zero() {
-    if (n) CU(cudaMemset(p, 0, sizeof(T) * n));
-  }
-  void free() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-  }
-  ~DevBuf() { free(); }
-};
-
-template <class T>
-struct HostBuf {
-  T* p = nullptr;
-  void alloc(size_t count) {
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    if (count) CU(cudaMallocHost(&p, sizeof(T) * count));
-  }
-  ~HostBuf() {
-    if (p) cudaFreeHost(p);
-  }
-};
-
-struct Family {
-  int64_t elems = 0;      // family length
-  int group = 1, pos = 0;  // ZeRO-1 data group size / position
-  int64_t begin = 0, end = 0;
-  int64_t chunk = 0;  // completion all-gather chunk
-  DevBuf<bf16> param, grad, gather;
-  DevBuf<float> master, m1, m2;
-  bool blocked = false;  // weight-matrix state in the blk_off layout (fused AdamW epilogue)
-  DevBuf<long long> dstep;  // steps_done on the device (graph-safe)
-  DevBuf<float> dcoef;      // {1/(1-b1^steps), 1/(1-b2^steps)}
-  int64_t steps = 0;
-  bool reset = false;
-  uint64_t upcast_peak = 0;
-  ncclComm_t dp = nullptr;
-};
-
-inline int64_t shard_lo(int64_t total, int parts, int i) {
-  const int64_t base = total / parts, extra = total % parts;
-  return i * base + (i < extra ? i : extra);
-}
 
 }  // namespace ted
 
@@ -233,42 +159,6 @@ const char* last_error() { return g_err.c_str(); }
 
 namespace {
 
-template <class F>
-int guard(F&& f) {
-  try {
-    f();
-    return TED_OK;
-  } catch (const ConfigError& e) {
-    g_err = e.what();
-    return TED_ERR_CONFIG;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return TED_ERR_CONFIG;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return TED_ERR_RUNTIME;
-  }
-}
-
-void require(bool ok, const std::string& msg) {
-  if (!ok) throw ConfigError(msg);
-}
-
-void require_device() {
-  int n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
-    throw RuntimeError("no CUDA device: the TED kernels are sm_100a-only (no CPU fallback)");
-  int dev = 0, major = 0;
-  CU(cudaGetDevice(&dev));
-  CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
-  if (major != 10) throw RuntimeError("TED kernels need an sm_100 (B200) device");
-}
-
-cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-
-void check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) throw RuntimeError(std::string(what) + ": " + cudaGetErrorString(e));
-}
 
 // --------------------------------------------------------------- parameters
 struct ParamLoc {
@@ -309,19 +199,6 @@ bool state_blocked(const ted_layer* L, const ParamLoc& pl) {
   return L->fam_exp.blocked && pl.fam == &L->fam_exp && pl.rows > 1;
 }
 
-uint16_t f2bf(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t((u >> 16) | 0x40);  // NaN
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return uint16_t(u >> 16);
-}
-float bf2f(uint16_t b) {
-  uint32_t u = uint32_t(b) << 16;
-  float x;
-  std::memcpy(&x, &u, 4);
-  return x;
-}
 
 __global__ void init_family_kernel(bf16* param, float* master, int64_t begin, int64_t end,
                                    int64_t off, int64_t rows, int64_t cols, int64_t full_cols,
@@ -429,12 +306,6 @@ void zero_asm_pads(ted_layer* L, bf16* buf, cudaStream_t s) {
           "zero_pad_rows");
 }
 
-void run_gemm(const GemmOperands& o, const GemmParams& p, int64_t rows, cudaStream_t s) {
-  const char* why = nullptr;
-  cudaError_t e = grouped_gemm(o, p, int(rows), s, &why);
-  if (e != cudaSuccess)
-    throw RuntimeError(std::string("grouped_gemm: ") + (why ? why : cudaGetErrorString(e)));
-}
 
 RowSrc pull_src(ted_layer* L, int which) {
   RowSrc r;
@@ -1023,7 +894,8 @@ void setup_peer_exchange(ted_layer* L) {
 
 void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* topo,
                   const ted_flags* flags, const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
-                  double cf, int shard_opt, int rank, const void* uid) {
+                  double cf, int shard_opt, int rank, const void* uid,
+                  ncclComm_t parent = nullptr) {
   require(model && topo && flags && adam && tiles, "null config pointer");
   L->model = *model;
   L->topo = *topo;
@@ -1073,10 +945,14 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
 
   // communicators (topology.cpp:56-93 colours; ascending-rank keys)
   if (L->world > 1) {
-    require(uid != nullptr, "world_size > 1 needs an NCCL unique id");
-    ncclUniqueId id;
-    std::memcpy(&id, uid, sizeof(id));
-    NC(ncclCommInitRank(&L->world_c, L->world, id, rank));
+    if (parent != nullptr) {  // a layer of a model stack: split the model's communicator
+      NC(ncclCommSplit(parent, 0, rank, &L->world_c, nullptr));
+    } else {
+      require(uid != nullptr, "world_size > 1 needs an NCCL unique id");
+      ncclUniqueId id;
+      std::memcpy(&id, uid, sizeof(id));
+      NC(ncclCommInitRank(&L->world_c, L->world, id, rank));
+    }
     NC(ncclCommSplit(L->world_c, L->ep + L->P * L->d, L->t, &L->tp_c, nullptr));
     NC(ncclCommSplit(L->world_c, L->t + L->T * L->d, L->ep, &L->ep_c, nullptr));
     NC(ncclCommSplit(L->world_c, L->t + L->T * L->ep, L->d, &L->expdp_c, nullptr));
@@ -1182,6 +1058,31 @@ int ted_nccl_unique_id(void* out128) {
     std::memcpy(out128, &id, sizeof(id));
   });
 }
+
+}  // extern "C"
+
+namespace ted {
+int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
+                       const ted_flags* flags, const ted_adam_cfg* adam,
+                       const ted_tile_cfg* tiles, double capacity_factor, int shard_optimizer,
+                       int rank, ncclComm_t parent, ted_layer** out) {
+  return guard([&] {
+    require(out != nullptr, "null output pointer");
+    auto* L = new ted_layer();
+    try {
+      create_layer(L, model, topo, flags, adam, tiles, capacity_factor, shard_optimizer, rank,
+                   nullptr, parent);
+      fix_views(L);
+    } catch (...) {
+      delete L;
+      throw;
+    }
+    *out = L;
+  });
+}
+}  // namespace ted
+
+extern "C" {
 
 int ted_layer_create(const ted_model_cfg* model, const ted_topo_cfg* topo,
                      const ted_flags* flags, const ted_adam_cfg* adam,

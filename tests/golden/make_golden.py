@@ -107,6 +107,15 @@ def main():
     losses = np.empty(3)
     assert R.ref_serial_step(2, 8, 2, 8, 7, 2, 3, losses) == 0
     g["serial_losses"] = losses
+    # SerialModel losses for the model-stack parity tests (layers, h, E, n, seed, shards)
+    stacks = [(2, 256, 4, 128, 1, 1), (4, 256, 4, 128, 5, 1), (2, 256, 4, 128, 3, 2),
+              (2, 256, 4, 128, 3, 1)]
+    sl = []
+    for (L_, h_, E_, n_, s_, S_) in stacks:
+        ls = np.empty(3)
+        assert R.ref_serial_step(L_, h_, E_, n_, s_, S_, 3, ls) == 0
+        sl.append([L_, h_, E_, n_, s_, S_] + list(ls))
+    g["stack_serial_losses"] = np.array(sl, np.float64)
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, len(g), "arrays")
 

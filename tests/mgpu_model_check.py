@@ -1,0 +1,71 @@
+"""Multi-GPU parity of the whole model (run under torchrun, one rank per GPU):
+
+    torchrun --nproc-per-node N ... tests/mgpu_model_check.py --tp T --ep P [--zero 0|1]
+
+Every rank sets the FULL reference tensors by name (sliced like slice_tensor), trains 3
+steps on its data shard (index d*EP + e, moe.cpp:229) and rank 0 sums the per-shard losses
+of the t = 0 ranks (the Trainer's loss, moe.cpp:822-831) and compares them with the
+reference SerialModel's losses (tests/golden).  Prints "MGPU-OK <json>"."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tp", type=int, default=2)
+    ap.add_argument("--ep", type=int, default=1)
+    ap.add_argument("--dtd", type=int, default=1)
+    ap.add_argument("--zero", type=int, default=1)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_06318_b200 as ted
+    from tests._stack import golden_losses, stack_batch, stack_params
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    ted.set_device(local)
+    dist.init_process_group("gloo")
+    T, P = args.tp, args.ep
+    D = world // (T * P)
+    shards = P * D
+    layers, h, E, n, seed = 2, 256, 4, 128, 3
+    model = ted.MoeModelConfig(layers, h, E, n, seed)
+    obj = [ted.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    M = ted.TedModel(model, ted.derive_config(world, T, P), ted.RunFlags(dtd=bool(args.dtd)),
+                     shard_optimizer=bool(args.zero), rank=rank, nccl_uid=obj[0])
+    for nm, full in stack_params(ted, model).items():
+        M.set_param(nm, full)
+    t, e, d = rank % T, (rank // T) % P, rank // (T * P)
+    shard = d * P + e
+    a = stack_batch(model, shards)[shard * n:(shard + 1) * n]
+    batch = torch.tensor(a, dtype=torch.float32).bfloat16().cuda()
+    losses = []
+    for _ in range(3):
+        M.step(batch)
+        losses.append(M.loss())
+    allv = [None] * world
+    dist.all_gather_object(allv, (t, losses))
+    M.close()
+    if rank == 0:
+        tot = np.sum([np.array(l) for (tt, l) in allv if tt == 0], axis=0)
+        ref = golden_losses(layers, h, E, n, seed, shards)
+        np.testing.assert_allclose(tot, ref, rtol=2e-2)
+        print("MGPU-OK " + json.dumps({"losses": tot.tolist(), "ref": ref.tolist()}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

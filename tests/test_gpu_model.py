@@ -1,0 +1,51 @@
+"""The whole model (layer stack: attention stand-in + MoE / dense FFN, ted_model_*) on one
+GPU against the reference's own SerialModel losses over 3 training steps (forward, loss,
+backward, AdamW) on identical seeded parameters and batch.  Tolerance: 2e-2 relative per
+step (bf16 storage of activations, weights and gradients; the reference is fp64)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from tests._stack import golden_losses, stack_batch, stack_params  # noqa: E402
+
+TOL = 2e-2
+
+
+@pytest.mark.parametrize("layers,h,E,n,seed", [(2, 256, 4, 128, 1), (4, 256, 4, 128, 5)])
+def test_stack_matches_reference_serial_model(layers, h, E, n, seed):
+    import paper_2303_06318_b200 as ted
+    model = ted.MoeModelConfig(layers, h, E, n, seed)
+    M = ted.TedModel(model, ted.TedConfig())
+    for nm, full in stack_params(ted, model).items():
+        M.set_param(nm, full)
+    batch = torch.tensor(stack_batch(model, 1), dtype=torch.float32).bfloat16().cuda()
+    losses = []
+    for _ in range(3):
+        M.step(batch)
+        losses.append(M.loss())
+    ref = golden_losses(layers, h, E, n, seed, 1)
+    np.testing.assert_allclose(losses, ref, rtol=TOL)
+    M.close()
+
+
+def test_stack_parameters_round_trip_and_update():
+    import paper_2303_06318_b200 as ted
+    model = ted.MoeModelConfig(2, 256, 4, 128, 1)
+    M = ted.TedModel(model, ted.TedConfig())
+    M.init_params(3)
+    w = M.get_param("layer1.ffn.w1").copy()
+    assert w.size == 256 * 1024 and np.abs(w).max() > 0
+    g = np.random.default_rng(0).standard_normal((256, 1024)).astype(np.float32)
+    M.set_param("layer1.ffn.w1", g)
+    back = M.get_param("layer1.ffn.w1").reshape(256, 1024)
+    assert np.max(np.abs(back - g) / (np.abs(g) + 1e-3)) < 1e-2  # bf16 storage
+    batch = torch.randn(128, 256, device="cuda").bfloat16()
+    M.step(batch)
+    assert not np.array_equal(back, M.get_param("layer1.ffn.w1").reshape(256, 1024))
+    assert np.abs(M.get_grad("layer0.attn.w2")).max() > 0
+    assert np.abs(M.get_grad("layer0.expert1.w1")).max() >= 0
+    with pytest.raises(ted.InvalidConfigError):
+        M.set_param("layer0.ffn.w1", g)  # layer 0 is a MoE layer: no dense FFN
+    M.close()

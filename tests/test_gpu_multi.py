@@ -21,11 +21,11 @@ def _port():
     return p
 
 
-def _run(nproc, *args, env=None):
+def _run(nproc, *args, env=None, script="mgpu_layer_check.py"):
     for _attempt in range(3):  # a freshly probed port can be taken before torchrun binds it
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
-               os.path.join(HERE, "mgpu_layer_check.py"), *args]
+               os.path.join(HERE, script), *args]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
                            env=dict(os.environ, **(env or {})))
         if "EADDRINUSE" not in r.stderr + r.stdout:
@@ -60,3 +60,14 @@ def test_four_gpus_corrupt_drop_is_detected():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--corrupt", "1", "--cf", "0")
+
+
+@pytest.mark.parametrize("nproc,tp,ep,zero", [(2, 2, 1, 1), (2, 1, 2, 1), (2, 1, 1, 1),
+                                              (4, 2, 2, 1), (4, 2, 1, 1), (4, 2, 1, 0)])
+def test_model_stack_matches_reference(nproc, tp, ep, zero):
+    """Whole model (attention stand-in + MoE / dense FFN, 2 layers) over TP x EP x DP, with
+    and without ZeRO-1, against the reference SerialModel losses (tests/mgpu_model_check.py)."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    _run(nproc, "--tp", str(tp), "--ep", str(ep), "--zero", str(zero),
+         script="mgpu_model_check.py")
