@@ -211,7 +211,9 @@ int ted_layer_get_routing(ted_layer* L, int32_t* expert, float* prob, int32_t* s
  * moe.cpp:418-426 / :688-696, parallel_linear.cpp:8-40), then the MoE branch on even
  * layers (layer_has_experts) or a dense FFN block on odd layers (moe.cpp:428-433 /
  * :571-580).  Parameters by the reference's names (enumerate_params, moe.cpp:115-147):
- * layer{l}.attn.{w1,b1,w2,b2}, layer{l}.gate.w, layer{l}.expert{e}.*, layer{l}.ffn.*.
+ * layer{l}.attn.{w1,b1,w2,b2}, layer{l}.gate.w, layer{l}.expert{e}.*, layer{l}.ffn.*
+ * (set_param of an expert housed on another EP rank is a no-op, like
+ * Trainer::set_parameter reaching only the owning ranks, moe.cpp:857-868).
  * `batch` is this rank's shard (tokens_per_shard x hidden bf16, device), shard index
  * d*EP + e replicated over the TP group (moe.cpp:229, :266-267).  Loss of this rank =
  * sum(y^2) / (2 N_global) over the last layer's output (moe.cpp:379-381); the Trainer's

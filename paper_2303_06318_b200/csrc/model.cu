@@ -569,6 +569,15 @@ int ted_model_set_param(ted_model* M, const char* name, const float* full) {
     require(parse(M, name, layer, blk, leaf), std::string("no parameter named ") + name);
     if (blk == "gate" || blk.compare(0, 6, "expert") == 0) {
       require(layer % 2 == 0, std::string("no parameter named ") + name);
+      if (blk != "gate") {  // experts housed on other EP ranks: nothing to set here
+        int e = -1;
+        try {
+          e = std::stoi(blk.substr(6));
+        } catch (...) {
+        }
+        require(e >= 0 && e < M->E, std::string("no parameter named ") + name);
+        if (e / (M->E / M->P) != M->ep) return;
+      }
       const int rc = ted_layer_set_param(M->moe[size_t(layer)], moe_name(name).c_str(), full);
       if (rc != TED_OK) throw ConfigError(last_error());
       return;
