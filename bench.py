@@ -385,20 +385,51 @@ def run_ours(args, w, rank, world, local_rank, dist):
     tokens_global = w["tokens"]
     value = tokens_global / (ms / 1e3)
     pk = peaks()
-    # dominant kernel: the expert FFN tcgen05 GEMMs (6 launches / step)
-    gemm_names = ["gemm1_fwd", "gemm2_fwd", "dgrad2", "wgrad2", "dgrad1", "wgrad1"]
-    gemm_ms = sum(stages.get(k, (0.0, 0))[0] for k in gemm_names) / nprof
-    kept_rows = sum(stats["kept_per_expert"][: max(1, w["experts"] // P)])
+    # roofline.  With the expert family unsharded (D = 1) AdamW runs inside the two wgrad
+    # GEMMs and that kernel dominates the step (47 % of the GPU time at C3, N=1,
+    # profiles/r02_ncu_summary.md): it is HBM-bound on the optimizer state.  The four
+    # forward / dgrad GEMMs are reported beside it against the tensor-core peak.
+    def st(k):
+        return stages.get(k, (0.0, 0))[0] / nprof
+    Eloc = max(1, w["experts"] // P)
+    kept_rows = sum(stats["kept_per_expert"][:Eloc])
     f_t = 4 * w["hidden"] // T
-    gemm_flops = 12.0 * kept_rows * w["hidden"] * f_t  # 2 fwd + 4 bwd GEMMs, algorithmic
-    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    h_ = w["hidden"]
+    tc_names = ["gemm1_fwd", "gemm2_fwd", "dgrad2", "dgrad1"]
+    tc_ms = sum(st(k) for k in tc_names)
+    tc_flops = 8.0 * kept_rows * h_ * f_t  # 4 GEMMs x 2 flops x rows x h x f/T, algorithmic
+    tc_ach = tc_flops / (tc_ms / 1e3) / 1e12 if tc_ms > 0 else None
     peak_tc = pk["bf16_tflops_sustained"]
-    traffic = None
+    tj = None
     for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic*.json"))):
         with open(tp) as f:  # from a committed ncu --set full capture of this workload
-            tj = json.load(f)
-        if tj.get("workload") == w["name"] and tj.get("n_gpus", 1) == world:
-            traffic = tj["traffic_bytes_per_launch_mean"]
+            cand = json.load(f)
+        if cand.get("workload") == w["name"] and cand.get("n_gpus", 1) == world:
+            tj = cand
+    roof_tc = {"bound": "tensor", "kernel": "expert FFN fwd + dgrad tcgen05 GEMMs (4/step)",
+               "achieved": tc_ach, "peak": peak_tc, "unit": "TFLOP/s",
+               "frac": (tc_ach / peak_tc) if tc_ach else None,
+               "traffic": (sum(tj["per_launch"][i] for i in (0, 1, 2, 4)) / 4) if tj else None,
+               "flops_per_launch": tc_flops / 4, "ms_per_launch": tc_ms / 4,
+               "peak_source": pk["source"] + " bf16_tflops_sustained"}
+    if D == 1:
+        wg_ms = (st("wgrad1") + st("wgrad2")) / 2
+        params = Eloc * h_ * f_t
+        rows = int(stats["asm_rows"])
+        # 26 B per parameter (fp32 master/m/v read + write, bf16 parameter write) + the
+        # wgrad operands read once (rows x (h + f/T) bf16)
+        wg_bytes = 26.0 * params + 2.0 * rows * (h_ + f_t)
+        wg_ach = wg_bytes / (wg_ms / 1e3) / 1e9 if wg_ms > 0 else None
+        roofline = {"bound": "hbm", "kernel": "wgrad GEMM + fused AdamW (2/step)",
+                    "achieved": wg_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": (wg_ach / pk["hbm_gbs"]) if wg_ach else None,
+                    "traffic": (sum(tj["per_launch"][i] for i in (3, 5)) / 2) if tj else None,
+                    "bytes_per_launch": wg_bytes, "ms_per_launch": wg_ms,
+                    "unit_work": "26 B per parameter + 2 B per operand element",
+                    "peak_source": pk["source"] + " hbm_gbs (copy)"}
+        extra_roof = {"roofline_gemm": roof_tc}
+    else:
+        roofline, extra_roof = roof_tc, {}
     stage_ms = {k: round(v[0] / nprof, 4) for k, v in sorted(stages.items())}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
@@ -411,13 +442,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
                    "step": "fwd+bwd+grad-sync+AdamW",
                    "l2": "no flush: per-step working set (weights+AdamW state+activations) "
                          "> 126 MB L2"},
-        "roofline": {"bound": "tensor", "kernel": "expert FFN tcgen05 grouped GEMMs (6/step)",
-                     "achieved": achieved, "peak": peak_tc, "unit": "TFLOP/s",
-                     "frac": (achieved / peak_tc) if achieved else None, "traffic": traffic,
-                     "traffic_unit": "DRAM bytes per GEMM launch (ncu, mean of the 6)",
-                     "flops_per_launch": gemm_flops / 6,
-                     "peak_source": pk["source"] + " bf16_tflops_sustained",
-                     "flops_per_step": gemm_flops, "ms_per_step": gemm_ms},
+        "roofline": roofline,
+        **extra_roof,
         "stage_ms": stage_ms,
         "gpu_launches": int(launches),
         "host_enqueue_ms_per_step": host_ms,
