@@ -668,59 +668,66 @@ constexpr int kDwTok = 32;  // tokens per dWg partial
 template <int EMAX, int CPT>
 __global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict__ a,
                                                           const float* __restrict__ dl,
-                                                          int64_t n, int h, int E,
+                                                          int64_t n, int h, int E, int tok,
                                                           float* __restrict__ part) {
+  // this CTA sums `tok` tokens (a multiple of kDwTok, staged kDwTok at a time) into one
+  // partial, so the partial buffer stays small next to the activations
   __shared__ float s_dl[kDwTok * EMAX];
-  const int64_t k0 = int64_t(blockIdx.x) * kDwTok;
-  for (int idx = threadIdx.x; idx < kDwTok * EMAX; idx += blockDim.x) {
-    const int t = idx / EMAX, j = idx % EMAX;
-    s_dl[idx] = (k0 + t < n && j < E) ? dl[(k0 + t) * E + j] : 0.f;
-  }
-  __syncthreads();
   const int i0 = (blockIdx.y * blockDim.x + threadIdx.x) * CPT;
-  if (i0 >= h) return;
+  const bool col_ok = i0 < h;
   float acc[CPT][EMAX];
 #pragma unroll
   for (int c = 0; c < CPT; ++c)
 #pragma unroll
     for (int j = 0; j < EMAX; ++j) acc[c][j] = 0.f;
-  const int tn = int(lmin(kDwTok, n - k0));
-  // 8 token rows in flight per thread: loads first, then the FMAs
-  for (int t0 = 0; t0 < tn; t0 += 8) {
-    float xb[8][CPT];
+  for (int64_t k0 = int64_t(blockIdx.x) * tok; k0 < lmin(n, int64_t(blockIdx.x + 1) * tok);
+       k0 += kDwTok) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kDwTok * EMAX; idx += blockDim.x) {
+      const int t = idx / EMAX, j = idx % EMAX;
+      s_dl[idx] = (k0 + t < n && j < E) ? dl[(k0 + t) * E + j] : 0.f;
+    }
+    __syncthreads();
+    if (!col_ok) continue;
+    const int tn = int(lmin(kDwTok, n - k0));
+    // 8 token rows in flight per thread: loads first, then the FMAs
+    for (int t0 = 0; t0 < tn; t0 += 8) {
+      float xb[8][CPT];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int t = t0 + u;
-      const bf16* src = a + (k0 + t) * h + i0;
-      if (t >= tn) {
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u;
+        const bf16* src = a + (k0 + t) * h + i0;
+        if (t >= tn) {
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) xb[u][c] = 0.f;
-      } else if constexpr (CPT == 8) {
-        float f[8];
-        unpack8(ldg_stream(src), f);
+          for (int c = 0; c < CPT; ++c) xb[u][c] = 0.f;
+        } else if constexpr (CPT == 8) {
+          float f[8];
+          unpack8(ldg_stream(src), f);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) xb[u][c] = f[c];
-      } else if constexpr (CPT == 4) {
-        const uint2 uu = *reinterpret_cast<const uint2*>(src);
-        const float2 f0 = bf2_to_f2(uu.x), f1 = bf2_to_f2(uu.y);
-        xb[u][0] = f0.x; xb[u][1] = f0.y; xb[u][2] = f1.x; xb[u][3] = f1.y;
-      } else if constexpr (CPT == 2) {
-        const float2 f0 = bf2_to_f2(*reinterpret_cast<const uint32_t*>(src));
-        xb[u][0] = f0.x; xb[u][1] = f0.y;
-      } else {
-        xb[u][0] = __bfloat162float(src[0]);
+          for (int c = 0; c < 8; ++c) xb[u][c] = f[c];
+        } else if constexpr (CPT == 4) {
+          const uint2 uu = *reinterpret_cast<const uint2*>(src);
+          const float2 f0 = bf2_to_f2(uu.x), f1 = bf2_to_f2(uu.y);
+          xb[u][0] = f0.x; xb[u][1] = f0.y; xb[u][2] = f1.x; xb[u][3] = f1.y;
+        } else if constexpr (CPT == 2) {
+          const float2 f0 = bf2_to_f2(*reinterpret_cast<const uint32_t*>(src));
+          xb[u][0] = f0.x; xb[u][1] = f0.y;
+        } else {
+          xb[u][0] = __bfloat162float(src[0]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (t0 + u >= tn) break;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+          for (int j = 0; j < EMAX; ++j)
+            acc[c][j] = fmaf(xb[u][c], s_dl[(t0 + u) * EMAX + j], acc[c][j]);
       }
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (t0 + u >= tn) break;
-#pragma unroll
-      for (int c = 0; c < CPT; ++c)
-#pragma unroll
-        for (int j = 0; j < EMAX; ++j)
-          acc[c][j] = fmaf(xb[u][c], s_dl[(t0 + u) * EMAX + j], acc[c][j]);
-    }
   }
+  if (!col_ok) return;
   float* out = part + (int64_t(blockIdx.x) * h + i0) * E;
 #pragma unroll
   for (int c = 0; c < CPT; ++c)
@@ -1186,29 +1193,40 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
   return cudaGetLastError();
 }
 
+// tokens per dWg partial: enough CTAs to fill the GPU (4 per SM), as few partials as that
+// allows (the partial buffer is h x E floats per token chunk)
+int dw_tok(int64_t n, int h, int E) {
+  const int cpt = E <= 8 ? 8 : (E <= 16 ? 4 : (E <= 32 ? 2 : 1));
+  const int64_t ycta = ceil_div(h, 128 * cpt);
+  const int64_t sub = std::max<int64_t>(1, ceil_div(n, kDwTok));
+  const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(sub, 4 * sm_count() / ycta));
+  return int(ceil_div(sub, chunks) * kDwTok);
+}
+
 size_t gate_dw_part_floats(int64_t n, int h, int E) {
-  return size_t(ceil_div(n, kDwTok)) * size_t(h) * size_t(E);
+  return size_t(std::max<int64_t>(1, ceil_div(n, dw_tok(n, h, E)))) * size_t(h) * size_t(E);
 }
 
 cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n, int h, int E,
                                  float* part, bf16* dwg, cudaStream_t s) {
   if (E > 64 || h % 8 != 0) return cudaErrorInvalidValue;
-  const int nb = ceil_div(n, kDwTok);
+  const int tok = dw_tok(n, h, E);
+  const int nb = ceil_div(n, tok);
   if (nb == 0) {
     return cudaMemsetAsync(dwg, 0, sizeof(bf16) * size_t(h) * E, s);
   }
   if (E <= 8) {
     gate_bwd_dw_kernel<8, 8><<<dim3(nb, ceil_div(h, 128 * 8)), 128, 0, s>>>(a, dlogits, n, h, E,
-                                                                          part);
+                                                                          tok, part);
   } else if (E <= 16) {
     gate_bwd_dw_kernel<16, 4><<<dim3(nb, ceil_div(h, 128 * 4)), 128, 0, s>>>(a, dlogits, n, h,
-                                                                           E, part);
+                                                                           E, tok, part);
   } else if (E <= 32) {
     gate_bwd_dw_kernel<32, 2><<<dim3(nb, ceil_div(h, 128 * 2)), 128, 0, s>>>(a, dlogits, n, h,
-                                                                           E, part);
+                                                                           E, tok, part);
   } else {
     gate_bwd_dw_kernel<64, 1><<<dim3(nb, ceil_div(h, 128)), 128, 0, s>>>(a, dlogits, n, h, E,
-                                                                       part);
+                                                                       tok, part);
   }
   const int64_t M = int64_t(h) * E;
   sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, nb, nullptr, int(M), 1, dwg, 0);
