@@ -598,69 +598,104 @@ __device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h
   return base + (R.pull_base[c * R.E + e] + r) * h;
 }
 
-template <int EMAX>
-__global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
-                                                               const float* __restrict__ dl,
-                                                               const bf16* __restrict__ wg,
-                                                               int64_t n, int h, int E, int HC,
-                                                               bf16* __restrict__ da) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  bf16* s_wg = reinterpret_cast<bf16*>(smem);  // [EMAX][HC]
+// da[k] = dX(k) + dlogits[k] . Wg^T on the tensor cores (gate_backward's dinput,
+// moe.cpp:206, plus the dispatch gradient moe.cpp:685): per warp 16 tokens x 32 columns
+// per step as four mma.sync.m16n8k16 n-tiles over K = experts (16 per k-step).  dlogits
+// (fp32) enter as a bf16 hi + lo pair (two MMAs, ~2^-17 relative), Wg (bf16) exactly,
+// fp32 accumulation.  The n-tiles' columns are permuted so each lane ends with 8
+// consecutive output columns of its two token rows: dX is read and da written as 16 B
+// vectors.  Warps 0-3 / 4-7 take the two halves of the columns of a 64-token block.
+template <int KS>
+__global__ void __launch_bounds__(kThreads, 3) gate_bwd_dx_mma_kernel(const RowSrc R,
+                                                                   const float* __restrict__ dl,
+                                                                   const bf16* __restrict__ wg,
+                                                                   int64_t n, int h, int E,
+                                                                   bf16* __restrict__ da) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
-  for (int c0 = 0; c0 < h; c0 += HC) {
-    const int hc = min(HC, h - c0);
-    __syncthreads();
-    stage_wg<EMAX>(wg, E, c0, hc, HC, s_wg);
-    __syncthreads();
-    for (int t = 0; t < kWarpTok; ++t) {
-      const int64_t k = tok0 + t;
-      if (k >= n) break;
-      const float d0 = lane < E ? dl[k * E + lane] : 0.f;
-      const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
-      const bf16* row = src_row(R, k, h, 0);
-      const bf16* src = row ? row + c0 : nullptr;
-      const bf16* row1 = R.nsum > 1 && row ? src_row(R, k, h, 1) : nullptr;
-      const bf16* src1 = row1 ? row1 + c0 : nullptr;
-      for (int base = lane * 8; base < hc; base += 256 * 4) {
-        uint4 xv[4], xv1[4];
+  const int g = lane >> 2, c = lane & 3;
+  const int tt = warp & 3, half = warp >> 2;
+  const int64_t kr[2] = {int64_t(blockIdx.x) * kRouteBlock + tt * 16 + g,
+                         int64_t(blockIdx.x) * kRouteBlock + tt * 16 + g + 8};
+  uint32_t ahi[KS][4], alo[KS][4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i0 = base + u * 256;
-          xv[u] = (src && i0 < hc) ? ldg_stream(src + i0) : make_uint4(0, 0, 0, 0);
-          xv1[u] = (src1 && i0 < hc) ? ldg_stream(src1 + i0) : make_uint4(0, 0, 0, 0);
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = q & 1, pq = q >> 1;  // a0: (row g, k 2c), a1: (g+8, 2c), a2: (g, 2c+8) ...
+      const int e0 = 16 * ks + 2 * c + 8 * pq;
+      const int64_t k = kr[r];
+      const float v0 = (k < n && e0 < E) ? dl[k * E + e0] : 0.f;
+      const float v1 = (k < n && e0 + 1 < E) ? dl[k * E + e0 + 1] : 0.f;
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+      const float2 hf = __bfloat1622float2(hi);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+      ahi[ks][q] = *reinterpret_cast<const uint32_t*>(&hi);
+      alo[ks][q] = *reinterpret_cast<const uint32_t*>(&lo);
+    }
+  // dX rows of this lane's two tokens (replica 0; further TP replicas are summed below)
+  const bf16* rows[2] = {kr[0] < n ? src_row(R, kr[0], h, 0) : nullptr,
+                         kr[1] < n ? src_row(R, kr[1], h, 0) : nullptr};
+  const int hh = h / 2;
+  const int cbeg = half * hh, cend = (half + 1) * hh;
+  auto load_x = [&](int col0, uint4 (&x)[2]) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+      x[r] = rows[r] ? ldg_stream(rows[r] + col0 + 8 * c) : make_uint4(0, 0, 0, 0);
+  };
+  uint4 xcur[2], xnxt[2];
+  load_x(cbeg, xcur);
+  for (int col0 = cbeg; col0 < cend; col0 += 32) {
+    if (col0 + 32 < cend) load_x(col0 + 32, xnxt);  // next step's dX in flight
+    float acc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+      // B column g of this n-tile is output column col0 + 8 (g >> 1) + 2 nt + (g & 1)
+      const bf16* wrow = wg + int64_t(col0 + 8 * (g >> 1) + 2 * nt + (g & 1)) * E;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        uint32_t b[2];
+#pragma unroll
+        for (int pq = 0; pq < 2; ++pq) {
+          const int e0 = 16 * ks + 2 * c + 8 * pq;
+          const bf16 w0 = e0 < E ? wrow[e0] : __float2bfloat16(0.f);
+          const bf16 w1 = e0 + 1 < E ? wrow[e0 + 1] : __float2bfloat16(0.f);
+          __nv_bfloat162 wv;
+          wv.x = w0;
+          wv.y = w1;
+          b[pq] = *reinterpret_cast<const uint32_t*>(&wv);
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i0 = base + u * 256;
-          if (i0 >= hc) continue;
-          float acc[8];
-          unpack8(xv[u], acc);
-          if (src1) {  // TP partial sums of the column-parallel dgrad (parallel_linear.cpp:19)
-            float p1[8];
-            unpack8(xv1[u], p1);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] += p1[q];
-            for (int rep = 2; rep < R.nsum; ++rep) {
-              unpack8(ldg_stream(src_row(R, k, h, rep) + c0 + i0), p1);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) acc[q] += p1[q];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < EMAX; ++j) {
-            const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);
-            float wv[8];
-            unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = fmaf(dj, wv[q], acc[q]);
-          }
-          *reinterpret_cast<uint4*>(da + k * h + c0 + i0) = pack8(acc);
-        }
+        mma_bf16_16816(acc[nt], ahi[ks][0], ahi[ks][1], ahi[ks][2], ahi[ks][3], b[0], b[1]);
+        mma_bf16_16816(acc[nt], alo[ks][0], alo[ks][1], alo[ks][2], alo[ks][3], b[0], b[1]);
       }
     }
+    // lane (g, c): row r's columns col0 + 8c .. +7 = acc[0..3][2r], acc[0..3][2r + 1]
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (kr[r] >= n) continue;
+      float o[8];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        o[2 * nt] = acc[nt][2 * r];
+        o[2 * nt + 1] = acc[nt][2 * r + 1];
+      }
+      float x[8];
+      unpack8(xcur[r], x);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] += x[q];
+      if (rows[r] != nullptr)  // TP partial sums of the column-parallel dgrad (:19)
+        for (int rep = 1; rep < R.nsum; ++rep) {
+          unpack8(ldg_stream(src_row(R, kr[r], h, rep) + col0 + 8 * c), x);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[q] += x[q];
+        }
+      *reinterpret_cast<uint4*>(da + kr[r] * h + col0 + 8 * c) = pack8(o);
+    }
+    xcur[0] = xnxt[0];
+    xcur[1] = xnxt[1];
   }
 }
+
 
 constexpr int kDwTok = 32;  // tokens per dWg partial
 
@@ -1177,18 +1212,9 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
   if (E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-#define TED_GBX(EM)                                                                            \
-  {                                                                                            \
-    const int HC = gate_hc<EM>(h);                                                             \
-    const size_t sm = size_t(EM) * HC * 2;                                                     \
-    smem_attr(gate_bwd_dx_kernel<EM>, sm);                                                     \
-    gate_bwd_dx_kernel<EM><<<grid, kThreads, sm, s>>>(src, dlogits, wg, n, h, E, HC, da);     \
-  }
-  if (E <= 8) TED_GBX(8)
-  else if (E <= 16) TED_GBX(16)
-  else if (E <= 32) TED_GBX(32)
-  else TED_GBX(64)
-#undef TED_GBX
+  if (E <= 16) gate_bwd_dx_mma_kernel<1><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  else if (E <= 32) gate_bwd_dx_mma_kernel<2><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  else gate_bwd_dx_mma_kernel<4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
   count_launch(1);
   return cudaGetLastError();
 }
