@@ -373,7 +373,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
                 "a2a_rows_offrank_rank0": sx["a2a_rows_offrank"],
                 "dtd_allgather_bytes_fwd_rank0_ledger": sx["ag_bytes_fwd"],
                 "nvlink_bytes_fwd_rank0": sx["peer_bytes_fwd"],
-                "exchange_ms_rank0": ex, "exchange_ms_total_rank0": round(sum(ex.values()), 4)}
+                "exchange_ms_rank0": ex, "exchange_ms_total_rank0": round(sum(ex.values()), 4),
+                "stage_ms_rank0": {k: round(v, 4) for k, v in sorted(stx.items())}}
             if Lx is not L:
                 Lx.close()
         dtd_cmp = arms
