@@ -605,8 +605,8 @@ __device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h
 // fp32 accumulation.  The n-tiles' columns are permuted so each lane ends with 8
 // consecutive output columns of its two token rows: dX is read and da written as 16 B
 // vectors.  Warps 0-3 / 4-7 take the two halves of the columns of a 64-token block.
-template <int KS>
-__global__ void __launch_bounds__(kThreads, 3) gate_bwd_dx_mma_kernel(const RowSrc R,
+template <int KS, int NS, int D>
+__global__ void __launch_bounds__(kThreads, 2) gate_bwd_dx_mma_kernel(const RowSrc R,
                                                                    const float* __restrict__ dl,
                                                                    const bf16* __restrict__ wg,
                                                                    int64_t n, int h, int E,
@@ -632,67 +632,81 @@ __global__ void __launch_bounds__(kThreads, 3) gate_bwd_dx_mma_kernel(const RowS
       ahi[ks][q] = *reinterpret_cast<const uint32_t*>(&hi);
       alo[ks][q] = *reinterpret_cast<const uint32_t*>(&lo);
     }
-  // dX rows of this lane's two tokens (replica 0; further TP replicas are summed below)
-  const bf16* rows[2] = {kr[0] < n ? src_row(R, kr[0], h, 0) : nullptr,
-                         kr[1] < n ? src_row(R, kr[1], h, 0) : nullptr};
+  // dX rows of this lane's two tokens, replicas 0..NS-1 prefetched D steps (of 32 columns)
+  // ahead -- on more than one GPU these are NVLink loads from the TP replicas' buffers
+  const int nsum = R.nsum < 1 ? 1 : R.nsum;
+  const bf16* rows[2][NS];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int rep = 0; rep < NS; ++rep)
+      rows[r][rep] = (kr[r] < n && rep < nsum) ? src_row(R, kr[r], h, rep) : nullptr;
   const int hh = h / 2;
   const int cbeg = half * hh, cend = (half + 1) * hh;
-  auto load_x = [&](int col0, uint4 (&x)[2]) {
+  uint4 X[D][2][NS];
+  auto load_x = [&](int col0, uint4 (&x)[2][NS]) {
 #pragma unroll
     for (int r = 0; r < 2; ++r)
-      x[r] = rows[r] ? ldg_stream(rows[r] + col0 + 8 * c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int rep = 0; rep < NS; ++rep)
+        x[r][rep] = (rows[r][rep] && col0 < cend) ? ldg_stream(rows[r][rep] + col0 + 8 * c)
+                                                  : make_uint4(0, 0, 0, 0);
   };
-  uint4 xcur[2], xnxt[2];
-  load_x(cbeg, xcur);
-  for (int col0 = cbeg; col0 < cend; col0 += 32) {
-    if (col0 + 32 < cend) load_x(col0 + 32, xnxt);  // next step's dX in flight
-    float acc[4][4];
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-      // B column g of this n-tile is output column col0 + 8 (g >> 1) + 2 nt + (g & 1)
-      const bf16* wrow = wg + int64_t(col0 + 8 * (g >> 1) + 2 * nt + (g & 1)) * E;
+  for (int u = 0; u < D; ++u) load_x(cbeg + 32 * u, X[u]);
+  for (int cb = cbeg; cb < cend; cb += 32 * D) {
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        uint32_t b[2];
-#pragma unroll
-        for (int pq = 0; pq < 2; ++pq) {
-          const int e0 = 16 * ks + 2 * c + 8 * pq;
-          const bf16 w0 = e0 < E ? wrow[e0] : __float2bfloat16(0.f);
-          const bf16 w1 = e0 + 1 < E ? wrow[e0 + 1] : __float2bfloat16(0.f);
-          __nv_bfloat162 wv;
-          wv.x = w0;
-          wv.y = w1;
-          b[pq] = *reinterpret_cast<const uint32_t*>(&wv);
-        }
-        mma_bf16_16816(acc[nt], ahi[ks][0], ahi[ks][1], ahi[ks][2], ahi[ks][3], b[0], b[1]);
-        mma_bf16_16816(acc[nt], alo[ks][0], alo[ks][1], alo[ks][2], alo[ks][3], b[0], b[1]);
-      }
-    }
-    // lane (g, c): row r's columns col0 + 8c .. +7 = acc[0..3][2r], acc[0..3][2r + 1]
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      if (kr[r] >= n) continue;
-      float o[8];
+    for (int u = 0; u < D; ++u) {
+      const int col0 = cb + 32 * u;
+      float acc[4][4];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
-        o[2 * nt] = acc[nt][2 * r];
-        o[2 * nt + 1] = acc[nt][2 * r + 1];
-      }
-      float x[8];
-      unpack8(xcur[r], x);
+        acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+        // B column g of this n-tile is output column col0 + 8 (g >> 1) + 2 nt + (g & 1)
+        const bf16* wrow = wg + int64_t(col0 + 8 * (g >> 1) + 2 * nt + (g & 1)) * E;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) o[q] += x[q];
-      if (rows[r] != nullptr)  // TP partial sums of the column-parallel dgrad (:19)
-        for (int rep = 1; rep < R.nsum; ++rep) {
-          unpack8(ldg_stream(src_row(R, kr[r], h, rep) + col0 + 8 * c), x);
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t b[2];
+#pragma unroll
+          for (int pq = 0; pq < 2; ++pq) {
+            const int e0 = 16 * ks + 2 * c + 8 * pq;
+            const bf16 w0 = e0 < E ? wrow[e0] : __float2bfloat16(0.f);
+            const bf16 w1 = e0 + 1 < E ? wrow[e0 + 1] : __float2bfloat16(0.f);
+            __nv_bfloat162 wv;
+            wv.x = w0;
+            wv.y = w1;
+            b[pq] = *reinterpret_cast<const uint32_t*>(&wv);
+          }
+          mma_bf16_16816(acc[nt], ahi[ks][0], ahi[ks][1], ahi[ks][2], ahi[ks][3], b[0], b[1]);
+          mma_bf16_16816(acc[nt], alo[ks][0], alo[ks][1], alo[ks][2], alo[ks][3], b[0], b[1]);
+        }
+      }
+      // lane (g, c): row r's columns col0 + 8c .. +7 = acc[0..3][2r], acc[0..3][2r + 1]
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (kr[r] >= n) continue;
+        float o[8], x[8];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          o[2 * nt] = acc[nt][2 * r];
+          o[2 * nt + 1] = acc[nt][2 * r + 1];
+        }
+#pragma unroll
+        for (int rep = 0; rep < NS; ++rep) {  // TP partial sums (parallel_linear.cpp:19)
+          unpack8(X[u][r][rep], x);
 #pragma unroll
           for (int q = 0; q < 8; ++q) o[q] += x[q];
         }
-      *reinterpret_cast<uint4*>(da + kr[r] * h + col0 + 8 * c) = pack8(o);
+        if (rows[r][0] != nullptr)
+          for (int rep = NS; rep < nsum; ++rep) {  // TP > NS: the remaining replicas
+            unpack8(ldg_stream(src_row(R, kr[r], h, rep) + col0 + 8 * c), x);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] += x[q];
+          }
+        *reinterpret_cast<uint4*>(da + kr[r] * h + col0 + 8 * c) = pack8(o);
+      }
+      load_x(col0 + 32 * D, X[u]);  // refill this ring slot D steps ahead
     }
-    xcur[0] = xnxt[0];
-    xcur[1] = xnxt[1];
   }
 }
 
@@ -1212,9 +1226,21 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
   if (E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  if (E <= 16) gate_bwd_dx_mma_kernel<1><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
-  else if (E <= 32) gate_bwd_dx_mma_kernel<2><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
-  else gate_bwd_dx_mma_kernel<4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  // NS replicas of each dX row prefetched D steps ahead (1 = single GPU / reduced rows,
+  // 2 = the TP-2 partial sums of the peer-memory exchange)
+#define TED_GBX(KS)                                                                          \
+  if (src.nsum >= 2)                                                                         \
+    gate_bwd_dx_mma_kernel<KS, 2, 2><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da); \
+  else                                                                                       \
+    gate_bwd_dx_mma_kernel<KS, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  if (E <= 16) {
+    TED_GBX(1)
+  } else if (E <= 32) {
+    TED_GBX(2)
+  } else {
+    TED_GBX(4)
+  }
+#undef TED_GBX
   count_launch(1);
   return cudaGetLastError();
 }
