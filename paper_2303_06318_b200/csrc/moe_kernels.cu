@@ -605,6 +605,75 @@ __device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h
 // fp32 accumulation.  The n-tiles' columns are permuted so each lane ends with 8
 // consecutive output columns of its two token rows: dX is read and da written as 16 B
 // vectors.  Warps 0-3 / 4-7 take the two halves of the columns of a 64-token block.
+// Pull variant for the peer-memory exchange (TP > 1: every dX row is the sum of T partial
+// rows read over NVLink): one token row per warp-iteration, 512 B contiguous per warp load
+// and four of them in flight per replica, dl . Wg^T by FMAs from smem-staged Wg.  Long
+// contiguous remote reads beat the MMA variant's 64 B row segments there (0.36 vs 0.44 ms
+// at C3 on 4 GPUs).
+template <int EMAX>
+__global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
+                                                               const float* __restrict__ dl,
+                                                               const bf16* __restrict__ wg,
+                                                               int64_t n, int h, int E, int HC,
+                                                               bf16* __restrict__ da) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  bf16* s_wg = reinterpret_cast<bf16*>(smem);  // [EMAX][HC]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock + warp * kWarpTok;
+  for (int c0 = 0; c0 < h; c0 += HC) {
+    const int hc = min(HC, h - c0);
+    __syncthreads();
+    stage_wg<EMAX>(wg, E, c0, hc, HC, s_wg);
+    __syncthreads();
+    for (int t = 0; t < kWarpTok; ++t) {
+      const int64_t k = tok0 + t;
+      if (k >= n) break;
+      const float d0 = lane < E ? dl[k * E + lane] : 0.f;
+      const float d1 = lane + 32 < E ? dl[k * E + lane + 32] : 0.f;
+      const bf16* row = src_row(R, k, h, 0);
+      const bf16* src = row ? row + c0 : nullptr;
+      const bf16* row1 = R.nsum > 1 && row ? src_row(R, k, h, 1) : nullptr;
+      const bf16* src1 = row1 ? row1 + c0 : nullptr;
+      for (int base = lane * 8; base < hc; base += 256 * 4) {
+        uint4 xv[4], xv1[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i0 = base + u * 256;
+          xv[u] = (src && i0 < hc) ? ldg_stream(src + i0) : make_uint4(0, 0, 0, 0);
+          xv1[u] = (src1 && i0 < hc) ? ldg_stream(src1 + i0) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i0 = base + u * 256;
+          if (i0 >= hc) continue;
+          float acc[8];
+          unpack8(xv[u], acc);
+          if (src1) {  // TP partial sums of the column-parallel dgrad (parallel_linear.cpp:19)
+            float p1[8];
+            unpack8(xv1[u], p1);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] += p1[q];
+            for (int rep = 2; rep < R.nsum; ++rep) {
+              unpack8(ldg_stream(src_row(R, k, h, rep) + c0 + i0), p1);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[q] += p1[q];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < EMAX; ++j) {
+            const float dj = __shfl_sync(FULL, j < 32 ? d0 : d1, j & 31);
+            float wv[8];
+            unpack8(*reinterpret_cast<const uint4*>(s_wg + j * HC + i0), wv);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = fmaf(dj, wv[q], acc[q]);
+          }
+          *reinterpret_cast<uint4*>(da + k * h + c0 + i0) = pack8(acc);
+        }
+      }
+    }
+  }
+}
+
 template <int KS, int NS, int D>
 __global__ void __launch_bounds__(kThreads, 2) gate_bwd_dx_mma_kernel(const RowSrc R,
                                                                    const float* __restrict__ dl,
@@ -1228,19 +1297,26 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
   if (grid == 0) return cudaSuccess;
   // NS replicas of each dX row prefetched D steps ahead (1 = single GPU / reduced rows,
   // 2 = the TP-2 partial sums of the peer-memory exchange)
-#define TED_GBX(KS)                                                                          \
-  if (src.nsum >= 2)                                                                         \
-    gate_bwd_dx_mma_kernel<KS, 2, 2><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da); \
-  else                                                                                       \
-    gate_bwd_dx_mma_kernel<KS, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
-  if (E <= 16) {
-    TED_GBX(1)
-  } else if (E <= 32) {
-    TED_GBX(2)
-  } else {
-    TED_GBX(4)
+  if (src.nsum >= 2) {  // NVLink pulls of TP partials: the row-streaming variant
+#define TED_GBX(EM)                                                                            \
+  {                                                                                            \
+    const int HC = gate_hc<EM>(h);                                                             \
+    const size_t sm = size_t(EM) * HC * 2;                                                     \
+    smem_attr(gate_bwd_dx_kernel<EM>, sm);                                                     \
+    gate_bwd_dx_kernel<EM><<<grid, kThreads, sm, s>>>(src, dlogits, wg, n, h, E, HC, da);     \
   }
+    if (E <= 8) TED_GBX(8)
+    else if (E <= 16) TED_GBX(16)
+    else if (E <= 32) TED_GBX(32)
+    else TED_GBX(64)
 #undef TED_GBX
+  } else if (E <= 16) {
+    gate_bwd_dx_mma_kernel<1, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  } else if (E <= 32) {
+    gate_bwd_dx_mma_kernel<2, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  } else {
+    gate_bwd_dx_mma_kernel<4, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+  }
   count_launch(1);
   return cudaGetLastError();
 }
