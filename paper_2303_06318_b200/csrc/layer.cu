@@ -62,11 +62,14 @@ struct ted_layer {
   // peer-memory exchange: IPC mappings of every plane rank's assembled buffers
   bool direct = false;
   int plane_rank = 0, plane_size = 1;
-  DevBuf<unsigned long long> peer_tab;  // [4][plane]: x_asm, dfe_asm, fe_asm, dx_asm
+  DevBuf<unsigned long long> peer_tab;  // [5][plane]: x_asm, dfe_asm, fe_asm, dx_asm, flags
   std::vector<void*> ipc_opened;
   DevBuf<long long> disp_base;  // [E] dispatch rows, then [Tc][E] pull rows
   HostBuf<long long> h_tabs;
   DevBuf<int> bar;
+  DevBuf<unsigned> bar_flags;  // plane barrier: slot r written by plane member r (IPC-mapped)
+  unsigned bar_epoch = 0;
+  bool nccl_barrier = false;
 
   // parameters: expert family (local experts: w1,b1,w2,b2 each) + non-expert (gate)
   Family fam_exp, fam_non;
@@ -273,7 +276,13 @@ void a2a_return(ted_layer* L, const bf16* asm_rows, bf16* home_rows, cudaStream_
 
 // stream-ordered barrier over the TP x EP plane (all writers' kernels are fenced)
 void plane_barrier(ted_layer* L, cudaStream_t s) {
-  NC(ncclAllReduce(L->bar.p, L->bar.p, 1, ncclInt32, ncclSum, L->plane_c, s));
+  if (L->nccl_barrier) {  // TED_BARRIER=nccl: stream-ordered 1-int all-reduce
+    NC(ncclAllReduce(L->bar.p, L->bar.p, 1, ncclInt32, ncclSum, L->plane_c, s));
+    return;
+  }
+  check(plane_barrier_peer(L->peer_tab.p + size_t(4) * L->plane_size, L->plane_size,
+                           L->plane_rank, ++L->bar_epoch, s),
+        "plane_barrier_peer");
 }
 
 const unsigned long long* peer_table(ted_layer* L, int which) {
@@ -861,27 +870,32 @@ void setup_peer_exchange(ted_layer* L) {
   L->h_tabs.alloc(size_t(L->E) * (1 + L->Tc));
   L->bar.alloc(1);
   L->bar.zero();
-  bf16* mine[4] = {L->x_asm.p, L->dfe_asm.p, L->fe_asm.p, L->dx_asm.p};
+  L->bar_flags.alloc(size_t(L->plane_size));
+  L->bar_flags.zero();
+  const char* bv = std::getenv("TED_BARRIER");
+  L->nccl_barrier = bv && std::strcmp(bv, "nccl") == 0;
+  constexpr int NB = 5;  // x_asm, dfe_asm, fe_asm, dx_asm, barrier flags
+  void* mine[NB] = {L->x_asm.p, L->dfe_asm.p, L->fe_asm.p, L->dx_asm.p, L->bar_flags.p};
   const int PS = L->plane_size;
   const size_t HB = sizeof(cudaIpcMemHandle_t);
-  std::vector<char> hmine(4 * HB), hall(size_t(PS) * 4 * HB);
-  for (int b = 0; b < 4; ++b)
+  std::vector<char> hmine(NB * HB), hall(size_t(PS) * NB * HB);
+  for (int b = 0; b < NB; ++b)
     CU(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(hmine.data() + b * HB), mine[b]));
   DevBuf<char> dh;
   dh.alloc(hall.size());
-  CU(cudaMemcpy(dh.p + size_t(L->plane_rank) * 4 * HB, hmine.data(), 4 * HB,
+  CU(cudaMemcpy(dh.p + size_t(L->plane_rank) * NB * HB, hmine.data(), NB * HB,
                 cudaMemcpyHostToDevice));
-  NC(ncclAllGather(dh.p + size_t(L->plane_rank) * 4 * HB, dh.p, 4 * HB, ncclChar, L->plane_c,
+  NC(ncclAllGather(dh.p + size_t(L->plane_rank) * NB * HB, dh.p, NB * HB, ncclChar, L->plane_c,
                    nullptr));
   CU(cudaDeviceSynchronize());
   CU(cudaMemcpy(hall.data(), dh.p, hall.size(), cudaMemcpyDeviceToHost));
-  std::vector<unsigned long long> tab(size_t(4) * PS);
+  std::vector<unsigned long long> tab(size_t(NB) * PS);
   for (int r = 0; r < PS; ++r)
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       void* ptr = mine[b];
       if (r != L->plane_rank) {
         cudaIpcMemHandle_t hd;
-        std::memcpy(&hd, hall.data() + (size_t(r) * 4 + b) * HB, HB);
+        std::memcpy(&hd, hall.data() + (size_t(r) * NB + b) * HB, HB);
         CU(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
         L->ipc_opened.push_back(ptr);
       }

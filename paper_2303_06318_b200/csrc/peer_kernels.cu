@@ -251,6 +251,40 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
   return cudaGetLastError();
 }
 
+// Plane barrier over NVLink peer memory: thread i publishes `epoch` into slot `me` of
+// member i's flag array (system-scope release after a system fence, so every earlier
+// peer store of this GPU is visible first), then waits until member i's epoch has
+// arrived in this GPU's own array (system-scope acquire).  A member that never arrives
+// turns into a trapped kernel after ~20 s instead of a hung GPU.
+__global__ void plane_barrier_kernel(const unsigned long long* __restrict__ flags, int PS,
+                                     int me, unsigned epoch) {
+  const int i = threadIdx.x;
+  __threadfence_system();
+  __syncthreads();
+  if (i < PS) {
+    unsigned* dst = reinterpret_cast<unsigned*>(flags[i]) + me;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
+    const unsigned* mine = reinterpret_cast<const unsigned*>(flags[me]) + i;
+    const long long t0 = clock64();
+    unsigned v = 0;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if (int(v - epoch) >= 0) break;
+      if (clock64() - t0 > (1ll << 35)) __trap();  // ~20 s at 1.9 GHz: a peer is gone
+    }
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me, unsigned epoch,
+                               cudaStream_t s) {
+  if (PS < 1 || PS > 1024) return cudaErrorInvalidValue;
+  plane_barrier_kernel<<<1, ((PS + 31) / 32) * 32, 0, s>>>(flags, PS, me, epoch);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t combine_pull(const RowSrc& src, const float* prob, int64_t n, int h, bf16* y,
                          bf16* fhome, float* loss_part, cudaStream_t s) {
   if (h % 8 != 0 || src.peers == nullptr) return cudaErrorInvalidValue;
