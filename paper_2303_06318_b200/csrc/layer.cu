@@ -108,7 +108,13 @@ struct ted_layer {
     unsigned long long launches = 0;
     std::vector<cudaEvent_t> evs;  // timing event nodes (timed graph only)
     std::vector<const char*> names;
-  } g_plain;
+    unsigned long long used = 0;  // last use (LRU among the cached graphs)
+  };
+  // one graph per (input, output, input-gradient) buffer triple, so callers that double
+  // buffer their inputs (H2D of step i+1 under step i) replay without re-capturing
+  static constexpr int kGraphs = 4;
+  Graph graphs[kGraphs];
+  unsigned long long graph_clock = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
   size_t side_used = 0;
 
@@ -1120,7 +1126,7 @@ int ted_layer_create(const ted_model_cfg* model, const ted_topo_cfg* topo,
 void ted_layer_destroy(ted_layer* L) {
   if (!L) return;
   cudaDeviceSynchronize();
-  graph_reset(L->g_plain);
+  for (auto& g : L->graphs) graph_reset(g);
   for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
   for (auto& pr : L->side_evs) {
     cudaEventDestroy(pr.first);
@@ -1317,8 +1323,18 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
     if (L->local && L->hs && L->use_graph && !L->timing) {
       family_reset_if_needed(L->fam_non, ms);  // set_param resets stay outside the graph
       family_reset_if_needed(L->fam_exp, ms);
-      ted_layer::Graph& g = L->g_plain;
-      if (!g.exec || g.a != a || g.y != y || g.da != da) graph_capture(L, g, a, y, da);
+      ted_layer::Graph* hit = nullptr;
+      ted_layer::Graph* lru = &L->graphs[0];
+      for (auto& c : L->graphs) {
+        if (c.exec && c.a == a && c.y == y && c.da == da) hit = &c;
+        if (c.used < lru->used) lru = &c;
+      }
+      if (!hit) {
+        hit = lru;
+        graph_capture(L, *hit, a, y, da);
+      }
+      ted_layer::Graph& g = *hit;
+      g.used = ++L->graph_clock;
       CU(cudaGraphLaunch(g.exec, L->hs));
       count_launch(int(g.launches));
       L->fam_non.steps += 1;
