@@ -499,6 +499,68 @@ def run_ours(args, w, rank, world, local_rank, dist):
         L.close()
 
 
+def run_model_stack(args, rank, world, local_rank, dist):
+    """configs[3] (C4): a full training step of a layer stack (attention stand-in + MoE on
+    even layers / dense FFN on odd layers, ted_model_*) with the tiled AdamW and ZeRO-1,
+    16 experts, d=4096, 32768 tokens in total, TP=2 x EP=2 x DP=N/4 (fewer GPUs: TP first,
+    then EP).  A side measurement: the headline bench is the C3 layer."""
+    import torch
+
+    import paper_2303_06318_b200 as ted
+    torch.cuda.set_device(local_rank)
+    ted.set_device(local_rank)
+    T = 2 if world % 2 == 0 else 1
+    P = 2 if world % 4 == 0 else 1
+    D = world // (T * P)
+    h, E, tokens, layers = 4096, 16, 32768, args.layers
+    n = tokens // (P * D)
+    model = ted.MoeModelConfig(layers, h, E, n, 0)
+    uid = None
+    if world > 1:
+        obj = [ted.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    M = ted.TedModel(model, ted.derive_config(world, T, P), ted.RunFlags(dtd=T > 1),
+                     capacity_factor=1.25, shard_optimizer=True, rank=rank, nccl_uid=uid)
+    M.init_params(1234)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(1000 + rank // T)
+    batch = torch.randn(n, h, device="cuda", generator=g).bfloat16()
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        M.step(batch)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ted.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            M.step(batch)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t_ = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_.item())
+    loss = M.loss()
+    M.close()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": tokens / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": f"C4 model stack, {layers} layers", "hidden": h,
+                       "ffn": 4 * h, "experts": E, "tokens": tokens, "tokens_per_shard": n,
+                       "capacity_factor": 1.25, "tp": T, "ep": P, "dp": D, "dtd": T > 1,
+                       "zero1": True, "step": "Trainer::step: fwd+loss+bwd+grad-sync+AdamW"},
+            "gpu_launches": int((ted.kernel_launches() - launches0) // max(args.steps, 1)),
+            "loss_rank0": loss, "clocks": clk.summary()}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -507,7 +569,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtd", type=int, default=1)
     ap.add_argument("--ref-sample", type=int, default=0, help="0: automatic (10-30 s)")
-    ap.add_argument("--workload", default="c3", choices=["c3", "c2"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4"])
+    ap.add_argument("--layers", type=int, default=2, help="c4: layers of the stack")
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] side line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dtd-compare", action="store_true")
@@ -519,7 +582,17 @@ def main():
         world = args.gpus if world == 1 else world
     if args.workload == "c2" and world > 1:
         raise SystemExit("--workload c2 is the single-GPU configuration")
-    w = workload(world, bool(args.dtd), args.workload)
+    if args.workload == "c4" and args.impl == "ours":
+        dist = None
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_model_stack(args, rank, world, local_rank, dist)
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    w = workload(world, bool(args.dtd), "c3" if args.workload == "c4" else args.workload)
     dist = None
     if args.impl == "reference":
         run_reference(args, w, rank, world)

@@ -40,6 +40,7 @@ def main():
     ap.add_argument("--cf", type=float, default=1.25)
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--corrupt", type=int, default=0)
+    ap.add_argument("--ledger", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -135,6 +136,17 @@ def main():
             print("MGPU-OK " + json.dumps(report), flush=True)
         else:
             assert worst < TOL, f"multi-GPU parity failed: {report}"
+            if args.ledger:
+                # the layer's ledger accounting on the real exchange path == the reference's
+                # predict_comm_volume (cost_model.cpp:346-416) for the same config
+                gold = np.load(os.path.join(ROOT, "tests", "golden", "golden.npz"))["predict_comm"]
+                row = [r for r in gold if (int(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4]),
+                                           int(r[5])) == (world, args.tp, args.ep, h, n, args.dtd)]
+                assert row, "no predict_comm golden for this config"
+                a2a = sum(r["stats"]["a2a_bytes_fwd"] for r in allr)
+                ag = sum(r["stats"]["ag_bytes_fwd"] for r in allr)
+                assert (a2a, ag) == (int(row[0][6]), int(row[0][7])), (a2a, ag, row[0])
+                report.update(ledger_a2a=a2a, ledger_ag=ag)
             print("MGPU-OK " + json.dumps(report), flush=True)
     dist.barrier()
     L.close()

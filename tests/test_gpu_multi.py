@@ -71,3 +71,14 @@ def test_model_stack_matches_reference(nproc, tp, ep, zero):
         pytest.skip(f"needs {nproc} GPUs")
     _run(nproc, "--tp", str(tp), "--ep", str(ep), "--zero", str(zero),
          script="mgpu_model_check.py")
+
+
+@pytest.mark.parametrize("dtd", [0, 1])
+def test_four_gpus_ledger_matches_predict_comm_volume(dtd):
+    """E = EP = 2, TP = 2, h = 256, n = 1024, no capacity drops: the forward all-to-all and
+    DTD all-gather payload bytes the layer accounts on the real exchange path, summed over
+    ranks, equal the reference's predict_comm_volume (tests/golden)."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "--tp", "2", "--ep", "2", "--dtd", str(dtd), "--experts", "2", "--hidden", "256",
+         "--tokens", "1024", "--cf", "0", "--ledger", "1")
