@@ -237,6 +237,13 @@ int ted_model_optimizer_step(ted_model* M, void* stream);
 int ted_model_loss(ted_model* M, double* loss, void* stream);
 /* last layer's output (tokens_per_shard x hidden bf16, device) */
 int ted_model_output(ted_model* M, uint16_t* y, void* stream);
+/* device memory of this rank (MemoryReport, moe.hpp / moe.cpp:746-757), bytes:
+ * out[0] parameters + gradients + optimizer state, out[1] activations and workspaces,
+ * out[2] checkpointed layer inputs, out[3] CAC stash of collective outputs.
+ * RunFlags.ckpt = 1 keeps only the layer inputs and recomputes each layer before its
+ * backward (one activation set serves the stack); ckpt + cac replays the recorded
+ * collective outputs in the recompute instead of communicating (channel.cpp:20-51). */
+int ted_model_memory(ted_model* M, int64_t* out);
 
 #ifdef __cplusplus
 }

@@ -160,6 +160,7 @@ _sig("ted_model_backward", _i32, [_vp, _vp])
 _sig("ted_model_optimizer_step", _i32, [_vp, _vp])
 _sig("ted_model_loss", _i32, [_vp, C.POINTER(_dbl), _vp])
 _sig("ted_model_output", _i32, [_vp, _vp, _vp])
+_sig("ted_model_memory", _i32, [_vp, C.POINTER(_i64)])
 
 EXPORTED = [
     "ted_default_configs", "ted_last_error", "ted_version", "ted_derive_config",
@@ -172,7 +173,7 @@ EXPORTED = [
     "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
     "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_step",
     "ted_model_forward", "ted_model_backward", "ted_model_optimizer_step", "ted_model_loss",
-    "ted_model_output"]
+    "ted_model_output", "ted_model_memory"]
 
 
 def lib():
@@ -227,7 +228,7 @@ class TedConfig:  # topology.hpp:22-28 (experts = expert-parallel degree)
 
 
 @dataclass
-class RunFlags:  # moe.hpp:40-46 (ckpt defaults off: activation checkpointing is not built)
+class RunFlags:  # moe.hpp:40-46 (ckpt / cac: the model stack (TedModel); a single MoeLayer rejects them)
     dtd: bool = False
     cac: bool = False
     ckpt: bool = False
@@ -575,3 +576,9 @@ class TedModel:
 
     def output(self, y, stream=None):
         _check(_lib.ted_model_output(self._h, _p(y), _stream(stream)))
+
+    def memory(self) -> dict:
+        out = (_i64 * 4)()
+        _check(_lib.ted_model_memory(self._h, out))
+        return dict(params_grads_optimizer=out[0], activations=out[1], checkpoint=out[2],
+                    cac_stash=out[3])

@@ -84,6 +84,10 @@ struct ted_layer {
   HostBuf<int> h_kc_all, h_seg;
   // activations
   DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home, dx_asm;
+  ted_layer* share = nullptr;     // activation buffers borrowed from this layer (ckpt)
+  int fwd_mode = FWD_LIVE;        // LIVE / RECORD / REPLAY (CAC)
+  DevBuf<bf16> stash_x, stash_f;  // CAC stash: assembled rows, combined home rows
+  int64_t stash_rows = 0;
   const bf16* last_a = nullptr;
   const bf16* last_y = nullptr;
   LayerPlan plan;
@@ -339,7 +343,68 @@ RowSrc pull_src(ted_layer* L, int which) {
 }
 
 // --------------------------------------------------------------- forward
+// Z = X W1 + b1, H = gelu(Z) over the assembled rows (column_parallel_forward + gelu,
+// parallel_linear.cpp:8-11, nn.cpp:108-112); leaves g / o set up for GEMM2
+void expert_gemm1(ted_layer* L, int64_t rows, cudaStream_t s, GemmParams& g, GemmOperands& o) {
+  bf16* P = L->fam_exp.param.p;
+  g = GemmParams{};
+  g.mode = GEMM_ROWS;
+  g.groups = L->Eloc;
+  g.seg_off = L->seg_off.p;
+  o = GemmOperands{};
+  o.A = L->x_asm.p;
+  o.lda = L->h;
+  o.a_mn = false;
+  o.B = P + L->off_w1;
+  o.ldb = L->fT;
+  o.b_group_stride = L->per_expert;
+  o.b_mn = true;
+  L->mark("gemm1_fwd", s);
+  g.epi = EPI_BIAS_GELU;
+  g.M = 0;
+  g.N = L->fT;
+  g.K = L->h;
+  g.C = L->z.p;
+  g.ldc = L->fT;
+  g.bias = P + L->off_b1;
+  g.bias_group_stride = L->per_expert;
+  g.aux = L->hbuf.p;
+  g.ld_aux = L->fT;
+  run_gemm(o, g, rows, s);
+}
+
+void stash_alloc(ted_layer* L) {
+  if (L->stash_x.n == 0) {
+    L->stash_x.alloc(size_t(L->R_max) * L->h);
+    L->stash_f.alloc(size_t(L->n) * L->h);
+  }
+}
+
+// CAC recompute (Mode::Replay, channel.cpp:37-51): the routing state of the recorded
+// forward is still in place; the collectives' outputs come from the stash, so only the
+// local math the backward reads (Z and H of GEMM1) is recomputed
+void layer_forward_replay(ted_layer* L, const bf16* a, cudaStream_t s) {
+  require(L->stash_x.n != 0, "CAC replay without a recorded forward");
+  L->last_a = a;
+  const int64_t rows = L->stash_rows;
+  check(cudaMemcpyAsync(L->x_asm.p, L->stash_x.p, sizeof(bf16) * size_t(rows) * L->h,
+                        cudaMemcpyDeviceToDevice, s),
+        "replay");
+  GemmParams g{};
+  GemmOperands o{};
+  expert_gemm1(L, rows, s, g, o);
+  check(cudaMemcpyAsync(L->fhome.p, L->stash_f.p, sizeof(bf16) * size_t(L->n) * L->h,
+                        cudaMemcpyDeviceToDevice, s),
+        "replay");
+  L->mark("_end", s);
+  L->have_forward = true;
+}
+
 void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
+  if (L->fwd_mode == FWD_REPLAY && !L->local) {
+    layer_forward_replay(L, a, s);
+    return;
+  }
   const int h = L->h, E = L->E;
   L->last_a = a;
   L->last_y = y;
@@ -449,32 +514,18 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     rows = std::max<int64_t>(L->plan.asm_rows, 128);
   }
 
+  if (L->fwd_mode == FWD_RECORD && !L->local) {  // CAC: stash the exchanged expert rows
+    stash_alloc(L);
+    L->stash_rows = rows;
+    check(cudaMemcpyAsync(L->stash_x.p, L->x_asm.p, sizeof(bf16) * size_t(rows) * h,
+                          cudaMemcpyDeviceToDevice, s),
+          "stash");
+  }
   // expert FFN (tensor cores): Z = X W1 + b1, H = gelu(Z); Fe = H W2 (+ b2 on TP rank 0)
   bf16* P = L->fam_exp.param.p;
   GemmParams g{};
-  g.mode = GEMM_ROWS;
-  g.groups = L->Eloc;
-  g.seg_off = L->seg_off.p;
   GemmOperands o{};
-  o.A = L->x_asm.p;
-  o.lda = h;
-  o.a_mn = false;
-  o.B = P + L->off_w1;
-  o.ldb = L->fT;
-  o.b_group_stride = L->per_expert;
-  o.b_mn = true;
-  L->mark("gemm1_fwd", s);
-  g.epi = EPI_BIAS_GELU;
-  g.M = 0;
-  g.N = L->fT;
-  g.K = h;
-  g.C = L->z.p;
-  g.ldc = L->fT;
-  g.bias = P + L->off_b1;
-  g.bias_group_stride = L->per_expert;
-  g.aux = L->hbuf.p;
-  g.ld_aux = L->fT;
-  run_gemm(o, g, rows, s);
+  expert_gemm1(L, rows, s, g, o);
 
   L->mark("gemm2_fwd", s);
   o.A = L->hbuf.p;
@@ -504,6 +555,10 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(combine_pull(src, L->prob.p, L->n, h, y, L->fhome.p, L->loss_part.p, s),
           "combine_pull");
     check(loss_finalize(L->loss_part.p, L->nblk, 1.0 / (2.0 * nglob), L->loss.p, s), "loss");
+    if (L->fwd_mode == FWD_RECORD)  // CAC: stash the combined (returned + reduced) rows
+      check(cudaMemcpyAsync(L->stash_f.p, L->fhome.p, sizeof(bf16) * size_t(L->n) * h,
+                            cudaMemcpyDeviceToDevice, s),
+            "stash");
     L->mark("_end", s);
     L->have_forward = true;
     return;
@@ -523,6 +578,10 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
                   L->tp_c, s);
     }
     fh = L->fhome.p;
+    if (L->fwd_mode == FWD_RECORD)
+      check(cudaMemcpyAsync(L->stash_f.p, L->fhome.p, sizeof(bf16) * size_t(L->n) * h,
+                            cudaMemcpyDeviceToDevice, s),
+            "stash");
   }
   L->mark("combine_fwd", s);
   check(combine_forward(fh, L->pos_home.p, L->prob.p, L->n, h, y, L->loss_part.p, s),
@@ -871,7 +930,8 @@ std::vector<std::string> local_param_names(ted_layer* L) {
 // Export the four exchange buffers with CUDA IPC, all-gather the handles over the plane
 // and map every peer's buffers (NVLink peer access), giving device tables of base pointers.
 void setup_peer_exchange(ted_layer* L) {
-  L->dx_asm.alloc(size_t(L->R_max) * L->h);
+  if (L->share) L->dx_asm.view(L->share->dx_asm);
+  else L->dx_asm.alloc(size_t(L->R_max) * L->h);
   L->disp_base.alloc(size_t(L->E) * (1 + L->Tc));
   L->h_tabs.alloc(size_t(L->E) * (1 + L->Tc));
   L->bar.alloc(1);
@@ -896,6 +956,31 @@ void setup_peer_exchange(ted_layer* L) {
   CU(cudaDeviceSynchronize());
   CU(cudaMemcpy(hall.data(), dh.p, hall.size(), cudaMemcpyDeviceToHost));
   std::vector<unsigned long long> tab(size_t(NB) * PS);
+  if (L->share) {  // buffers 0-3 are the sharing layer's: reuse its mapped peer addresses
+    std::vector<unsigned long long> st(size_t(NB) * PS);
+    CU(cudaMemcpy(st.data(), L->share->peer_tab.p, st.size() * sizeof(unsigned long long),
+                  cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> tab(size_t(NB) * PS);
+    for (int r = 0; r < PS; ++r)
+      for (int b = 0; b < NB; ++b) {
+        if (b < 4) {
+          tab[size_t(b) * PS + r] = st[size_t(b) * PS + r];
+          continue;
+        }
+        void* ptr = mine[b];
+        if (r != L->plane_rank) {
+          cudaIpcMemHandle_t hd;
+          std::memcpy(&hd, hall.data() + (size_t(r) * NB + b) * HB, HB);
+          CU(cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+          L->ipc_opened.push_back(ptr);
+        }
+        tab[size_t(b) * PS + r] = reinterpret_cast<unsigned long long>(ptr);
+      }
+    L->peer_tab.alloc(tab.size());
+    CU(cudaMemcpy(L->peer_tab.p, tab.data(), tab.size() * sizeof(unsigned long long),
+                  cudaMemcpyHostToDevice));
+    return;
+  }
   for (int r = 0; r < PS; ++r)
     for (int b = 0; b < NB; ++b) {
       void* ptr = mine[b];
@@ -915,7 +1000,7 @@ void setup_peer_exchange(ted_layer* L) {
 void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* topo,
                   const ted_flags* flags, const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
                   double cf, int shard_opt, int rank, const void* uid,
-                  ncclComm_t parent = nullptr) {
+                  ncclComm_t parent = nullptr, ted_layer* share = nullptr) {
   require(model && topo && flags && adam && tiles, "null config pointer");
   L->model = *model;
   L->topo = *topo;
@@ -1023,20 +1108,36 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->gate_part.alloc(gate_dw_part_floats(n, L->h, L->E));
   L->col_part.alloc(std::max(colsum_part_floats(L->fT, L->Eloc, int(L->R_max)),
                              colsum_part_floats(L->h, L->Eloc, int(L->R_max))));
-  L->x_asm.alloc(size_t(L->R_max) * h);
-  L->x_asm.zero();
-  L->z.alloc(size_t(L->R_max) * L->fT);
-  L->hbuf.alloc(size_t(L->R_max) * L->fT);
-  L->fe_asm.alloc(size_t(L->R_max) * h);
-  L->dfe_asm.alloc(size_t(L->R_max) * h);
-  L->dfe_asm.zero();
-  if (!L->local) {
-    L->xsend.alloc(size_t(n) * h);
-    L->xsend.zero();
-    L->fhome.alloc(size_t(n) * h);
-    L->fhome.zero();
-    L->dfe_send.alloc(size_t(n) * h);
-    L->dx_home.alloc(size_t(n) * h);
+  if (share != nullptr) {  // activation checkpointing: one activation set for the stack
+    require(share->R_max == L->R_max && share->local == L->local && share->n == n &&
+                share->h == h && share->fT == L->fT,
+            "activation sharing needs layers of one shape");
+    L->share = share;
+    for (auto pr : {std::make_pair(&L->x_asm, &share->x_asm), std::make_pair(&L->z, &share->z),
+                    std::make_pair(&L->hbuf, &share->hbuf),
+                    std::make_pair(&L->fe_asm, &share->fe_asm),
+                    std::make_pair(&L->dfe_asm, &share->dfe_asm),
+                    std::make_pair(&L->xsend, &share->xsend),
+                    std::make_pair(&L->fhome, &share->fhome),
+                    std::make_pair(&L->dfe_send, &share->dfe_send),
+                    std::make_pair(&L->dx_home, &share->dx_home)})
+      pr.first->view(*pr.second);
+  } else {
+    L->x_asm.alloc(size_t(L->R_max) * h);
+    L->x_asm.zero();
+    L->z.alloc(size_t(L->R_max) * L->fT);
+    L->hbuf.alloc(size_t(L->R_max) * L->fT);
+    L->fe_asm.alloc(size_t(L->R_max) * h);
+    L->dfe_asm.alloc(size_t(L->R_max) * h);
+    L->dfe_asm.zero();
+    if (!L->local) {
+      L->xsend.alloc(size_t(n) * h);
+      L->xsend.zero();
+      L->fhome.alloc(size_t(n) * h);
+      L->fhome.zero();
+      L->dfe_send.alloc(size_t(n) * h);
+      L->dx_home.alloc(size_t(n) * h);
+    }
   }
   if (L->direct) setup_peer_exchange(L);
   {
@@ -1085,13 +1186,13 @@ namespace ted {
 int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
                        const ted_flags* flags, const ted_adam_cfg* adam,
                        const ted_tile_cfg* tiles, double capacity_factor, int shard_optimizer,
-                       int rank, ncclComm_t parent, ted_layer** out) {
+                       int rank, ncclComm_t parent, ted_layer* share, ted_layer** out) {
   return guard([&] {
     require(out != nullptr, "null output pointer");
     auto* L = new ted_layer();
     try {
       create_layer(L, model, topo, flags, adam, tiles, capacity_factor, shard_optimizer, rank,
-                   nullptr, parent);
+                   nullptr, parent, share);
       fix_views(L);
     } catch (...) {
       delete L;
@@ -1099,6 +1200,27 @@ int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
     }
     *out = L;
   });
+}
+void layer_set_forward_mode(ted_layer* L, int mode) {
+  L->fwd_mode = mode;
+  if (mode == FWD_RECORD && !L->local) stash_alloc(L);
+}
+
+void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int64_t* stash) {
+  int64_t act = 0;
+  for (const DevBuf<bf16>* b : {&L->x_asm, &L->z, &L->hbuf, &L->fe_asm, &L->xsend, &L->fhome,
+                                &L->dfe_send, &L->dfe_asm, &L->dx_home, &L->dx_asm})
+    act += int64_t(b->bytes());
+  for (const DevBuf<float>* b : {&L->logits, &L->probs, &L->prob, &L->dlogits, &L->gate_part,
+                                 &L->col_part})
+    act += int64_t(b->bytes());
+  int64_t par = 0;
+  for (const Family* F : {&L->fam_exp, &L->fam_non})
+    par += int64_t(F->param.bytes() + F->grad.bytes() + F->gather.bytes() + F->master.bytes() +
+                   F->m1.bytes() + F->m2.bytes());
+  if (activations) *activations = act;
+  if (params) *params = par;
+  if (stash) *stash = int64_t(L->stash_x.bytes() + L->stash_f.bytes());
 }
 }  // namespace ted
 

@@ -118,6 +118,7 @@ struct ted_model {
   std::vector<DevBuf<bf16>> xin;      // layer inputs (np x h, zero pad rows); xin[L] = output
   std::vector<DevBuf<bf16>> abuf;     // attention outputs (input of the MoE / FFN part)
   DevBuf<bf16> dy0, dy1, dmid, dpart;
+  bool ckpt = false, cac = false;  // activation checkpointing; communication-avoiding recompute
   DevBuf<int> seg;                    // {0, np}
   DevBuf<float> col_part;
   DevBuf<double> loss_part, loss;
@@ -127,14 +128,47 @@ struct ted_model {
 namespace {
 
 void dense_params(ted_model* M, int l, bool ffn, int64_t& off) {
-  (void)l;
   DenseBlock& B = ffn ? M->ffn[size_t(l)] : M->attn[size_t(l)];
   B.off = off;
   off += M->per_block;
+  // one Z / H pair per block kind (recomputed): a layer's attention block must keep its
+  // own through the FFN block's recompute and backward
+  const bool first = ffn ? (l == 1) : (l == 0);
+  if (M->ckpt && !first) {
+    const DenseBlock& owner = ffn ? M->ffn[1] : M->attn[0];
+    B.z.view(owner.z);
+    B.hb.view(owner.hb);
+    return;
+  }
   B.z.alloc(size_t(M->np) * M->fT);
   B.z.zero();
   B.hb.alloc(size_t(M->np) * M->fT);
   B.hb.zero();
+}
+
+// GEMM1 + GELU only (the part of a block's forward its backward reads): the CAC recompute
+// of a block whose row-parallel all-reduce output is still in place
+void dense_gemm1(ted_model* M, DenseBlock& B, const bf16* X, cudaStream_t s) {
+  bf16* P = M->fam.param.p + B.off;
+  GemmParams g{};
+  g.mode = GEMM_ROWS;
+  g.groups = 1;
+  g.seg_off = M->seg.p;
+  GemmOperands o{};
+  o.A = X;
+  o.lda = M->h;
+  o.B = P;
+  o.ldb = M->fT;
+  o.b_mn = true;
+  g.epi = EPI_BIAS_GELU;
+  g.N = M->fT;
+  g.K = M->h;
+  g.C = B.z.p;
+  g.ldc = M->fT;
+  g.bias = P + int64_t(M->h) * M->fT;
+  g.aux = B.hb.p;
+  g.ld_aux = M->fT;
+  run_gemm(o, g, M->np, s);
 }
 
 void zero_pad_rows(ted_model* M, bf16* buf, cudaStream_t s) {
@@ -369,8 +403,11 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   require(model->layers >= 1, "layers must be >= 1, got " + std::to_string(model->layers));
   require(model->hidden >= 1 && model->experts >= 1 && model->tokens_per_shard >= 1,
           "model: hidden, experts and tokens_per_shard must be >= 1");
-  require(flags->cac == 0 && flags->ckpt == 0,
-          "flags: ckpt/cac (activation checkpointing, CAC) are not implemented in this build");
+  // ckpt: keep only every layer's input and recompute the layer before its backward
+  // (moe.cpp:343-375, :393-415); cac (with ckpt): the recompute replays the stashed
+  // collective outputs instead of communicating (channel.cpp:20-51)
+  M->ckpt = flags->ckpt != 0;
+  M->cac = M->ckpt && flags->cac != 0;
   M->layers = model->layers;
   M->h = model->hidden;
   M->f = 4 * M->h;
@@ -437,9 +474,13 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   M->moe.assign(size_t(M->layers), nullptr);
   ted_model_cfg one = *model;
   one.layers = 1;
+  ted_flags lf = *flags;  // checkpointing is the stack's business, not the layer's
+  lf.ckpt = 0;
+  lf.cac = 0;
   for (int l = 0; l < M->layers; l += 2) {
     ted_layer* L = nullptr;
-    if (layer_create_child(&one, topo, flags, adam, tiles, cf, shard_opt, rank, M->world_c,
+    ted_layer* share = (M->ckpt && l > 0) ? M->moe[0] : nullptr;
+    if (layer_create_child(&one, topo, &lf, adam, tiles, cf, shard_opt, rank, M->world_c, share,
                            &L) != TED_OK)
       throw RuntimeError(std::string("layer ") + std::to_string(l) + ": " + last_error());
     M->moe[size_t(l)] = L;
@@ -451,9 +492,13 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
     b.alloc(size_t(M->np) * M->h);
     b.zero();
   }
-  for (auto& b : M->abuf) {
-    b.alloc(size_t(M->np) * M->h);
-    b.zero();
+  for (size_t l = 0; l < M->abuf.size(); ++l) {
+    if (M->ckpt && !M->cac && l > 0) {  // recomputed: one buffer (with CAC it is the stash
+      M->abuf[l].view(M->abuf[0]);       // of the attention block's all-reduce output)
+      continue;
+    }
+    M->abuf[l].alloc(size_t(M->np) * M->h);
+    M->abuf[l].zero();
   }
   for (DevBuf<bf16>* b : {&M->dy0, &M->dy1, &M->dmid, &M->dpart}) {
     b->alloc(size_t(M->np) * M->h);
@@ -476,6 +521,7 @@ void model_forward(ted_model* M, const bf16* batch, cudaStream_t s) {
   for (int l = 0; l < M->layers; ++l) {
     dense_forward(M, M->attn[size_t(l)], M->xin[size_t(l)].p, M->abuf[size_t(l)].p, s);
     if (l % 2 == 0) {
+      layer_set_forward_mode(M->moe[size_t(l)], M->cac ? FWD_RECORD : FWD_LIVE);
       const int rc = ted_layer_forward(M->moe[size_t(l)],
                                        reinterpret_cast<const uint16_t*>(M->abuf[size_t(l)].p),
                                        reinterpret_cast<uint16_t*>(M->xin[size_t(l + 1)].p), s);
@@ -493,6 +539,29 @@ void model_forward(ted_model* M, const bf16* batch, cudaStream_t s) {
   M->have_forward = true;
 }
 
+// the layer's forward again from its checkpointed input (Phase::Recompute, moe.cpp:396-404):
+// live, or with CAC replaying the recorded collective outputs (the attention / FFN
+// all-reduce outputs are still in abuf / xin, the MoE exchange outputs in the layer's
+// stash), in which case only the GEMM1 + GELU the backward reads are recomputed
+void recompute_layer(ted_model* M, int l, cudaStream_t s) {
+  const bool replay = M->cac && M->world > 1;
+  DenseBlock& A = M->attn[size_t(l)];
+  if (replay) dense_gemm1(M, A, M->xin[size_t(l)].p, s);
+  else dense_forward(M, A, M->xin[size_t(l)].p, M->abuf[size_t(l)].p, s);
+  if (l % 2 == 0) {
+    ted_layer* L = M->moe[size_t(l)];
+    layer_set_forward_mode(L, M->cac ? FWD_REPLAY : FWD_LIVE);
+    const int rc = ted_layer_forward(L, reinterpret_cast<const uint16_t*>(M->abuf[size_t(l)].p),
+                                     reinterpret_cast<uint16_t*>(M->dpart.p), s);
+    layer_set_forward_mode(L, FWD_LIVE);
+    if (rc != TED_OK) throw RuntimeError(last_error());
+  } else if (replay) {
+    dense_gemm1(M, M->ffn[size_t(l)], M->abuf[size_t(l)].p, s);
+  } else {
+    dense_forward(M, M->ffn[size_t(l)], M->abuf[size_t(l)].p, M->dpart.p, s);
+  }
+}
+
 void model_backward(ted_model* M, cudaStream_t s) {
   if (!M->have_forward) throw ConfigError("backward called before forward");
   const int h = M->h;
@@ -504,6 +573,7 @@ void model_backward(ted_model* M, cudaStream_t s) {
   bf16* dy = M->dy0.p;
   bf16* dx = M->dy1.p;
   for (int l = M->layers - 1; l >= 0; --l) {
+    if (M->ckpt) recompute_layer(M, l, s);
     if (l % 2 == 0) {
       const int rc = ted_layer_backward(M->moe[size_t(l)], reinterpret_cast<const uint16_t*>(dy),
                                         reinterpret_cast<uint16_t*>(M->dmid.p), s);
@@ -709,6 +779,38 @@ int ted_model_loss(ted_model* M, double* loss, void* stream) {
     require(M && loss, "null argument");
     CU(cudaMemcpyAsync(loss, M->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
     CU(cudaStreamSynchronize(S(stream)));
+  });
+}
+
+int ted_model_memory(ted_model* M, int64_t* out) {
+  return guard([&] {
+    require(M && out, "null argument");
+    int64_t act = 0, par = 0, stash = 0;
+    for (ted_layer* L : M->moe)
+      if (L) {
+        int64_t a = 0, p = 0, st = 0;
+        layer_memory(L, &a, &p, &st);
+        act += a;
+        par += p;
+        stash += st;
+      }
+    for (const auto* v : {&M->attn, &M->ffn})
+      for (const DenseBlock& B : *v) act += int64_t(B.z.bytes() + B.hb.bytes());
+    int64_t ckpt = 0;
+    for (size_t l = 0; l < M->abuf.size(); ++l) {
+      if (M->cac && M->world > 1) stash += int64_t(M->abuf[l].bytes());  // attn AR outputs
+      else act += int64_t(M->abuf[l].bytes());
+    }
+    for (const auto& b : M->xin) ckpt += int64_t(b.bytes());  // layer inputs (+ output)
+    for (const DevBuf<bf16>* b : {&M->dy0, &M->dy1, &M->dmid, &M->dpart})
+      act += int64_t(b->bytes());
+    const Family& F = M->fam;
+    par += int64_t(F.param.bytes() + F.grad.bytes() + F.gather.bytes() + F.master.bytes() +
+                   F.m1.bytes() + F.m2.bytes());
+    out[0] = par;    // parameters, gradients, optimizer state
+    out[1] = act;    // activations and workspaces
+    out[2] = ckpt;   // layer inputs kept for the backward / recompute
+    out[3] = stash;  // CAC stash of collective outputs
   });
 }
 

@@ -42,18 +42,27 @@ template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;  // false: a view of another buffer (activation sharing under ckpt)
   void alloc(size_t count) {
     free();
     n = count;
     if (count) CU(cudaMalloc(&p, sizeof(T) * count));
   }
+  void view(const DevBuf& other) {
+    free();
+    p = other.p;
+    n = other.n;
+    owned = false;
+  }
+  size_t bytes() const { return owned ? sizeof(T) * n : 0; }
   void zero() {
     if (n) CU(cudaMemset(p, 0, sizeof(T) * n));
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
+    owned = true;
   }
   ~DevBuf() { free(); }
 };
@@ -155,9 +164,21 @@ inline void run_gemm(const GemmOperands& o, const GemmParams& p, int64_t rows, c
 
 // a MoE layer of a model stack whose communicators are split from the model's world
 // communicator `parent` (layer.cu); the C-ABI twin is ted_layer_create
+// `share` (optional): an earlier MoE layer of the same stack whose activation buffers this
+// layer reuses (activation checkpointing: every layer recomputes its forward right
+// before its backward, so one set of activations serves the whole stack)
 int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
                        const ted_flags* flags, const ted_adam_cfg* adam,
                        const ted_tile_cfg* tiles, double capacity_factor, int shard_optimizer,
-                       int rank, ncclComm_t parent, ted_layer** out);
+                       int rank, ncclComm_t parent, ted_layer* share, ted_layer** out);
+// forward modes for activation checkpointing with communication-avoiding recompute (CAC,
+// channel.cpp:20-51): LIVE runs everything; RECORD also stashes the exchange outputs
+// (assembled expert rows and the combined home rows); REPLAY is the recompute that takes
+// them from the stash instead of communicating and reruns only what the backward reads
+enum { FWD_LIVE = 0, FWD_RECORD = 1, FWD_REPLAY = 2 };
+void layer_set_forward_mode(ted_layer* L, int mode);
+// device bytes this layer owns (activations and workspaces, parameters and optimizer
+// state, CAC stash)
+void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int64_t* stash);
 
 }  // namespace ted

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--ep", type=int, default=1)
     ap.add_argument("--dtd", type=int, default=1)
     ap.add_argument("--zero", type=int, default=1)
+    ap.add_argument("--ckpt", type=int, default=0)
+    ap.add_argument("--cac", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -43,7 +45,8 @@ def main():
     model = ted.MoeModelConfig(layers, h, E, n, seed)
     obj = [ted.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    M = ted.TedModel(model, ted.derive_config(world, T, P), ted.RunFlags(dtd=bool(args.dtd)),
+    M = ted.TedModel(model, ted.derive_config(world, T, P),
+                     ted.RunFlags(dtd=bool(args.dtd), ckpt=bool(args.ckpt), cac=bool(args.cac)),
                      shard_optimizer=bool(args.zero), rank=rank, nccl_uid=obj[0])
     for nm, full in stack_params(ted, model).items():
         M.set_param(nm, full)

@@ -49,3 +49,27 @@ def test_stack_parameters_round_trip_and_update():
     with pytest.raises(ted.InvalidConfigError):
         M.set_param("layer0.ffn.w1", g)  # layer 0 is a MoE layer: no dense FFN
     M.close()
+
+
+@pytest.mark.parametrize("ckpt,cac", [(1, 0), (1, 1)])
+def test_checkpointing_recompute_is_exact(ckpt, cac):
+    """RunFlags.ckpt (recompute every layer before its backward) and ckpt + cac give the
+    same losses as the plain run (the reference: test_moe.cpp:345-386, exact), with one
+    activation set for the whole stack."""
+    import paper_2303_06318_b200 as ted
+    model = ted.MoeModelConfig(4, 256, 4, 128, 5)
+    runs, mem = {}, {}
+    for key in ((0, 0), (ckpt, cac)):
+        M = ted.TedModel(model, ted.TedConfig(), ted.RunFlags(ckpt=bool(key[0]), cac=bool(key[1])))
+        for nm, full in stack_params(ted, model).items():
+            M.set_param(nm, full)
+        batch = torch.tensor(stack_batch(model, 1), dtype=torch.float32).bfloat16().cuda()
+        ls = []
+        for _ in range(3):
+            M.step(batch)
+            ls.append(M.loss())
+        runs[key], mem[key] = ls, M.memory()
+        M.close()
+    assert runs[(0, 0)] == runs[(ckpt, cac)]
+    np.testing.assert_allclose(runs[(0, 0)], golden_losses(4, 256, 4, 128, 5, 1), rtol=TOL)
+    assert mem[(ckpt, cac)]["activations"] < mem[(0, 0)]["activations"]

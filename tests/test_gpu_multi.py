@@ -82,3 +82,13 @@ def test_four_gpus_ledger_matches_predict_comm_volume(dtd):
         pytest.skip("needs 4 GPUs")
     _run(4, "--tp", "2", "--ep", "2", "--dtd", str(dtd), "--experts", "2", "--hidden", "256",
          "--tokens", "1024", "--cf", "0", "--ledger", "1")
+
+
+@pytest.mark.parametrize("ckpt,cac", [(1, 0), (1, 1)])
+def test_model_stack_checkpointing_four_gpus(ckpt, cac):
+    """Activation checkpointing, live and with CAC replay of the recorded exchange and
+    all-reduce outputs, over TP2 x EP2: the reference SerialModel's losses."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "--tp", "2", "--ep", "2", "--ckpt", str(ckpt), "--cac", str(cac),
+         script="mgpu_model_check.py")
