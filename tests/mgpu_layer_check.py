@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--seed", type=int, default=7)
     ap.add_argument("--corrupt", type=int, default=0)
     ap.add_argument("--ledger", type=int, default=0)
+    ap.add_argument("--skew", type=float, default=0.0)
     args = ap.parse_args()
 
     import torch
@@ -69,6 +70,8 @@ def main():
                      ted.RunFlags(dtd=bool(args.dtd), corrupt_drop=bool(args.corrupt)),
                      capacity_factor=cf, rank=rank, nccl_uid=uid[0])
     inp = O.make_layer_inputs(S, n, h, f, E, args.seed, bf16=True)
+    if args.skew > 0:  # C5 routing stress: Zipf-like gate column scales skew the loads
+        inp["wg"] = O.bf16_round(inp["wg"] * (1.0 + args.skew / (1.0 + np.arange(E)))[None, :])
     L.set_param("layer0.gate.w", inp["wg"])
     Eloc = E // P
     for le in range(Eloc):

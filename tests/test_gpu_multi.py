@@ -92,3 +92,14 @@ def test_model_stack_checkpointing_four_gpus(ckpt, cac):
         pytest.skip("needs 4 GPUs")
     _run(4, "--tp", "2", "--ep", "2", "--ckpt", str(ckpt), "--cac", str(cac),
          script="mgpu_model_check.py")
+
+
+@pytest.mark.parametrize("E,cf", [(64, 1.0), (32, 1.5), (64, 2.0)])
+def test_four_gpus_routing_stress(E, cf):
+    """configs[4] (C5) at 4 GPUs: skewed gate (Zipf-like column scales), 32-64 experts,
+    capacity factor 1.0-2.0 with heavy drops on the popular experts, TP2 x EP2 with DTD:
+    outputs and gradients against the oracle run serially over all shards."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--experts", str(E), "--cf", str(cf),
+         "--skew", "3.0", "--tokens", "1024")
