@@ -133,6 +133,50 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
 }
 
+// Epilogue walk with quarter half tiles (32 rows x 8 columns: 24 state registers) and NW
+// warps per CTA sharing the four TMEM sub-partitions unevenly (NW/4 warps per sub-partition
+// split the 256 columns into NW/4 runs of 8-column quarters)
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    epi_sim_q(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+              int groups, int M, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int WPS = NW / 4;       // warps per sub-partition
+  constexpr int NQ = 256 / 8;       // quarters per tile row block
+  const int sp = warp % 4, k = warp / 4;
+  const int q0 = (NQ * k) / WPS, q1 = (NQ * (k + 1)) / WPS;
+  const int nt = N / 256, per = (M / 128) * nt, total = groups * per;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int64_t tbase = int64_t(t) * (128 * 256) + lane * 4;
+    for (int q = q0; q < q1; ++q) {
+      // tile-major: quarter q of sub-partition sp = half (q / 2) of the warp share, chunk pair
+      const int cc = q * 8;  // column in the tile
+      const int share = sp * 4 + (cc >> 6), half = (cc >> 4) & 3, jc = (cc >> 2) & 3;
+      const int64_t o = tbase + (int64_t(share) * 4 + half) * 512 + jc * 128;
+      float4 a0 = *reinterpret_cast<const float4*>(w + o), a1 = *reinterpret_cast<const float4*>(w + o + 128);
+      float4 b0 = *reinterpret_cast<const float4*>(m + o), b1 = *reinterpret_cast<const float4*>(m + o + 128);
+      float4 c0 = *reinterpret_cast<const float4*>(v + o), c1 = *reinterpret_cast<const float4*>(v + o + 128);
+      float* A[2] = {&a0.x, &a1.x};
+      float* B[2] = {&b0.x, &b1.x};
+      float* Cc[2] = {&c0.x, &c1.x};
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          B[u][e] = 0.9f * B[u][e] + 0.1f * A[u][e];
+          Cc[u][e] = 0.999f * Cc[u][e] + 0.001f * A[u][e] * A[u][e];
+          A[u][e] -= 1e-4f * (B[u][e] / (sqrtf(Cc[u][e]) + 1e-8f));
+        }
+      *reinterpret_cast<float4*>(w + o) = a0;
+      *reinterpret_cast<float4*>(w + o + 128) = a1;
+      *reinterpret_cast<float4*>(m + o) = b0;
+      *reinterpret_cast<float4*>(m + o + 128) = b1;
+      *reinterpret_cast<float4*>(v + o) = c0;
+      *reinterpret_cast<float4*>(v + o + 128) = c1;
+    }
+  }
+}
+
 int main() {
   const int64_t n = int64_t(64) << 20;  // elements (fp32 arrays of 256 MB)
   const int64_t n4 = n / 4;
@@ -195,6 +239,9 @@ int main() {
       [&] { epi_sim<NW, D, LY><<<sms, NW * 32>>>(W, Mm, V, G, M, N); });
     EPI(8, 1, 0) EPI(8, 2, 0) EPI(16, 1, 0) EPI(16, 2, 0)
     EPI(8, 1, 1) EPI(8, 2, 1) EPI(16, 1, 1) EPI(16, 2, 1) EPI(32, 1, 1)
+#define EPQ(NW) run("epi_sim_q " #NW " warps (quarters, uneven)", eb, \
+      [&] { epi_sim_q<NW><<<sms, NW * 32>>>(W, Mm, V, G, M, N); });
+    EPQ(16) EPQ(20) EPQ(24) EPQ(28) EPQ(32)
     const int64_t n1 = int64_t(G) * M * N;
     run("flat adam (same size) U1 8xSM", n1 * 26.0,
         [&] { adam_k<1><<<sms * 8, 256>>>(w, m, v, g, p, n1 / 4); });
