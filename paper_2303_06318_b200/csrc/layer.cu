@@ -1201,6 +1201,17 @@ int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
     *out = L;
   });
 }
+void layer_backward_then_step(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
+  L->overlap_opt = true;  // fuse_ok decides inside: AdamW in the wgrad epilogues
+  try {
+    layer_backward(L, dy, da, s);
+  } catch (...) {
+    L->overlap_opt = false;
+    throw;
+  }
+  L->overlap_opt = false;
+}
+
 void layer_set_forward_mode(ted_layer* L, int mode) {
   L->fwd_mode = mode;
   if (mode == FWD_RECORD && !L->local) stash_alloc(L);

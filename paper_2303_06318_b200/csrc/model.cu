@@ -562,7 +562,7 @@ void recompute_layer(ted_model* M, int l, cudaStream_t s) {
   }
 }
 
-void model_backward(ted_model* M, cudaStream_t s) {
+void model_backward(ted_model* M, cudaStream_t s, bool step_follows = false) {
   if (!M->have_forward) throw ConfigError("backward called before forward");
   const int h = M->h;
   const double nglob = double(M->n) * M->P * M->D;
@@ -575,9 +575,14 @@ void model_backward(ted_model* M, cudaStream_t s) {
   for (int l = M->layers - 1; l >= 0; --l) {
     if (M->ckpt) recompute_layer(M, l, s);
     if (l % 2 == 0) {
-      const int rc = ted_layer_backward(M->moe[size_t(l)], reinterpret_cast<const uint16_t*>(dy),
-                                        reinterpret_cast<uint16_t*>(M->dmid.p), s);
-      if (rc != TED_OK) throw RuntimeError(last_error());
+      if (step_follows) {
+        layer_backward_then_step(M->moe[size_t(l)], dy, M->dmid.p, s);
+      } else {
+        const int rc = ted_layer_backward(M->moe[size_t(l)],
+                                          reinterpret_cast<const uint16_t*>(dy),
+                                          reinterpret_cast<uint16_t*>(M->dmid.p), s);
+        if (rc != TED_OK) throw RuntimeError(last_error());
+      }
     } else {
       dense_backward(M, M->ffn[size_t(l)], M->abuf[size_t(l)].p, dy, M->dmid.p, s);
     }
@@ -769,7 +774,7 @@ int ted_model_step(ted_model* M, const uint16_t* batch, void* stream) {
     require(M && batch, "null argument");
     const cudaStream_t s = S(stream);
     model_forward(M, reinterpret_cast<const bf16*>(batch), s);
-    model_backward(M, s);
+    model_backward(M, s, /*step_follows=*/true);
     model_optimizer(M, s);
   });
 }

@@ -177,6 +177,10 @@ int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
 // them from the stash instead of communicating and reruns only what the backward reads
 enum { FWD_LIVE = 0, FWD_RECORD = 1, FWD_REPLAY = 2 };
 void layer_set_forward_mode(ted_layer* L, int mode);
+// backward when the optimizer step follows (Trainer::step): with an unsharded expert
+// family the AdamW update runs inside the wgrad epilogues and the layer's next
+// optimizer step skips that family
+void layer_backward_then_step(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s);
 // device bytes this layer owns (activations and workspaces, parameters and optimizer
 // state, CAC stash)
 void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int64_t* stash);
