@@ -28,6 +28,7 @@
 
 #include "ted_internal.h"
 #include "ted_ptx.cuh"
+#include "ted_vec.cuh"
 
 namespace ted {
 
@@ -436,6 +437,17 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
               v[8 * j + 2 * q] *= gelu_grad_f(f.x);
               v[8 * j + 2 * q + 1] *= gelu_grad_f(f.y);
             }
+          }
+          if (p.colsum_part != nullptr) {
+            // bias gradient: column sums of the stored (bf16) dZ over this warp's 32 rows,
+            // one partial per 32-row split -- colsum_groups' layout, finished by
+            // colsum_finish (rows are padded with zero dZ, like the unfused column sums)
+            float cs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = __bfloat162float(__float2bfloat16(v[i]));
+            const float tot = reduce_scatter32(cs, lane);
+            const int rs = ti.m_blk * 4 + sp;
+            p.colsum_part[(int64_t(rs) * p.groups + ti.g) * p.N + col + lane] = tot;
           }
         }
         if (EPI == EPI_BIAS || EPI == EPI_BIAS_GELU) {

@@ -719,7 +719,12 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   o.ldb = h;
   o.b_group_stride = L->per_expert;
   o.b_mn = false;
+  g.colsum_part = L->col_part.p;  // db1 partials straight from the epilogue's dZ
   run_gemm(o, g, rows, s);
+  L->mark("colsum", s);
+  check(colsum_finish(L->col_part.p, L->fT, L->seg_off.p, L->Eloc, G + L->off_b1,
+                      L->per_expert, s),
+        "colsum db1");
   L->mark("wgrad2", s);
   // wgrad of GEMM2: dW2 = H^T dFe  -> expert family grads (row_parallel_backward :36)
   g = GemmParams{};
@@ -795,10 +800,6 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   o.ldb = L->fT;
   o.b_mn = true;
   run_gemm(o, g, rows, s);
-  L->mark("colsum", s);
-  check(colsum_groups(L->z.p, L->fT, L->fT, L->seg_off.p, L->Eloc, maxg, L->col_part.p,
-                      G + L->off_b1, L->per_expert, s),
-        "colsum db1");
   if (fuse_adam) {
     bias_adam(L, L->off_b1, L->fT, s);
     L->exp_done_fused = true;

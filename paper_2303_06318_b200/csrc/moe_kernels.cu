@@ -33,22 +33,6 @@ constexpr int kWarpTok = kRouteBlock / 8;  // tokens per warp (8)
 
 __host__ __device__ __forceinline__ int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
-// Reduce-scatter of 32 per-lane partial values: afterwards lane l holds the warp total of
-// value index l.  31 shuffles instead of 32 x 5.
-__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < off; ++i) {
-      const float send = upper ? v[i] : v[i + off];
-      const float keep = upper ? v[i + off] : v[i];
-      v[i] = keep + __shfl_xor_sync(FULL, send, off);
-    }
-  }
-  return v[0];
-}
-
 // ------------------------------------------------------------------ gate forward
 // Candidate order for top-1: strictly larger value wins, equal values -> lower index.
 // NaN logits at j > 0 never win; a NaN at j = 0 pins the choice to expert 0 (the
@@ -1377,6 +1361,16 @@ cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, 
   sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, 0, seg_off, w, kColRows, out,
                                                       out_stride);
   count_launch(2);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum_finish(const float* part, int w, const int* seg_off, int G, bf16* out,
+                          int64_t out_stride, cudaStream_t s) {
+  if (w % 8 != 0 || G < 1) return cudaErrorInvalidValue;
+  const int64_t M = int64_t(G) * w;
+  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, 0, seg_off, w, kColRows, out,
+                                                      out_stride);
+  count_launch(1);
   return cudaGetLastError();
 }
 

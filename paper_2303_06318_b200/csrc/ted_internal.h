@@ -57,6 +57,9 @@ struct GemmParams {
   float* adam_m1 = nullptr;
   float* adam_m2 = nullptr;
   const float* adam_coef = nullptr;  // device {1/(1-b1^t), 1/(1-b2^t)}
+  // EPI_DGELU (ROWS mode): also write the 32-row column-sum partials of dZ (bias gradient,
+  // the colsum_groups partial layout [row split][group][N]) -- skips a pass over dZ
+  float* colsum_part = nullptr;
   // (EPI_ADAM: master/m1/m2 use the blk_off layout per group, group stride c_group_stride)
   float lr = 0.f, b1 = 0.f, b2 = 0.f, omb1 = 0.f, omb2 = 0.f, eps = 0.f, wd = 0.f;
 };
@@ -177,6 +180,9 @@ cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n,
                                  float* part, bf16* dwg, cudaStream_t s);
 size_t gate_dw_part_floats(int64_t n, int h, int E);
 // db_g[j] = sum over rows of group g of D[row][j]  (D [rows][w] bf16)
+// the second half of colsum_groups: sum the 32-row partials (written by a DGELU epilogue)
+cudaError_t colsum_finish(const float* part, int w, const int* seg_off, int G, bf16* out,
+                          int64_t out_stride, cudaStream_t s);
 cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, int G,
                           int max_rows_per_group, float* part, bf16* out, int64_t out_stride,
                           cudaStream_t s);

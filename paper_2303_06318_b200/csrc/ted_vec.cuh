@@ -46,4 +46,20 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 }  // namespace
+// Reduce-scatter of 32 per-lane partial values: afterwards lane l holds the warp total of
+// value index l (31 shuffles instead of 32 x 5).
+__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const float send = upper ? v[i] : v[i + off];
+      const float keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
 }  // namespace ted
