@@ -838,6 +838,95 @@ __global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict
       if (j < E) out[c * E + j] = acc[c][j];
 }
 
+// dWg = a^T . dlogits on the tensor cores (gate_backward's dweight, moe.cpp:205):
+// mma.sync.m16n8k16 with M = hidden columns, N = experts, K = tokens.  A warp owns 64
+// hidden columns (four M-tiles) for a chunk of `tok` tokens; per 16-token k-step lane
+// (g, c) loads 16 B (8 hidden columns at 8g) of the token rows 2c, 2c+1, 2c+8, 2c+9 and
+// byte-permutes them into the A fragments: M-tile mt's rows g / g+8 are hidden columns
+// 8g + 2mt / 8g + 2mt + 1 (a permutation of M undone when writing).  dlogits (fp32) enter
+// as bf16 hi + lo (two MMAs, ~2^-17 relative); fp32 accumulation; one partial per chunk.
+template <int NT>
+__global__ void __launch_bounds__(128) gate_bwd_dw_mma_kernel(const bf16* __restrict__ a,
+                                                              const float* __restrict__ dl,
+                                                              int64_t n, int h, int E, int tok,
+                                                              float* __restrict__ part) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int hb = (blockIdx.y * 4 + warp) * 64;
+  if (hb >= h) return;
+  const int64_t k_beg = int64_t(blockIdx.x) * tok, k_end = lmin(n, k_beg + tok);
+  float acc[4][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
+  const int tr[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};  // this lane's token rows
+  auto load = [&](int64_t k0, uint4 (&x)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t t = k0 + tr[i];
+      x[i] = t < k_end ? ldg_stream(a + t * h + hb + 8 * g) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 xc[4], xn[4];
+  load(k_beg, xc);
+  for (int64_t k0 = k_beg; k0 < k_end; k0 += 16) {
+    if (k0 + 16 < k_end) load(k0 + 16, xn);
+    // B fragments: dlogits of tokens (2c, 2c+1) and (2c+8, 2c+9) for expert nt*8 + g
+    uint32_t bhi[NT][2], blo[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int e = nt * 8 + g;
+#pragma unroll
+      for (int pq = 0; pq < 2; ++pq) {
+        const int64_t t0 = k0 + tr[2 * pq], t1 = k0 + tr[2 * pq + 1];
+        const float v0 = (t0 < k_end && e < E) ? dl[t0 * E + e] : 0.f;
+        const float v1 = (t1 < k_end && e < E) ? dl[t1 * E + e] : 0.f;
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+        const float2 hf = __bfloat1622float2(hi);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+        bhi[nt][pq] = *reinterpret_cast<const uint32_t*>(&hi);
+        blo[nt][pq] = *reinterpret_cast<const uint32_t*>(&lo);
+      }
+    }
+    const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&xc[0]);
+    const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&xc[1]);
+    const uint32_t* w2 = reinterpret_cast<const uint32_t*>(&xc[2]);
+    const uint32_t* w3 = reinterpret_cast<const uint32_t*>(&xc[3]);
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      // row g: hidden column 8g + 2mt (low halves), row g + 8: 8g + 2mt + 1 (high halves)
+      const uint32_t a0 = __byte_perm(w0[mt], w1[mt], 0x5410);
+      const uint32_t a1 = __byte_perm(w0[mt], w1[mt], 0x7632);
+      const uint32_t a2 = __byte_perm(w2[mt], w3[mt], 0x5410);
+      const uint32_t a3 = __byte_perm(w2[mt], w3[mt], 0x7632);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, bhi[nt][0], bhi[nt][1]);
+        mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, blo[nt][0], blo[nt][1]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xc[i] = xn[i];
+  }
+  float* out = part + int64_t(blockIdx.x) * h * E;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int e = nt * 8 + 2 * c;
+      const int64_t r0 = hb + 8 * g + 2 * mt, r1 = r0 + 1;
+      if (e < E) {
+        out[r0 * E + e] = acc[mt][nt][0];
+        out[r1 * E + e] = acc[mt][nt][2];
+      }
+      if (e + 1 < E) {
+        out[r0 * E + e + 1] = acc[mt][nt][1];
+        out[r1 * E + e + 1] = acc[mt][nt][3];
+      }
+    }
+}
+
 // out[m] = sum_{s < ns(m)} part[s * stride + m] in a fixed order.  A CTA owns 32
 // consecutive m; its 8 warps take every 8th partial with 4 independent loads in flight,
 // then combine through smem.  ns(m) = ns_const, or (rows of group m / w) / rows_per_split
@@ -1308,8 +1397,10 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
 // tokens per dWg partial: enough CTAs to fill the GPU (4 per SM), as few partials as that
 // allows (the partial buffer is h x E floats per token chunk)
 int dw_tok(int64_t n, int h, int E) {
+  // E <= 32 and h % 64 == 0: the mma.sync kernel (256 hidden columns per CTA); else FMA
+  const bool mma = E <= 32 && h % 64 == 0;
   const int cpt = E <= 8 ? 8 : (E <= 16 ? 4 : (E <= 32 ? 2 : 1));
-  const int64_t ycta = ceil_div(h, 128 * cpt);
+  const int64_t ycta = mma ? ceil_div(h, 256) : ceil_div(h, 128 * cpt);
   const int64_t sub = std::max<int64_t>(1, ceil_div(n, kDwTok));
   const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(sub, 4 * sm_count() / ycta));
   return int(ceil_div(sub, chunks) * kDwTok);
@@ -1327,7 +1418,12 @@ cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n,
   if (nb == 0) {
     return cudaMemsetAsync(dwg, 0, sizeof(bf16) * size_t(h) * E, s);
   }
-  if (E <= 8) {
+  if (E <= 32 && h % 64 == 0) {
+    const dim3 grid(nb, ceil_div(h, 256));
+    if (E <= 8) gate_bwd_dw_mma_kernel<1><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+    else if (E <= 16) gate_bwd_dw_mma_kernel<2><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+    else gate_bwd_dw_mma_kernel<4><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+  } else if (E <= 8) {
     gate_bwd_dw_kernel<8, 8><<<dim3(nb, ceil_div(h, 128 * 8)), 128, 0, s>>>(a, dlogits, n, h, E,
                                                                           tok, part);
   } else if (E <= 16) {
