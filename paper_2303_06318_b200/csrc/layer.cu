@@ -94,12 +94,12 @@ struct ted_layer {
   int64_t last_dropped = 0;
   bool have_forward = false;
 
-  // side stream: the expert family's AdamW overlaps the tail of the backward
-  cudaStream_t side = nullptr;  // lowest priority
-  cudaStream_t hs = nullptr;    // highest priority: the step's main work in ted_layer_step
-  cudaEvent_t ev_w2 = nullptr, ev_w1 = nullptr, ev_side_done = nullptr, ev_fork = nullptr,
-              ev_join = nullptr;
-  bool overlap_opt = false, exp_done_fused = false;
+  // the stream ted_layer_step forks onto (and captures its CUDA graph on)
+  cudaStream_t hs = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // step_follows: the optimizer step follows this backward (ted_layer_step / a model step),
+  // so the expert family's AdamW may run inside the wgrad epilogues (exp_done_fused)
+  bool step_follows = false, exp_done_fused = false;
   bool fuse_ok = false;  // expert family unsharded, no DP sync: AdamW may fuse into wgrad
 
   // CUDA graph of the whole single-rank training step (ted_layer_step): the step has no
@@ -119,8 +119,6 @@ struct ted_layer {
   static constexpr int kGraphs = 4;
   Graph graphs[kGraphs];
   unsigned long long graph_clock = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_evs;
-  size_t side_used = 0;
 
   // live per-stage timing (CUDA events on the launching stream)
   bool timing = false;
@@ -141,22 +139,6 @@ struct ted_layer {
     CU(cudaEventRecord(evs[ev_used], s));
     ev_names[ev_used] = name;
     ++ev_used;
-  }
-  // interval on the side stream: call with begin=true before, false after the work
-  void side_mark(bool begin, cudaStream_t s) {
-    if (!timing || capturing) return;
-    if (begin) {
-      if (side_used == side_evs.size()) {
-        cudaEvent_t a, b;
-        CU(cudaEventCreate(&a));
-        CU(cudaEventCreate(&b));
-        side_evs.push_back({a, b});
-      }
-      CU(cudaEventRecord(side_evs[side_used].first, s));
-    } else {
-      CU(cudaEventRecord(side_evs[side_used].second, s));
-      ++side_used;
-    }
   }
 };
 
@@ -739,7 +721,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   g.c_group_stride = L->per_expert;
   // the optimizer follows this backward and the expert family needs no data-parallel sync:
   // AdamW runs inside the wgrad epilogues (W2 is no longer read: dgrad2 ran before)
-  const bool fuse_adam = L->overlap_opt && L->fuse_ok;
+  const bool fuse_adam = L->step_follows && L->fuse_ok;
   if (fuse_adam) {
     family_begin(L, L->fam_exp, s);
     set_adam_epilogue(L, g, L->off_w2);
@@ -1154,13 +1136,9 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   if (L->fuse_ok) {
     int least = 0, greatest = 0;
     CU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    CU(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, least));
     CU(cudaStreamCreateWithPriority(&L->hs, cudaStreamNonBlocking, greatest));
     CU(cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&L->ev_w2, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&L->ev_w1, cudaEventDisableTiming));
-    CU(cudaEventCreateWithFlags(&L->ev_side_done, cudaEventDisableTiming));
   }
   CU(cudaDeviceSynchronize());
 }
@@ -1203,14 +1181,14 @@ int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
   });
 }
 void layer_backward_then_step(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
-  L->overlap_opt = true;  // fuse_ok decides inside: AdamW in the wgrad epilogues
+  L->step_follows = true;  // fuse_ok decides inside: AdamW in the wgrad epilogues
   try {
     layer_backward(L, dy, da, s);
   } catch (...) {
-    L->overlap_opt = false;
+    L->step_follows = false;
     throw;
   }
-  L->overlap_opt = false;
+  L->step_follows = false;
 }
 
 void layer_set_forward_mode(ted_layer* L, int mode) {
@@ -1262,13 +1240,8 @@ void ted_layer_destroy(ted_layer* L) {
   cudaDeviceSynchronize();
   for (auto& g : L->graphs) graph_reset(g);
   for (cudaEvent_t e : L->evs) cudaEventDestroy(e);
-  for (auto& pr : L->side_evs) {
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
-  }
-  for (cudaEvent_t e : {L->ev_w2, L->ev_w1, L->ev_side_done, L->ev_fork, L->ev_join})
+  for (cudaEvent_t e : {L->ev_fork, L->ev_join})
     if (e) cudaEventDestroy(e);
-  if (L->side) cudaStreamDestroy(L->side);
   if (L->hs) cudaStreamDestroy(L->hs);
   for (void* ptr : L->ipc_opened) cudaIpcCloseMemHandle(ptr);
   L->ipc_opened.clear();
@@ -1387,17 +1360,17 @@ int ted_layer_optimizer_step(ted_layer* L, void* stream) {
 
 namespace {
 
-// forward + synthetic loss + backward (AdamW overlapped) + optimizer on stream ms
+// forward + synthetic loss + backward (AdamW fused into wgrad) + optimizer on stream ms
 void step_body(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, cudaStream_t ms) {
   layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), ms);
-  L->overlap_opt = L->hs != nullptr;  // the optimizer follows: overlap it with the backward
+  L->step_follows = true;  // the optimizer follows: fuse AdamW into the wgrad epilogues
   try {
     layer_backward(L, nullptr, reinterpret_cast<bf16*>(da), ms);
   } catch (...) {
-    L->overlap_opt = false;
+    L->step_follows = false;
     throw;
   }
-  L->overlap_opt = false;
+  L->step_follows = false;
   layer_optimizer(L, ms);
 }
 
@@ -1447,7 +1420,7 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
     require(L && a && y && da, "null argument");
     cudaStream_t cs = S(stream);
     cudaStream_t ms = cs;
-    if (L->hs) {  // fork onto the high-priority stream; the side stream runs AdamW under it
+    if (L->hs) {  // fork onto the layer's own stream (the graph is captured on it)
       CU(cudaEventRecord(L->ev_fork, cs));
       CU(cudaStreamWaitEvent(L->hs, L->ev_fork, 0));
       ms = L->hs;
@@ -1553,7 +1526,6 @@ int ted_layer_timing(ted_layer* L, int enable) {
     CU(cudaDeviceSynchronize());
     L->timing = enable != 0;
     L->ev_used = 0;
-    L->side_used = 0;
     L->stage_ms.clear();
     L->stage_cnt.clear();
   });
@@ -1573,13 +1545,6 @@ int ted_layer_timing_read(ted_layer* L, char* out, int cap) {
       L->stage_cnt[nm] += 1;
     }
     L->ev_used = 0;
-    for (size_t i = 0; i < L->side_used; ++i) {
-      float ms = 0.f;
-      CU(cudaEventElapsedTime(&ms, L->side_evs[i].first, L->side_evs[i].second));
-      L->stage_ms["adam_overlapped"] += ms;
-      L->stage_cnt["adam_overlapped"] += 1;
-    }
-    L->side_used = 0;
     std::string js = "{";
     bool first = true;
     for (auto& kv : L->stage_ms) {

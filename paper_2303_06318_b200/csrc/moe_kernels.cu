@@ -1090,8 +1090,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
   }
   constexpr int U = 4;  // independent 4-element vectors in flight per thread
   const int64_t total = int64_t(nseg) * seg_len4;
-  // short-lived CTAs (U*256 vectors each) so a concurrently launched persistent GEMM on a
-  // higher-priority stream gets SMs back quickly
+  // one pass of U*256 vectors per CTA (the grid covers the whole range)
   const int64_t stride = blockDim.x;
   {
     const int64_t t0 = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x;
