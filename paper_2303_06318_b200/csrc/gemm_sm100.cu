@@ -263,45 +263,51 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      TileInfo ti;
-      for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp walks the schedule (every value below is warp-uniform, so it lives in
+    // uniform registers) and one elected lane issues: a single-lane loop made the compiler
+    // re-broadcast every descriptor (ELECT + R2UR per MMA), which cost as many issue cycles
+    // as the MMAs themselves.  Shared-memory descriptors are built once; a stage or K step
+    // only adds to their 16 B-granular start-address field.
+    constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+    const uint64_t a_desc0 = A_MN ? ptx::sdesc_sw128(ptx::smem_u32(sA), 64 * BK * 2, 1024)
+                                  : ptx::sdesc_sw128(ptx::smem_u32(sA), 16, 1024);
+    const uint64_t b_desc0 = B_MN ? ptx::sdesc_sw128(ptx::smem_u32(sB), 64 * BK * 2, 1024)
+                                  : ptx::sdesc_sw128(ptx::smem_u32(sB), 16, 1024);
+    constexpr uint64_t kStepA = A_MN ? (2048 >> 4) : (32 >> 4);  // per 16-element K step
+    constexpr uint64_t kStepB = B_MN ? (2048 >> 4) : (32 >> 4);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    TileInfo ti;
+    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+      ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      ptx::tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      const int kb_n = ti.k_len / BK;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        const int kb_n = ti.k_len / BK;
-        for (int kb = 0; kb < kb_n; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a_addr = ptx::smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b_addr = ptx::smem_u32(sB + stage * B_STAGE_BYTES);
+        const uint64_t ad = a_desc0 + uint64_t(stage) * (A_STAGE_BYTES >> 4);
+        const uint64_t bd = b_desc0 + uint64_t(stage) * (B_STAGE_BYTES >> 4);
+        if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 B per 16-element K step inside the 128 B swizzled row.
-            // MN-major: +16 K-rows = 2048 B per step; 64-wide MN atoms 8 KB apart.
-            const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_addr + k * 2048, 64 * BK * 2, 1024)
-                                     : ptx::sdesc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_addr + k * 2048, 64 * BK * 2, 1024)
-                                     : ptx::sdesc_sw128(b_addr + k * 32, 16, 1024);
-            ptx::umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            ptx::umma_bf16(tmem_d, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
           ptx::umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
         }
-        ptx::umma_commit(&tfull[acc]);  // accumulator ready (also fires for k_len == 0)
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
+      }
+      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);  // accumulator ready (k_len 0 too)
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
