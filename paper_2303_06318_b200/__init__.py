@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import os
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 # TED_LIB: load another build of the same library (A/B measurements of kernel variants)

@@ -2,7 +2,6 @@
 same op on the same bf16 operands.  Covers every mode / operand-major / epilogue the
 MoE layer uses (expert FFN fwd, dgrad, wgrad; reference nn.cpp:22-121,
 parallel_linear.cpp:8-40).  Tolerance: bf16 output rounding -> rel-L2 <= 1e-2."""
-import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
