@@ -68,8 +68,11 @@ struct ted_layer {
   HostBuf<long long> h_tabs;
   DevBuf<int> bar;
   DevBuf<unsigned> bar_flags;  // plane barrier: slot r written by plane member r (IPC-mapped)
-  unsigned bar_epoch = 0;
+  DevBuf<unsigned> bar_epoch;  // device barrier epoch (advances on graph replays too)
   bool nccl_barrier = false;
+  // peer exchange with the plan built on the device (no host round trip per step, so the
+  // multi-GPU step is graph-capturable); the host plan is rebuilt lazily for statistics
+  bool devplan = false;
 
   // parameters: expert family (local experts: w1,b1,w2,b2 each) + non-expert (gate)
   Family fam_exp, fam_non;
@@ -273,7 +276,7 @@ void plane_barrier(ted_layer* L, cudaStream_t s) {
     return;
   }
   check(plane_barrier_peer(L->peer_tab.p + size_t(4) * L->plane_size, L->plane_size,
-                           L->plane_rank, ++L->bar_epoch, s),
+                           L->plane_rank, L->bar_epoch.p, s),
         "plane_barrier_peer");
 }
 
@@ -298,10 +301,18 @@ void build_peer_tables(ted_layer* L, const int* cnt) {
   }
 }
 
+// rows the assembled buffers span this step (the device-plan path does not know them on
+// the host: the whole workspace, the GEMMs schedule tiles from the device segments)
+int64_t asm_rows_bound(const ted_layer* L) {
+  return (L->direct && L->devplan) ? L->R_max : std::max<int64_t>(L->plan.asm_rows, 128);
+}
+
 void zero_asm_pads(ted_layer* L, bf16* buf, cudaStream_t s) {
   int maxpad = 0;
-  for (int le = 0; le < L->Eloc; ++le)
-    maxpad = std::max(maxpad, L->plan.seg_off[le + 1] - L->plan.seg_off[le] - L->plan.seg_rows[le]);
+  if (L->direct && L->devplan) maxpad = kPad - 1;
+  else
+    for (int le = 0; le < L->Eloc; ++le)
+      maxpad = std::max(maxpad, L->plan.seg_off[le + 1] - L->plan.seg_off[le] - L->plan.seg_rows[le]);
   if (maxpad > 0)
     check(zero_pad_rows(buf, L->h, L->h, L->seg_off.p, L->seg_valid_view, L->Eloc, maxpad, s),
           "zero_pad_rows");
@@ -426,6 +437,32 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     // pad rows: at most 127 per expert
     check(zero_pad_rows(L->x_asm.p, h, h, L->seg_off.p, L->seg_valid_view, E, kPad, s), "zero_pad");
     rows = L->R_max;
+  } else if (L->direct && L->devplan) {
+    L->mark("count_exchange", s);
+    // chunk counts over the plane (the reference's A2A metadata, fabric.cpp:282-285; also
+    // orders this step's peer writes after every peer's previous-step reads), then the
+    // exchange plan on the device
+    const size_t nc = size_t(L->Tc) * E;
+    NC(ncclAllGather(L->kc.p, L->kc_all.p, nc, ncclInt32, L->plane_c, s));
+    check(plan_peer(L->kc_all.p, L->T, L->P, E, L->Tc, L->ep, L->dtd ? L->t : 0, L->seg_off.p,
+                    L->disp_base.p, L->disp_base.p + E, s),
+          "plan_peer");
+    L->mark("dispatch_peer", s);
+    PeerDst pd;
+    pd.peers = peer_table(L, 0);
+    pd.disp_base = L->disp_base.p;
+    pd.send_base = L->send_base.p;
+    pd.Eloc = L->Eloc;
+    pd.Tp = L->T;
+    pd.my_t = L->t;
+    pd.all_replicas = L->dtd ? 1 : 0;
+    check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
+          "scatter_rows_peer");
+    L->mark("barrier", s);
+    plane_barrier(L, s);
+    L->mark("zero_pad", s);
+    zero_asm_pads(L, L->x_asm.p, s);
+    rows = asm_rows_bound(L);
   } else {
     L->mark("count_exchange", s);
     // count exchange over EP (the reference's A2A metadata, fabric.cpp:282-285)
@@ -493,7 +530,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     }
     L->mark("zero_pad", s);
     zero_asm_pads(L, L->x_asm.p, s);
-    rows = std::max<int64_t>(L->plan.asm_rows, 128);
+    rows = asm_rows_bound(L);
   }
 
   if (L->fwd_mode == FWD_RECORD && !L->local) {  // CAC: stash the exchanged expert rows
@@ -666,7 +703,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     plane_barrier(L, s);
     L->mark("zero_pad", s);
     zero_asm_pads(L, L->dfe_asm.p, s);
-    rows = std::max<int64_t>(L->plan.asm_rows, 128);
+    rows = asm_rows_bound(L);
   } else {
     a2a_dispatch(L, L->dfe_send.p, L->dfe_asm.p, s);  // moe.cpp:614
     if (L->dtd) {
@@ -676,7 +713,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     }
     L->mark("zero_pad", s);
     zero_asm_pads(L, L->dfe_asm.p, s);
-    rows = std::max<int64_t>(L->plan.asm_rows, 128);
+    rows = asm_rows_bound(L);
   }
   bf16* P = L->fam_exp.param.p;
   bf16* G = L->fam_exp.grad.p;
@@ -921,6 +958,10 @@ void setup_peer_exchange(ted_layer* L) {
   L->bar.zero();
   L->bar_flags.alloc(size_t(L->plane_size));
   L->bar_flags.zero();
+  L->bar_epoch.alloc(1);
+  L->bar_epoch.zero();
+  const char* dp = std::getenv("TED_DEVPLAN");
+  L->devplan = !(dp && std::strcmp(dp, "0") == 0);
   const char* bv = std::getenv("TED_BARRIER");
   L->nccl_barrier = bv && std::strcmp(bv, "nccl") == 0;
   constexpr int NB = 5;  // x_asm, dfe_asm, fe_asm, dx_asm, barrier flags
@@ -1427,7 +1468,7 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
     }
     // stage timing runs eagerly (event pairs around every stage; the host enqueues faster
     // than the GPU drains, so the intervals are kernel time)
-    if (L->local && L->hs && L->use_graph && !L->timing) {
+    if ((L->local || (L->direct && L->devplan)) && L->hs && L->use_graph && !L->timing) {
       family_reset_if_needed(L->fam_non, ms);  // set_param resets stay outside the graph
       family_reset_if_needed(L->fam_exp, ms);
       ted_layer::Graph* hit = nullptr;
@@ -1488,6 +1529,16 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
       o->asm_rows = so[E];
       for (int e = 0; e < E && e < 64; ++e) o->kept_per_expert[e] = kc[e];
     } else {
+      if (L->direct && L->devplan) {  // the step planned on the device: rebuild the host plan
+        const size_t nc = size_t(Tc) * E;
+        std::vector<int> all(nc * L->plane_size), cnt(nc * L->P);
+        CU(cudaMemcpy(all.data(), L->kc_all.p, all.size() * sizeof(int),
+                      cudaMemcpyDeviceToHost));
+        for (int src = 0; src < L->P; ++src)
+          std::memcpy(cnt.data() + size_t(src) * nc, all.data() + size_t(L->T * src) * nc,
+                      nc * sizeof(int));
+        L->plan = build_plan(L->P, L->T, E, L->dtd, L->ep, L->t, cnt.data());
+      }
       o->send_rows = L->plan.send_rows;
       o->a2a_rows_offrank = L->plan.a2a_rows_offrank;
       o->a2a_bytes_fwd = 2 * L->plan.a2a_rows_total * hb;

@@ -257,10 +257,18 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
 // arrived in this GPU's own array (system-scope acquire).  A member that never arrives
 // turns into a trapped kernel after ~20 s instead of a hung GPU.
 __global__ void plane_barrier_kernel(const unsigned long long* __restrict__ flags, int PS,
-                                     int me, unsigned epoch) {
+                                     int me, unsigned* __restrict__ epoch_dev) {
+  // the epoch lives on the device (every member runs the same barrier sequence), so a
+  // captured CUDA graph of the step advances it on every replay
+  __shared__ unsigned s_epoch;
   const int i = threadIdx.x;
+  if (i == 0) {
+    s_epoch = *epoch_dev + 1;
+    *epoch_dev = s_epoch;
+  }
   __threadfence_system();
   __syncthreads();
+  const unsigned epoch = s_epoch;
   if (i < PS) {
     unsigned* dst = reinterpret_cast<unsigned*>(flags[i]) + me;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
@@ -277,10 +285,57 @@ __global__ void plane_barrier_kernel(const unsigned long long* __restrict__ flag
   __threadfence_system();
 }
 
-cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me, unsigned epoch,
-                               cudaStream_t s) {
+cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
+                               unsigned* epoch_dev, cudaStream_t s) {
   if (PS < 1 || PS > 1024) return cudaErrorInvalidValue;
-  plane_barrier_kernel<<<1, ((PS + 31) / 32) * 32, 0, s>>>(flags, PS, me, epoch);
+  plane_barrier_kernel<<<1, ((PS + 31) / 32) * 32, 0, s>>>(flags, PS, me, epoch_dev);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+// The peer-exchange plan on the device (ted_plan.h's offsets, no host round trip): from the
+// plane-gathered chunk counts (member t + T*ep contributes [Tc][E]; TP peers route
+// identical tokens, so the t = 0 members' counts are the sources' counts) compute this
+// rank's assembled segments (seg_off[Eloc+1], then valid rows [Eloc]) and, for every
+// expert e, where this rank's rows land in e's assembled buffer: disp_base[e] (my chunk)
+// and pull_base[c][e] (every chunk c, for the return pulls).  One thread per expert.
+__global__ void plan_peer_kernel(const int* __restrict__ kc_all, int T, int P, int E, int Tc,
+                                 int my_ep, int my_c, int* __restrict__ seg,
+                                 long long* __restrict__ disp_base,
+                                 long long* __restrict__ pull_base) {
+  const int Eloc = E / P;
+  auto C = [&](int s_, int c, int e) { return kc_all[(int64_t(T) * s_ * Tc + c) * E + e]; };
+  const int e = threadIdx.x;
+  if (e < E) {
+    const int ep2 = e / Eloc, le = e % Eloc;
+    long long base = 0;  // segment start of local expert le on rank ep2 (128-padded)
+    for (int l2 = 0; l2 < le; ++l2) {
+      long long rows = 0;
+      for (int c = 0; c < Tc; ++c)
+        for (int s_ = 0; s_ < P; ++s_) rows += C(s_, c, ep2 * Eloc + l2);
+      base += (rows + 127) / 128 * 128;
+    }
+    long long r = base;
+    for (int c = 0; c < Tc; ++c) {
+      long long before = 0;
+      for (int s_ = 0; s_ < my_ep; ++s_) before += C(s_, c, e);
+      pull_base[c * E + e] = r + before;
+      if (c == my_c) disp_base[e] = r + before;
+      for (int s_ = 0; s_ < P; ++s_) r += C(s_, c, e);
+    }
+    if (ep2 == my_ep) {
+      seg[le] = int(base);
+      seg[Eloc + 1 + le] = int(r - base);
+      if (le == Eloc - 1) seg[Eloc] = int((r + 127) / 128 * 128);
+    }
+  }
+}
+
+cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep, int my_c,
+                      int* seg, long long* disp_base, long long* pull_base, cudaStream_t s) {
+  if (E < 1 || E > 1024 || E % P != 0) return cudaErrorInvalidValue;
+  plan_peer_kernel<<<1, ((E + 31) / 32) * 32, 0, s>>>(kc_all, T, P, E, Tc, my_ep, my_c, seg,
+                                                     disp_base, pull_base);
   count_launch(1);
   return cudaGetLastError();
 }

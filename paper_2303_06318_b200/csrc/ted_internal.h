@@ -164,8 +164,12 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
                               cudaStream_t s);
 // y[k] = prob[k] * row(k), fhome[k] = row(k) (token order, for the backward), loss partials
 // barrier of the EP x TP plane through IPC-mapped flag arrays (flags[r] = member r's array)
-cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me, unsigned epoch,
-                               cudaStream_t s);
+cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
+                               unsigned* epoch_dev, cudaStream_t s);
+// the peer-exchange plan on the device: seg = [seg_off Eloc+1][valid rows Eloc],
+// disp_base [E], pull_base [Tc][E] from the plane-gathered counts
+cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep, int my_c,
+                      int* seg, long long* disp_base, long long* pull_base, cudaStream_t s);
 cudaError_t combine_pull(const RowSrc& src, const float* prob, int64_t n, int h, bf16* y,
                          bf16* fhome, float* loss_part, cudaStream_t s);
 // dchosen = <fhome[k], dy[k]> (token-order fhome), dlogits, and p*dy rows scattered to the

@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--corrupt", type=int, default=0)
     ap.add_argument("--ledger", type=int, default=0)
     ap.add_argument("--skew", type=float, default=0.0)
+    ap.add_argument("--step-check", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -153,6 +154,45 @@ def main():
             print("MGPU-OK " + json.dumps(report), flush=True)
     dist.barrier()
     L.close()
+    if args.step_check:
+        # ted_layer_step (fused AdamW; a replayed CUDA graph on the peer path) against the
+        # separate forward / backward / optimizer_step calls: same parameters after 3 steps
+        layers = []
+        for _ in range(2):
+            u = [ted.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(u, src=0)
+            Lx = ted.MoeLayer(ted.MoeModelConfig(1, h, E, n, args.seed), topo,
+                              ted.RunFlags(dtd=bool(args.dtd)), capacity_factor=cf, rank=rank,
+                              nccl_uid=u[0])
+            Lx.set_param("layer0.gate.w", inp["wg"])
+            for le in range(Eloc):
+                e = ep * Eloc + le
+                for k in ("w1", "b1", "w2", "b2"):
+                    Lx.set_param(f"layer0.expert{e}.{k}", inp[k][e])
+            layers.append(Lx)
+        La, Lb = layers
+        for _ in range(3):
+            La.step(a, y, da)
+            Lb.forward(a, y)
+            Lb.backward(None, da)
+            Lb.optimizer_step()
+        torch.cuda.synchronize()
+        errs = []
+        for le in range(Eloc):
+            e = ep * Eloc + le
+            for k in ("w1", "b1", "w2", "b2"):
+                pa, pb = La.get_param(f"layer0.expert{e}.{k}"), Lb.get_param(f"layer0.expert{e}.{k}")
+                errs.append(rel(pa, pb))
+        errs.append(rel(La.get_param("layer0.gate.w"), Lb.get_param("layer0.gate.w")))
+        worst_step = max(errs)
+        allw = [None] * world
+        dist.all_gather_object(allw, worst_step)
+        La.close()
+        Lb.close()
+        if rank == 0:
+            assert max(allw) < 1e-3, f"step (graph) vs separate calls: {allw}"
+            print("MGPU-OK step-check " + json.dumps({"worst": max(allw)}), flush=True)
+        dist.barrier()
     dist.destroy_process_group()
 
 

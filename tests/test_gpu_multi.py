@@ -103,3 +103,14 @@ def test_four_gpus_routing_stress(E, cf):
         pytest.skip("needs 4 GPUs")
     _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--experts", str(E), "--cf", str(cf),
          "--skew", "3.0", "--tokens", "1024")
+
+
+@pytest.mark.parametrize("nproc,tp,ep,dtd", [(2, 2, 1, 1), (4, 2, 2, 1), (4, 2, 2, 0)])
+def test_step_graph_matches_separate_calls(nproc, tp, ep, dtd):
+    """ted_layer_step on the peer path (device-side exchange plan, fused AdamW, replayed
+    CUDA graph) leaves the same parameters as forward / backward / optimizer_step."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    out = _run(nproc, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd), "--experts", "8",
+               "--step-check", "1")
+    assert "step-check" in out
