@@ -15,11 +15,14 @@
 //   KDIM mode (wgrad):       group g reduces over rows [seg_off[g], seg_off[g+1]) of
 //                            A^T and B, writing C_g = A_g^T B_g.
 // Epilogues are fused: bias, bias+GELU (writes pre-activation Z and H), dGELU
-// (dZ = acc * gelu'(Z), Z brought in by TMA).
+// (dZ = acc * gelu'(Z), Z brought in by TMA; optionally the bias-gradient column-sum
+// partials of dZ), and AdamW (the wgrad tile is the gradient of a parameter block:
+// master / m / v updated in the tile-major state layout, bf16 parameter written).
 //
-// Tile 128 x 256 x 64; warp 0 = TMA producer, warp 1 = MMA issuer, warp 2 = TMEM
-// allocator, warps 4.. = epilogue (warp w reads TMEM lanes 32*(w%4)..+31; 8 epilogue warps
-// take one half of the tile's 256 columns each, the 16 of the AdamW variant a quarter).
+// Tile 128 x 256 x 64, banded tile order for L2 reuse; warp 0 = TMA producer, warp 1 = MMA
+// issuer (warp-converged, one elected lane issues), warp 2 = TMEM allocator, warps 4.. =
+// epilogue (warp w reads TMEM lanes 32*(w%4)..+31; 8 epilogue warps take one half of the
+// tile's 256 columns each, the 16 of the AdamW variant a quarter).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>

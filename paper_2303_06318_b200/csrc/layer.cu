@@ -1,16 +1,21 @@
 // layer.cu -- one rank's TED MoE layer: the B200-native MoeRank MoE branch.
 //
 // Forward  (MoeRank::forward_layer, moe.cpp:435-563):
-//   gate -> capacity scan -> [DTD chunk] dispatch pack -> EP all-to-all -> [DTD TP
-//   all-gather] -> GEMM1+bias+GELU -> GEMM2+bias -> [TP all-reduce] -> return all-to-all
-//   -> [DTD TP all-gather] -> combine.
+//   gate -> capacity scan -> [DTD chunk] dispatch -> EP all-to-all + [DTD TP all-gather]
+//   -> GEMM1+bias+GELU -> GEMM2+bias -> [TP all-reduce] + return all-to-all + [DTD home
+//   all-gather] -> combine.  On more than one GPU the bracketed collectives are NVLink
+//   peer-memory kernels (peer_kernels.cu: one scatter, one pull that also sums the TP
+//   partials) ordered by plane barriers; the exchange plan is built on the device, so the
+//   step has no host round trip and ted_layer_step replays it as a CUDA graph.
+//   TED_EXCHANGE=nccl keeps the NCCL send/recv + all-gather + all-reduce version.
 // Backward (MoeRank::backward_layer, moe.cpp:582-686): the mirror image, with dgrad
-//   GEMMs (dGELU fused), wgrad GEMMs written straight into the flat expert family,
-//   bias column sums, gate backward.
+//   GEMMs (dGELU and the db1 column sums fused), wgrad GEMMs written straight into the
+//   flat expert family -- or, when the optimizer step follows and the family is
+//   unsharded, with AdamW fused into their epilogues -- bias column sums, gate backward.
 // Optimizer (run_grad_sync / family_optimizer_step, moe.cpp:699-741): DP all-reduce of
 //   each family, AdamW over the ZeRO-1 owned range, completion all-gather.
-// Collectives: NCCL over NVLink/NVSwitch; one communicator per TED group family
-// (ncclCommSplit of the world communicator, colours from topology.cpp:56-93).
+// Communicators: one per TED group family (ncclCommSplit of the world communicator,
+// colours from topology.cpp:56-93) plus the EP x TP plane of each data replica.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>

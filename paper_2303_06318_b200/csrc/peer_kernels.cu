@@ -12,8 +12,9 @@
 //   backward dispatch (moe.cpp:603-632): p * dy rows stored into the experts' dFe buffers
 //       exactly like the forward dispatch; the return of dX (with the column-parallel
 //       dgrad's TP partial sums, parallel_linear.cpp:19) is a pull in gate backward.
-// Ordering across ranks is provided by stream-ordered NCCL barriers in layer.cu; every
-// writer kernel ends with a system-scope fence.
+// Ordering across ranks: plane barriers through IPC-mapped flag arrays (below; NCCL
+// all-reduce barriers with TED_BARRIER=nccl); every writer kernel ends with a system-scope
+// fence.  plan_peer builds the exchange plan on the device.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
