@@ -223,18 +223,19 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
   const int total = s_tstart[p.groups];
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      TileInfo ti;
-      for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
-        const int kb_n = ti.k_len / BK;
-        for (int kb = 0; kb < kb_n; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
+    // ------------------------------------------------------------ TMA producer
+    // warp-converged like the MMA issuer: uniform coordinates, one elected lane issues
+    int stage = 0;
+    uint32_t phase = 0;
+    TileInfo ti;
+    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+      const int kb_n = ti.k_len / BK;
+      for (int kb = 0; kb < kb_n; ++kb) {
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
+        uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
+        if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
-          uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
           if (p.mode == GEMM_ROWS) {
             const int row0 = s_off[ti.g] + ti.m_blk * BM;
             const int k0 = kb * BK;
@@ -258,10 +259,11 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
               ptx::tma_load_3d(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
                                ti.n_blk * BN + i * 64, krow, 0);
           }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        __syncwarp();
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
