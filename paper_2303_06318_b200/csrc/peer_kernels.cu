@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "ted_internal.h"
+#include "ted_plan.h"
 #include "ted_vec.cuh"
 
 namespace ted {
@@ -304,32 +305,8 @@ __global__ void plan_peer_kernel(const int* __restrict__ kc_all, int T, int P, i
                                  int my_ep, int my_c, int* __restrict__ seg,
                                  long long* __restrict__ disp_base,
                                  long long* __restrict__ pull_base) {
-  const int Eloc = E / P;
-  auto C = [&](int s_, int c, int e) { return kc_all[(int64_t(T) * s_ * Tc + c) * E + e]; };
   const int e = threadIdx.x;
-  if (e < E) {
-    const int ep2 = e / Eloc, le = e % Eloc;
-    long long base = 0;  // segment start of local expert le on rank ep2 (128-padded)
-    for (int l2 = 0; l2 < le; ++l2) {
-      long long rows = 0;
-      for (int c = 0; c < Tc; ++c)
-        for (int s_ = 0; s_ < P; ++s_) rows += C(s_, c, ep2 * Eloc + l2);
-      base += (rows + 127) / 128 * 128;
-    }
-    long long r = base;
-    for (int c = 0; c < Tc; ++c) {
-      long long before = 0;
-      for (int s_ = 0; s_ < my_ep; ++s_) before += C(s_, c, e);
-      pull_base[c * E + e] = r + before;
-      if (c == my_c) disp_base[e] = r + before;
-      for (int s_ = 0; s_ < P; ++s_) r += C(s_, c, e);
-    }
-    if (ep2 == my_ep) {
-      seg[le] = int(base);
-      seg[Eloc + 1 + le] = int(r - base);
-      if (le == Eloc - 1) seg[Eloc] = int((r + 127) / 128 * 128);
-    }
-  }
+  if (e < E) peer_plan_expert(kc_all, T, P, E, Tc, my_ep, my_c, e, disp_base, pull_base, seg);
 }
 
 cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep, int my_c,

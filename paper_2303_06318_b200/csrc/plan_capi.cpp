@@ -56,4 +56,31 @@ int ted_plan_build(int P, int T, int E, int dtd, int my_ep, int my_t, const int*
   }
 }
 
+// blk_row / blk_cnt [Eloc][Tc][P] of this rank's assembled layout
+int ted_plan_blocks(int P, int T, int E, int dtd, int my_ep, int my_t, const int* cnt,
+                    int64_t* blk_row, int* blk_cnt) {
+  try {
+    ted::LayerPlan L = ted::build_plan(P, T, E, dtd != 0, my_ep, my_t, cnt);
+    std::memcpy(blk_row, L.blk_row.data(), sizeof(int64_t) * L.blk_row.size());
+    std::memcpy(blk_cnt, L.blk_cnt.data(), sizeof(int) * L.blk_cnt.size());
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// the device plan's per-expert function run on the CPU (kc_all: [plane][Tc][E] in plane
+// order t + T*ep): seg [2*Eloc+1], disp_base [E], pull_base [Tc][E]
+int ted_plan_peer_tables(int T, int P, int E, int Tc, int my_ep, int my_c, const int* kc_all,
+                         int* seg, long long* disp_base, long long* pull_base) {
+  if (E < 1 || P < 1 || E % P != 0) {
+    g_err = "experts must be a multiple of the expert-parallel degree";
+    return 2;
+  }
+  for (int e = 0; e < E; ++e)
+    ted::peer_plan_expert(kc_all, T, P, E, Tc, my_ep, my_c, e, disp_base, pull_base, seg);
+  return 0;
+}
+
 }  // extern "C"

@@ -160,4 +160,45 @@ inline LayerPlan build_plan(int P, int T, int E, bool dtd, int my_ep, int my_t,
   return L;
 }
 
+#ifdef __CUDACC__
+#define TED_HD __host__ __device__
+#else
+#define TED_HD
+#endif
+
+// The peer-exchange plan as the device computes it (plan_peer_kernel, one call per
+// expert e): from the plane-gathered chunk counts (member t + T*ep contributes [Tc][E];
+// the t = 0 members' rows are the sources' counts) the row where this rank's block
+// (expert e, chunk c, source my_ep) starts in e's assembled buffer -- pull_base[c*E + e],
+// and disp_base[e] for this rank's own chunk my_c -- plus, for a local expert, its
+// segment (seg[le] = start, seg[Eloc+1+le] = valid rows, seg[Eloc] = padded end).  Same
+// offsets as build_plan's blk_row / seg_off (tested on the CPU through plan_capi.cpp).
+TED_HD inline void peer_plan_expert(const int* kc_all, int T, int P, int E, int Tc, int my_ep,
+                                    int my_c, int e, long long* disp_base,
+                                    long long* pull_base, int* seg) {
+  const int Eloc = E / P;
+  const int ep2 = e / Eloc, le = e % Eloc;
+  auto C = [&](int s_, int c, int ee) { return kc_all[(int64_t(T) * s_ * Tc + c) * E + ee]; };
+  long long base = 0;  // segment start of local expert le on rank ep2 (128-padded)
+  for (int l2 = 0; l2 < le; ++l2) {
+    long long rows = 0;
+    for (int c = 0; c < Tc; ++c)
+      for (int s_ = 0; s_ < P; ++s_) rows += C(s_, c, ep2 * Eloc + l2);
+    base += (rows + 127) / 128 * 128;
+  }
+  long long r = base;
+  for (int c = 0; c < Tc; ++c) {
+    long long before = 0;
+    for (int s_ = 0; s_ < my_ep; ++s_) before += C(s_, c, e);
+    pull_base[c * E + e] = r + before;
+    if (c == my_c) disp_base[e] = r + before;
+    for (int s_ = 0; s_ < P; ++s_) r += C(s_, c, e);
+  }
+  if (ep2 == my_ep) {
+    seg[le] = int(base);
+    seg[Eloc + 1 + le] = int(r - base);
+    if (le == Eloc - 1) seg[Eloc] = int((r + 127) / 128 * 128);
+  }
+}
+
 }  // namespace ted

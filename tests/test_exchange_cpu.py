@@ -12,6 +12,7 @@ Checks, against an independent numpy restatement of the reference's ordering rul
     the GPU combine kernel reads (pos_home), dropped tokens nowhere (moe.cpp:504-556);
   * ledger bytes equal the reference's predict_comm_volume (cost_model.cpp:346-416).
 """
+import ctypes as C
 import os
 
 import numpy as np
@@ -260,3 +261,47 @@ def test_gloo_exchange(world, T, P, E, dtd):
     for p in procs:
         p.join(timeout=60)
     assert all(v == "ok" for v in res.values()), res
+
+
+@pytest.mark.parametrize("P,T,E,dtd", [(2, 2, 4, 1), (4, 2, 16, 1), (4, 2, 16, 0), (1, 2, 8, 1),
+                                       (4, 1, 8, 0), (2, 4, 8, 1)])
+def test_device_plan_matches_host_planner(P, T, E, dtd):
+    """The peer path's device plan (peer_plan_expert, run by plan_peer_kernel; here through
+    its CPU build) places every rank's rows exactly where the host planner's assembled
+    layout puts them (build_plan's blk_row / seg_off, the layout the NCCL path and the
+    reference ordering tests use)."""
+    L = X.plan_lib()
+    Tc = T if (dtd and T > 1) else 1
+    Eloc = E // P
+    rng = np.random.default_rng(P * 100 + T * 10 + E + dtd)
+    cnt = rng.integers(0, 300, (P, Tc, E)).astype(np.int32)
+    plane = np.zeros((P * T, Tc, E), np.int32)  # member t + T*ep; TP peers agree
+    for ep in range(P):
+        for t in range(T):
+            plane[t + T * ep] = cnt[ep]
+    blocks = {}
+    for ep2 in range(P):
+        br = np.zeros(Eloc * Tc * P, np.int64)
+        bc = np.zeros(Eloc * Tc * P, np.int32)
+        assert L.ted_plan_blocks(P, T, E, dtd, ep2, 0, cnt.ctypes.data_as(C.c_void_p),
+                                 br.ctypes.data_as(C.c_void_p), bc.ctypes.data_as(C.c_void_p)) == 0
+        blocks[ep2] = br.reshape(Eloc, Tc, P)
+    for ep in range(P):
+        for t in range(T):
+            my_c = t if Tc > 1 else 0
+            seg = np.zeros(2 * Eloc + 1, np.int32)
+            disp = np.zeros(E, np.int64)
+            pull = np.zeros(Tc * E, np.int64)
+            assert L.ted_plan_peer_tables(T, P, E, Tc, ep, my_c, plane.ctypes.data_as(C.c_void_p),
+                                          seg.ctypes.data_as(C.c_void_p),
+                                          disp.ctypes.data_as(C.c_void_p),
+                                          pull.ctypes.data_as(C.c_void_p)) == 0
+            pull = pull.reshape(Tc, E)
+            for e in range(E):
+                ep2, le = divmod(e, Eloc)
+                for c in range(Tc):
+                    assert pull[c, e] == blocks[ep2][le, c, ep]
+                assert disp[e] == blocks[ep2][le, my_c, ep]
+            pl = X.build_plan(P, T, E, dtd, ep, t, cnt)
+            np.testing.assert_array_equal(seg[:Eloc + 1], pl["seg_off"])
+            np.testing.assert_array_equal(seg[Eloc + 1:], pl["seg_rows"])
