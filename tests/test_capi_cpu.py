@@ -98,3 +98,25 @@ def test_plan_library_loads():
     from tests import _exchange as X
     pl = X.build_plan(2, 2, 4, True, 0, 1, np.ones((2, 2, 4), np.int32))
     assert pl["seg_off"][-1] % 128 == 0
+
+
+def _build_example(tmp_path):
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    exe = str(tmp_path / "layer_step")
+    cmd = ["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+           "-I", "/usr/local/cuda/include", os.path.join(root, "examples", "layer_step.c"),
+           "-L", os.path.join(root, "paper_2303_06318_b200"), "-lted_b200",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,--allow-shlib-undefined", "-o", exe]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe, root
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    """include/ted.h is plain C: a C11 host program (the reference-side integration
+    sketch of INTEGRATION.md) compiles with -Wall -Werror and links against the library."""
+    _build_example(tmp_path)

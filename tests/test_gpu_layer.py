@@ -153,3 +153,18 @@ def test_fused_adam_step_matches_unfused_path():
     assert rel_l2(La.get_param("layer0.gate.w"), Lb.get_param("layer0.gate.w")) < 1e-3
     La.close()
     Lb.close()
+
+
+def test_c_host_program_trains_the_layer(tmp_path):
+    """The C host program (examples/layer_step.c) drives the layer through the C ABI alone
+    (no Python, no torch in the process): three steps, finite decreasing loss."""
+    import os
+    import subprocess
+    from tests.test_capi_cpu import _build_example
+    exe, root = _build_example(tmp_path)
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.join(root, "paper_2303_06318_b200") + ":" +
+               os.environ.get("LD_LIBRARY_PATH", ""))
+    r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    losses = [float(line.split()[-1]) for line in r.stdout.splitlines() if line.startswith("step")]
+    assert len(losses) == 3 and all(np.isfinite(losses)) and losses[-1] < losses[0], r.stdout
