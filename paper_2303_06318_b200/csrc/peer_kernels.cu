@@ -29,7 +29,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpTok = kRouteBlock / 8;
 
-__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
 
 // Row r of this token on replica t of expert e's EP rank.
 __device__ __forceinline__ bf16* dst_row(const PeerDst& D, int t, int e, int64_t r, int h) {
