@@ -42,7 +42,6 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE_BYTES = BN * BK * 2;  // 32 KB
 constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
 constexpr int MAX_GROUPS = 128;  // local experts per launch
-constexpr int MAX_EPI_WARPS = 16;
 constexpr uint32_t TMEM_COLS = 512;                // 2 accumulator buffers x 256 fp32 columns
 constexpr int EPI_BLOCK_BYTES = 32 * 32 * 2;       // one 32x32 bf16 staging block
 
