@@ -159,11 +159,12 @@ def ref_sample_plan(w, sample_tokens):
     return sample_tokens, (w["experts"] if h <= 1024 else min(w["experts"], 2))
 
 
-def reference_tokens_per_s(w, sample_tokens: int, experts: int):
+def reference_tokens_per_s(w, sample_tokens: int, experts: int, reps: int = 1):
     """Time the unmodified reference (oracle/_ref) on a bounded sample: the MoE branch
     (gate_forward + per-expert linear/gelu fwd+bwd + gate_backward, one thread per expert)
-    on `sample_tokens` tokens routed over `experts` experts, plus OptimizerShard::step_owned
-    on the layer's full parameter count amortised over the full batch."""
+    on `sample_tokens` tokens routed over `experts` experts (`reps` timed repetitions,
+    mean), plus OptimizerShard::step_owned on the layer's full parameter count amortised
+    over the full batch."""
     import ctypes as C
 
     import numpy as np
@@ -184,11 +185,14 @@ def reference_tokens_per_s(w, sample_tokens: int, experts: int):
     y, da = np.empty((sample_tokens, h)), np.empty((sample_tokens, h))
     dwg, dw1, db1 = np.empty((h, E)), np.empty((E, h, f)), np.empty((E, f))
     dw2, db2 = np.empty((E, f, h)), np.empty((E, h))
-    t0 = time.perf_counter()
-    rc = R.ref_moe_sublayer(sample_tokens, h, f, E, a, wg, w1, b1, w2, b2, dy, y, da, dwg, dw1,
-                            db1, dw2, db2, threads)
-    t_layer = time.perf_counter() - t0
-    assert rc == 0, R.ref_last_error()
+    t_layer = 0.0
+    for _ in range(max(1, reps)):
+        t0 = time.perf_counter()
+        rc = R.ref_moe_sublayer(sample_tokens, h, f, E, a, wg, w1, b1, w2, b2, dy, y, da, dwg,
+                                dw1, db1, dw2, db2, threads)
+        t_layer += time.perf_counter() - t0
+        assert rc == 0, R.ref_last_error()
+    t_layer /= max(1, reps)
     # optimizer over a slice of the family, scaled to the layer's parameter count
     params = w["experts"] * (2 * h * f + f + h) + h * w["experts"]
     probe = min(params, 4_000_000)
@@ -208,7 +212,9 @@ def run_reference(args, w, rank, world):
     if rank != 0:
         return
     sample, threads = ref_sample_plan(w, args.ref_sample)
-    tps, t_layer, t_adam = reference_tokens_per_s(w, sample, threads)
+    # one bounded sample per timed step, capped so the whole run stays within minutes
+    reps = max(1, min(args.steps, 3 if w["hidden"] > 1024 else 5))
+    tps, t_layer, t_adam = reference_tokens_per_s(w, sample, threads, reps)
     ms = w["tokens"] / tps * 1e3
     line = {
         "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
@@ -220,7 +226,8 @@ def run_reference(args, w, rank, world):
                    "experts": w["experts"], "tokens": w["tokens"], "capacity_factor": None},
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
                          "sample": f"{sample} tokens through the reference MoE branch "
-                                   f"({t_layer:.2f} s, {threads} expert threads) + "
+                                   f"({t_layer:.2f} s mean of {reps} timed repetitions, "
+                                   f"{threads} expert threads) + "
                                    f"step_owned over the layer's parameters ({t_adam:.2f} s, "
                                    f"1 thread) amortised over {w['tokens']} tokens"},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
