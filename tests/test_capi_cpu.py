@@ -92,6 +92,17 @@ def test_no_cpu_fallback_without_gpu():
     rc = ted.lib().ted_adam_step(None, None, None, None, None, 0, 4, 1, C.byref(a), C.byref(t),
                                  C.byref(pk), None)
     assert rc == ted.TED_ERR_RUNTIME
+    with pytest.raises(ted.TedRuntimeError):  # the whole model: no CPU path either
+        ted.TedModel(ted.MoeModelConfig(2, 256, 4, 64, 1), ted.TedConfig())
+
+
+def test_model_config_errors_are_config_status():
+    """Model-level configuration errors map to InvalidConfigError (status 2) before any
+    device work, like the reference's validate_model (moe.cpp:100-113)."""
+    with pytest.raises(ted.InvalidConfigError, match="layers must be >= 1"):
+        ted.TedModel(ted.MoeModelConfig(0, 256, 4, 64, 1), ted.TedConfig())
+    with pytest.raises(ted.InvalidConfigError, match="multiples of 256"):
+        ted.TedModel(ted.MoeModelConfig(2, 200, 4, 64, 1), ted.TedConfig())
 
 
 def test_plan_library_loads():
