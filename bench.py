@@ -2,6 +2,7 @@
 """bench.py -- MoE-layer tokens/s (fwd + bwd + tiled AdamW step) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dtd 0|1]
+                  [--workload c3|c2|c4] [--layers L] [--no-cpu-baseline] [--no-dtd-compare]
 
 Workload (all N): configs[2] of BASELINE.json, the layer the north-star target is quoted on
 -- d=4096, ffn=16384, 16 experts top-1, 32768 tokens in total, capacity factor 1.25 --
@@ -17,7 +18,11 @@ A step = one pass of the MoE layer over one batch: gate, capacity routing, dispa
 synthetic loss sum(y^2)/2N, the whole backward, gradient sync and AdamW.
 `value` times K steps with inputs resident in HBM (CUDA events, max over ranks);
 `e2e` repeats it through the public API with the step's tokens copied from pinned host
-memory and the loss read back every step.
+memory (double-buffered on a copy stream: step i+1's copy runs under step i) and the loss
+read back every step.  `roofline` is the dominant kernel (the wgrad GEMMs with the fused
+AdamW, HBM-bound); `roofline_gemm` the forward / dgrad GEMMs against the tensor peak.
+--workload c4 runs configs[3] instead: a layer stack (attention stand-in + MoE / dense FFN)
+through the Trainer-level model API, TP=2 x EP=2 x DP=N/4, ZeRO-1.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref/
 libtedsim_ref.so, the unmodified tedsim sources) on a bounded token sample of the same
