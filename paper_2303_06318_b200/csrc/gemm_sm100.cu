@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
   const int total = s_tstart[p.groups];
-
+  if (warp < 4) {
+  // control warpgroup (the AdamW variant hands registers to its 16 epilogue warps: the
+  // launch bound gives every warp 96; 4 control warps drop to 32, the epilogue takes 112)
+  if (EPI == EPI_ADAM) ptx::regs_dec<32>();
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     // warp-converged like the MMA issuer: uniform coordinates, one elected lane issues
@@ -314,19 +317,123 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
         acc_phase ^= 1;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else if (EPI == EPI_ADAM) {
+    ptx::regs_inc<112>();
+    // --------------------------------------------------- fused AdamW epilogue
+    // AdamW (optimizer.cpp:58-104) over this warp's 32 rows x SPAN columns of every tile.
+    // In the tile-major state layout (blk_off) the warp's share of a tile is, per state
+    // array, SPAN/4 consecutive 512 B chunks (chunk c = 4 columns x 32 rows, lane = row).
+    // The chunks stream through a register ring RING deep: the loads of chunk c+RING-1 are
+    // issued before chunk c is updated, and they run across tile boundaries (the state
+    // does not depend on the accumulator, so the next tile's first chunks are in flight
+    // while this tile finishes and before its accumulator is ready).  The bf16 parameters
+    // of each 32x16 half go out as one TMA tensor store.
+    constexpr int NC = SPAN / 4;  // chunks per warp and tile
+    constexpr int RING = 4;
+    static_assert(NC % RING == 0 && NC % 4 == 0, "ring must tile the chunk walk");
+    const int ew = warp - 4;
+    const int sp = ew & 3, cq = ew >> 2;
+    uint8_t* pblk = sEpi + size_t(ew) * CF::PER_WARP;
+    const float c1 = p.adam_coef[0], c2 = p.adam_coef[1];
+    const uint64_t pol = evict_first_policy();
+    const int nt = p.N / BN;
+    auto state_base = [&](const TileInfo& x) -> int64_t {
+      return int64_t(x.g) * p.c_group_stride + (int64_t(x.m_blk * nt + x.n_blk) << 15) +
+             int64_t((sp << 2) + cq) * 2048 + int64_t(lane) * 4;
+    };
+    float4 ring[RING][3];
+    auto issue = [&](float4 (&r)[3], int64_t o) {
+      r[0] = ld_state(p.adam_master + o, pol);
+      r[1] = ld_state(p.adam_m1 + o, pol);
+      r[2] = ld_state(p.adam_m2 + o, pol);
+    };
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int t = blockIdx.x;
+    TileInfo ti, tn;
+    bool have = decode_tile(p, s_off, s_tstart, total, t, ti);
+    int64_t cur = have ? state_base(ti) : 0;
+    if (have) {
+#pragma unroll
+      for (int c = 0; c < RING - 1; ++c) issue(ring[c], cur + c * 128);
+    }
+    while (have) {
+      const int tnext = t + gridDim.x;
+      const bool have_next = decode_tile(p, s_off, s_tstart, total, tnext, tn);
+      const int64_t nxt = have_next ? state_base(tn) : 0;
+      const int row0 = ti.m_blk * BM + sp * 32;
+      const int colw = ti.n_blk * BN + cq * SPAN;
+      const bool zero = ti.k_len == 0;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t tb = tmem_base + acc * BN + (uint32_t(sp * 32) << 16) + cq * SPAN;
+      float v[16];
+      uint32_t pw[8];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int cpf = c + RING - 1;  // chunk whose loads go out now
+        if (cpf < NC) issue(ring[cpf % RING], cur + cpf * 128);
+        else if (have_next) issue(ring[cpf % RING], nxt + (cpf - NC) * 128);
+        if (c % 4 == 0) {
+          ptx::tmem_ld16(tb + 4 * c, v);
+          if (c == NC - 4) {  // accumulator fully read: the MMA warp may reuse it
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+          }
+        }
+        float4* st = ring[c % RING];
+        float* mq = &st[0].x;
+        float* q1 = &st[1].x;
+        float* q2 = &st[2].x;
+        const int vb = (c % 4) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // the unfused path stores the bf16-rounded gradient: same rounding here
+          const float g = zero ? 0.f : __bfloat162float(__float2bfloat16(v[vb + q]));
+          adamw_elem(mq[q], q1[q], q2[q], g, p.adam, c1, c2);
+        }
+        const int64_t o = cur + c * 128;
+        st_state(p.adam_master + o, st[0], pol);
+        st_state(p.adam_m1 + o, st[1], pol);
+        st_state(p.adam_m2 + o, st[2], pol);
+        pw[(c % 4) * 2] = pack_bf16(mq[0], mq[1]);
+        pw[(c % 4) * 2 + 1] = pack_bf16(mq[2], mq[3]);
+        if (c % 4 == 3) {
+          // bf16 parameters of the half: 32 B rows, SWIZZLE_32B (chunk j of row r at
+          // j ^ ((r>>2)&1)); the previous half's store must have read pblk
+          if (lane == 0) ptx::bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            *reinterpret_cast<uint4*>(pblk + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+                make_uint4(pw[4 * j], pw[4 * j + 1], pw[4 * j + 2], pw[4 * j + 3]);
+          ptx::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_3d(&tmC, pblk, colw + 4 * (c - 3), row0, ti.g);
+            ptx::bulk_commit();
+          }
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+      t = tnext;
+      ti = tn;
+      cur = nxt;
+      have = have_next;
+    }
+    if (lane == 0) ptx::bulk_wait0();
+  } else {
     // -------------------------------------------------------------- epilogue
     const int ew = warp - 4;
     const int sp = ew & 3;      // TMEM sub-partition: lanes 32*(warp%4)..+31
     const int cq = ew >> 2;     // column span (SPAN wide) of the 256-wide tile
     uint8_t* blk0 = sEpi + size_t(ew) * CF::PER_WARP;
     uint8_t* blk1 = blk0 + EPI_BLOCK_BYTES;  // H (bias+GELU only)
-    uint8_t* pblk = blk0;  // EPI_ADAM: the bf16 parameter half block
-    float inv_c1 = 1.f, inv_c2 = 1.f;
-    if (EPI == EPI_ADAM) {
-      inv_c1 = p.adam_coef[0];
-      inv_c2 = p.adam_coef[1];
-    }
     int acc = 0;
     uint32_t acc_phase = 0, zphase = 0;
     TileInfo ti;
@@ -343,81 +450,6 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
       }
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
-      if (EPI == EPI_ADAM) {
-        // Fused AdamW (optimizer.cpp:58-104) over this warp's 32 rows x SPAN columns as
-        // 32x16 half tiles: the half's optimizer state (3 x 2 KB, contiguous in the
-        // tile-major blk_off layout) is loaded into registers first, the TMEM read overlaps
-        // the loads, then master/m/v are stored back and the bf16 parameter block goes out
-        // as one TMA tensor store.
-        constexpr int NH = SPAN / 16;
-        const int64_t gbase = int64_t(gz) * p.c_group_stride + int64_t(lane) * 4;
-        const uint64_t pol = evict_first_policy();
-        const int colw = ti.n_blk * BN + cq * SPAN;
-#pragma unroll 1
-        for (int k = 0; k < NH; ++k) {
-          const int64_t o = gbase + blk_off(row0, colw + 16 * k, p.N);
-          float4 cur[12];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            cur[j] = ld_state(p.adam_master + o + j * 128, pol);
-            cur[4 + j] = ld_state(p.adam_m1 + o + j * 128, pol);
-            cur[8 + j] = ld_state(p.adam_m2 + o + j * 128, pol);
-          }
-          float v[16];
-          ptx::tmem_ld16(tbase + cq * SPAN + 16 * k, v);
-          if (k == NH - 1) {  // accumulator fully read: the MMA warp may reuse it
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-          }
-          float nv[16];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float* mq = &cur[j].x;
-            float* q1 = &cur[4 + j].x;
-            float* q2 = &cur[8 + j].x;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              // the unfused path stores the bf16-rounded gradient: same rounding here
-              const float g = zero ? 0.f : __bfloat162float(__float2bfloat16(v[4 * j + q]));
-              q1[q] = p.b1 * q1[q] + p.omb1 * g;
-              q2[q] = p.b2 * q2[q] + p.omb2 * g * g;
-              mq[q] -= p.lr * ((q1[q] * inv_c1) / (sqrtf(q2[q] * inv_c2) + p.eps) +
-                               p.wd * mq[q]);
-              nv[4 * j + q] = mq[q];
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            st_state(p.adam_master + o + j * 128, cur[j], pol);
-            st_state(p.adam_m1 + o + j * 128, cur[4 + j], pol);
-            st_state(p.adam_m2 + o + j * 128, cur[8 + j], pol);
-          }
-          // bf16 parameters: 32 B rows, SWIZZLE_32B (chunk j of row r at j ^ ((r>>2)&1))
-          if (lane == 0) ptx::bulk_wait_read0();  // the previous half's store has read pblk
-          __syncwarp();
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            uint4 w;
-            w.x = pack_bf16(nv[8 * j + 0], nv[8 * j + 1]);
-            w.y = pack_bf16(nv[8 * j + 2], nv[8 * j + 3]);
-            w.z = pack_bf16(nv[8 * j + 4], nv[8 * j + 5]);
-            w.w = pack_bf16(nv[8 * j + 6], nv[8 * j + 7]);
-            *reinterpret_cast<uint4*>(pblk + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) = w;
-          }
-          ptx::fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_3d(&tmC, pblk, colw + 16 * k, row0, gz);
-            ptx::bulk_commit();
-          }
-        }
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
-        continue;
-      }
 #pragma unroll 1
       for (int c0 = cq * SPAN; c0 < (cq + 1) * SPAN; c0 += 32) {
         const int col = ti.n_blk * BN + c0;

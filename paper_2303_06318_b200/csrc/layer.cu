@@ -657,13 +657,9 @@ void set_adam_epilogue(ted_layer* L, GemmParams& g, int64_t off) {
   g.adam_m1 = F.m1.p + off;
   g.adam_m2 = F.m2.p + off;
   g.adam_coef = F.dcoef.p;
-  g.lr = float(L->adam.lr);
-  g.b1 = float(L->adam.beta1);
-  g.b2 = float(L->adam.beta2);
-  g.omb1 = float(1.0 - L->adam.beta1);
-  g.omb2 = float(1.0 - L->adam.beta2);
-  g.eps = float(L->adam.eps);
-  g.wd = float(L->adam.weight_decay);
+  g.adam = AdamK{float(L->adam.lr), float(L->adam.beta1), float(L->adam.beta2),
+                 float(1.0 - L->adam.beta1), float(1.0 - L->adam.beta2), float(L->adam.eps),
+                 float(L->adam.weight_decay)};
 }
 
 // --------------------------------------------------------------- backward

@@ -1020,15 +1020,14 @@ __global__ void __launch_bounds__(256) adam_kernel(float* __restrict__ master,
     inv_c1 = coef[0];
     inv_c2 = coef[1];
   }
+  const AdamK k{lr, b1, b2, omb1, omb2, eps, wd};
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += stride) {
     const float g = __bfloat162float(grad[begin + i]);
-    const float m = b1 * m1[i] + omb1 * g;
-    const float v = b2 * m2[i] + omb2 * g * g;
+    float m = m1[i], v = m2[i], p = master[i];
+    adamw_elem(p, m, v, g, k, inv_c1, inv_c2);
     m1[i] = m;
     m2[i] = v;
-    float p = master[i];
-    p -= lr * ((m * inv_c1) / (sqrtf(v * inv_c2) + eps) + wd * p);
     master[i] = p;
     param[begin + i] = __float2bfloat16(p);
   }
@@ -1048,6 +1047,7 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
     inv_c1 = coef[0];
     inv_c2 = coef[1];
   }
+  const AdamK k{lr, b1, b2, omb1, omb2, eps, wd};
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len4; i += stride) {
     const uint2 gu = reinterpret_cast<const uint2*>(grad + begin)[i];
@@ -1061,9 +1061,7 @@ __global__ void __launch_bounds__(256) adam_kernel_v4(float* __restrict__ master
     float* pq = &pp.x;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      mp[q] = b1 * mp[q] + omb1 * g[q];
-      vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
-      pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+      adamw_elem(pq[q], mp[q], vp[q], g[q], k, inv_c1, inv_c2);
     }
     reinterpret_cast<float4*>(m1)[i] = mm;
     reinterpret_cast<float4*>(m2)[i] = vv;
@@ -1088,6 +1086,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
     inv_c1 = coef[0];
     inv_c2 = coef[1];
   }
+  const AdamK k{lr, b1, b2, omb1, omb2, eps, wd};
   constexpr int U = 4;  // independent 4-element vectors in flight per thread
   const int64_t total = int64_t(nseg) * seg_len4;
   // one pass of U*256 vectors per CTA (the grid covers the whole range)
@@ -1120,9 +1119,7 @@ __global__ void __launch_bounds__(256) adam_segments_kernel(
       float* pq = &pp[u].x;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        mp[q] = b1 * mp[q] + omb1 * g[q];
-        vp[q] = b2 * vp[q] + omb2 * g[q] * g[q];
-        pq[q] -= lr * ((mp[q] * inv_c1) / (sqrtf(vp[q] * inv_c2) + eps) + wd * pq[q]);
+        adamw_elem(pq[q], mp[q], vp[q], g[q], k, inv_c1, inv_c2);
       }
       reinterpret_cast<float4*>(m1)[idx[u]] = mm[u];
       reinterpret_cast<float4*>(m2)[idx[u]] = vv[u];
@@ -1148,6 +1145,7 @@ __global__ void __launch_bounds__(256) adam_tiles_kernel(
     inv_c1 = coef[0];
     inv_c2 = coef[1];
   }
+  const AdamK k{lr, b1, b2, omb1, omb2, eps, wd};
   const int lane = threadIdx.x & 31;
   const int64_t per_seg = int64_t(rows) * cols / 512;
   const int64_t nblk = per_seg * nseg;
@@ -1184,9 +1182,7 @@ __global__ void __launch_bounds__(256) adam_tiles_kernel(
       float* pc = &c[j].x;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        pa[q] = b1 * pa[q] + omb1 * g[q];
-        pc[q] = b2 * pc[q] + omb2 * g[q] * g[q];
-        pw_[q] -= lr * ((pa[q] * inv_c1) / (sqrtf(pc[q] * inv_c2) + eps) + wd * pw_[q]);
+        adamw_elem(pw_[q], pa[q], pc[q], g[q], k, inv_c1, inv_c2);
       }
       pw[2 * j] = f2_to_bf2(w[j].x, w[j].y);
       pw[2 * j + 1] = f2_to_bf2(w[j].z, w[j].w);

@@ -37,6 +37,11 @@ __host__ __device__ inline int64_t blk_off(int64_t r, int64_t c, int64_t cols) {
          ((cc >> 2) & 3) * 128 + (rr & 31) * 4 + (cc & 3);
 }
 
+// AdamW hyper-parameters as the kernels use them (AdamConfig, optimizer.hpp:17-23; omb = 1 - beta)
+struct AdamK {
+  float lr, b1, b2, omb1, omb2, eps, wd;
+};
+
 struct GemmParams {
   int mode;  // GemmMode
   int epi;   // EpiKind
@@ -61,7 +66,7 @@ struct GemmParams {
   // the colsum_groups partial layout [row split][group][N]) -- skips a pass over dZ
   float* colsum_part = nullptr;
   // (EPI_ADAM: master/m1/m2 use the blk_off layout per group, group stride c_group_stride)
-  float lr = 0.f, b1 = 0.f, b2 = 0.f, omb1 = 0.f, omb2 = 0.f, eps = 0.f, wd = 0.f;
+  AdamK adam{};
 };
 
 struct GemmOperands {

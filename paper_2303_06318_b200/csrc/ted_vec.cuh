@@ -3,6 +3,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include "ted_internal.h"
+
 namespace ted {
 namespace {
 
@@ -38,6 +40,18 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+// AdamW on one element (optimizer.cpp:94-100): m = b1 m + (1-b1) g, v = b2 v + (1-b2) g^2,
+// p -= lr (m c1 / (sqrt(v c2) + eps) + wd p) with c1, c2 the bias corrections.  Every AdamW
+// kernel (the fused wgrad epilogue and the standalone ones) uses this one expression, so
+// fused and unfused steps agree bit for bit.  IEEE sqrt and division: the SFU-approximate
+// pair (sqrt.approx + rcp.approx, a third of the instructions) measured 3-4 % SLOWER in the
+// fused wgrad epilogue inside the power-capped step (tools/ab_lib.sh, same box).
+__device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g, const AdamK& k,
+                                           float c1, float c2) {
+  m = k.b1 * m + k.omb1 * g;
+  v = k.b2 * v + (k.omb2 * g) * g;
+  p -= k.lr * ((m * c1) / (sqrtf(v * c2) + k.eps) + k.wd * p);
 }
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
