@@ -63,8 +63,8 @@ typedef struct {
 
 typedef struct {
   int dtd;          /* duplicate token dropping */
-  int cac;          /* comm-aware checkpointing (not implemented: must be 0) */
-  int ckpt;         /* activation checkpointing (not implemented: must be 0) */
+  int cac;          /* comm-aware checkpointing: ted_model_* (a single ted_layer rejects it) */
+  int ckpt;         /* activation checkpointing: ted_model_* (a single ted_layer rejects it) */
   int track_tokens; /* keep per-layer placement verdicts */
   int corrupt_drop; /* fault injection: dispatch the wrong DTD chunk */
 } ted_flags;
@@ -131,6 +131,14 @@ int ted_adam_step(float* master_dev, float* m1_dev, float* m2_dev, uint16_t* par
                   const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
                   uint64_t* upcast_peak_bytes, void* stream);
 
+/* Placement verdict of the DTD round trip (moe.cpp:537-556) from a dispatch's row
+ * records (pos_send: row this rank sent, -1 = not sent; pos_home: home row, -1 = dropped):
+ * true iff the tokens sent are exactly the capacity-kept tokens of chunk slot_chunk of T
+ * equal chunks (slot_chunk < 0: of every chunk, no DTD).  verdict_dev[0] = the verdict,
+ * verdict_dev[1] &= it (device int32[2]). */
+int ted_placement_verdict(const int32_t* pos_send_dev, const int32_t* pos_home_dev, int64_t n,
+                          int T, int slot_chunk, int32_t* verdict_dev, void* stream);
+
 /* ---------------------------------------------------------------- MoE layer (MoeRank) */
 
 typedef struct ted_layer ted_layer;
@@ -152,6 +160,13 @@ int ted_nccl_unique_id(void* out128);
 int ted_layer_set_param(ted_layer* L, const char* name, const float* full_host);
 int ted_layer_get_param(ted_layer* L, const char* name, float* shard_host, int64_t* numel);
 int ted_layer_get_grad(ted_layer* L, const char* name, float* shard_host, int64_t* numel);
+/* ted_layer_step (and ted_model_step) run AdamW inside the expert wgrad GEMMs when the
+ * expert family is unsharded: the epilogue writes the updated parameters and, by default,
+ * not the bf16 w1/w2 gradients (2 B/parameter of HBM traffic saved).  After such a step
+ * ted_layer_get_grad of an expert w1/w2 fails with TED_ERR_RUNTIME.  keep = 1 makes the
+ * fused epilogue also store those gradients (the reference keeps every gradient readable
+ * after a step); a separate ted_layer_backward always stores them. */
+int ted_layer_keep_grads(ted_layer* L, int keep);
 /* Synthetic deterministic init on device (uniform [-scale, scale) with the reference
  * scales 1/sqrt(h), 1/sqrt(4h), 0.1); not bitwise the reference's mt19937_64 stream. */
 int ted_layer_init_params(ted_layer* L, uint64_t seed);
@@ -181,11 +196,13 @@ typedef struct {
   int64_t ag_bytes_fwd;      /* DTD all-gather payload (2 per fwd pass) */
   int64_t ar_bytes_fwd;      /* TP all-reduce payload */
   int64_t asm_rows;          /* expert-side rows (padded) */
-  int placement_ok;          /* DTD placement verdict (moe.cpp:537-556) */
+  int placement_ok;          /* DTD placement verdict of the last forward, computed on the
+                                device from the rows the dispatch selected (moe.cpp:537-556) */
   int64_t kept_per_expert[64]; /* local experts: rows processed */
   int64_t peer_bytes_fwd;    /* NVLink bytes this rank moves per forward (peer exchange:
                                 dispatch stores to other GPUs + pulls of TP partial rows) */
   int peer_exchange;         /* 1: NVLink peer-memory exchange, 0: NCCL send/recv */
+  int placement_ok_all;      /* verdict of every forward so far (MoeRank::placement_ok_) */
 } ted_layer_stats;
 int ted_layer_get_stats(ted_layer* L, ted_layer_stats* out);
 
@@ -228,6 +245,8 @@ int ted_model_set_param(ted_model* M, const char* name, const float* full);
 int ted_model_get_param(ted_model* M, const char* name, float* out, int64_t* numel);
 int ted_model_get_grad(ted_model* M, const char* name, float* out, int64_t* numel);
 int ted_model_init_params(ted_model* M, uint64_t seed);
+/* ted_layer_keep_grads for every MoE layer of the stack */
+int ted_model_keep_grads(ted_model* M, int keep);
 /* Trainer::step (moe.cpp:838-844): run_forward, run_backward, run_grad_sync,
  * run_optimizer_step */
 int ted_model_step(ted_model* M, const uint16_t* batch, void* stream);

@@ -101,7 +101,7 @@ class LayerStats(C.Structure):
                 ("ag_bytes_fwd", C.c_int64), ("ar_bytes_fwd", C.c_int64),
                 ("asm_rows", C.c_int64), ("placement_ok", C.c_int),
                 ("kept_per_expert", C.c_int64 * 64), ("peer_bytes_fwd", C.c_int64),
-                ("peer_exchange", C.c_int)]
+                ("peer_exchange", C.c_int), ("placement_ok_all", C.c_int)]
 
 
 def _sig(name, res, args):
@@ -128,6 +128,7 @@ _sig("ted_grouped_gemm", _i32, [_i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _
 _sig("ted_adam_step", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, C.POINTER(AdamC),
                              C.POINTER(TileC), C.POINTER(_u64), _vp])
 _sig("ted_nccl_unique_id", _i32, [C.c_char_p])
+_sig("ted_placement_verdict", _i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp])
 _sig("ted_layer_create", _i32, [C.POINTER(ModelCfg), C.POINTER(TopoCfg), C.POINTER(FlagsC),
                                 C.POINTER(AdamC), C.POINTER(TileC), _dbl, _i32, _i32,
                                 C.c_char_p, C.POINTER(_vp)])
@@ -136,6 +137,7 @@ _sig("ted_layer_set_param", _i32, [_vp, C.c_char_p, _vp])
 _sig("ted_layer_get_param", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
 _sig("ted_layer_get_grad", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
 _sig("ted_layer_init_params", _i32, [_vp, _u64])
+_sig("ted_layer_keep_grads", _i32, [_vp, _i32])
 _sig("ted_layer_forward", _i32, [_vp, _vp, _vp, _vp])
 _sig("ted_layer_backward", _i32, [_vp, _vp, _vp, _vp])
 _sig("ted_layer_optimizer_step", _i32, [_vp, _vp])
@@ -154,6 +156,7 @@ _sig("ted_model_set_param", _i32, [_vp, C.c_char_p, _vp])
 _sig("ted_model_get_param", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
 _sig("ted_model_get_grad", _i32, [_vp, C.c_char_p, _vp, C.POINTER(_i64)])
 _sig("ted_model_init_params", _i32, [_vp, _u64])
+_sig("ted_model_keep_grads", _i32, [_vp, _i32])
 _sig("ted_model_step", _i32, [_vp, _vp, _vp])
 _sig("ted_model_forward", _i32, [_vp, _vp, _vp])
 _sig("ted_model_backward", _i32, [_vp, _vp])
@@ -165,13 +168,13 @@ _sig("ted_model_memory", _i32, [_vp, C.POINTER(_i64)])
 EXPORTED = [
     "ted_default_configs", "ted_last_error", "ted_version", "ted_derive_config",
     "ted_shard_range", "ted_gate_forward", "ted_gate_route_logits", "ted_route",
-    "ted_gate_backward", "ted_grouped_gemm", "ted_adam_step", "ted_layer_create",
+    "ted_gate_backward", "ted_grouped_gemm", "ted_adam_step", "ted_placement_verdict", "ted_layer_create",
     "ted_layer_destroy", "ted_nccl_unique_id", "ted_layer_set_param", "ted_layer_get_param",
-    "ted_layer_get_grad", "ted_layer_init_params", "ted_layer_forward", "ted_layer_backward",
+    "ted_layer_get_grad", "ted_layer_keep_grads", "ted_layer_init_params", "ted_layer_forward", "ted_layer_backward",
     "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_get_stats",
     "ted_layer_get_routing", "ted_layer_timing", "ted_layer_timing_read", "ted_kernel_launches",
     "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
-    "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_step",
+    "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_keep_grads", "ted_model_step",
     "ted_model_forward", "ted_model_backward", "ted_model_optimizer_step", "ted_model_loss",
     "ted_model_output", "ted_model_memory"]
 
@@ -362,6 +365,13 @@ def adam_step(master, m1, m2, param, grad, begin, end, step, adam=None, tiles=No
     return peak.value
 
 
+def placement_verdict(pos_send, pos_home, T: int, slot_chunk: int, verdict, stream=None):
+    """DTD placement verdict (moe.cpp:537-556) on device int32 row records; verdict is a
+    device int32[2] ([0] this call, [1] &= it)."""
+    _check(_lib.ted_placement_verdict(_p(pos_send), _p(pos_home), pos_send.numel(), T,
+                                      slot_chunk, _p(verdict), _stream(stream)))
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(_lib.ted_nccl_unique_id(buf))
@@ -431,6 +441,11 @@ class MoeLayer:
 
     def init_params(self, seed: int = 0):
         _check(_lib.ted_layer_init_params(self._h, seed))
+
+    def keep_grads(self, keep: bool = True):
+        """step() fuses AdamW into the wgrad GEMMs; keep=True also stores the expert
+        w1/w2 gradients there (else get_grad of those fails after a fused step)."""
+        _check(_lib.ted_layer_keep_grads(self._h, int(keep)))
 
     def forward(self, a, y, stream=None):
         _check(_lib.ted_layer_forward(self._h, _p(a), _p(y), _stream(stream)))
@@ -556,6 +571,9 @@ class TedModel:
 
     def init_params(self, seed: int = 0):
         _check(_lib.ted_model_init_params(self._h, seed))
+
+    def keep_grads(self, keep: bool = True):
+        _check(_lib.ted_model_keep_grads(self._h, int(keep)))
 
     def step(self, batch, stream=None):
         _check(_lib.ted_model_step(self._h, _p(batch), _stream(stream)))

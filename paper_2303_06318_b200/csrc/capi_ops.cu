@@ -258,4 +258,15 @@ int ted_adam_step(float* master, float* m1, float* m2, uint16_t* param, const ui
   });
 }
 
+int ted_placement_verdict(const int32_t* pos_send, const int32_t* pos_home, int64_t n, int T,
+                          int slot_chunk, int32_t* verdict, void* stream) {
+  return guard([&] {
+    need(n >= 0 && T >= 1, "placement_verdict: bad sizes");
+    need(slot_chunk < T, "placement_verdict: slot chunk outside [0, T)");
+    device_ok();
+    cuda_ok(placement_verdict(pos_send, pos_home, n, T, slot_chunk, verdict, S(stream)),
+            "placement_verdict");
+  });
+}
+
 }  // extern "C"

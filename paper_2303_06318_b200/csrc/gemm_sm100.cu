@@ -81,7 +81,8 @@ struct Cfg {
   static constexpr int COL_SPAN = BN / (EPI_WARPS / 4);  // tile columns per epilogue warp
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
   static constexpr int STAGES = 4;
-  static constexpr size_t PER_WARP = EPI == EPI_ADAM ? P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
+  // AdamW: the parameter half block and (keep-gradients mode) the gradient half block
+  static constexpr size_t PER_WARP = EPI == EPI_ADAM ? 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -369,7 +370,8 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
       ptx::tc_fence_after();
       const uint32_t tb = tmem_base + acc * BN + (uint32_t(sp * 32) << 16) + cq * SPAN;
       float v[16];
-      uint32_t pw[8];
+      uint32_t pw[8], gw[8];
+      const bool keep_grad = p.adam_grad != nullptr;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const int cpf = c + RING - 1;  // chunk whose loads go out now
@@ -393,6 +395,11 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           // the unfused path stores the bf16-rounded gradient: same rounding here
           const float g = zero ? 0.f : __bfloat162float(__float2bfloat16(v[vb + q]));
           adamw_elem(mq[q], q1[q], q2[q], g, p.adam, c1, c2);
+          v[vb + q] = g;
+        }
+        if (keep_grad) {
+          gw[(c % 4) * 2] = pack_bf16(v[vb], v[vb + 1]);
+          gw[(c % 4) * 2 + 1] = pack_bf16(v[vb + 2], v[vb + 3]);
         }
         const int64_t o = cur + c * 128;
         st_state(p.adam_master + o, st[0], pol);
@@ -405,14 +412,23 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           // j ^ ((r>>2)&1)); the previous half's store must have read pblk
           if (lane == 0) ptx::bulk_wait_read0();
           __syncwarp();
+          const int sw = lane * 32, s0 = ((lane >> 2) & 1) << 4;
 #pragma unroll
           for (int j = 0; j < 2; ++j)
-            *reinterpret_cast<uint4*>(pblk + lane * 32 + ((j ^ ((lane >> 2) & 1)) << 4)) =
+            *reinterpret_cast<uint4*>(pblk + sw + (s0 ^ (j << 4))) =
                 make_uint4(pw[4 * j], pw[4 * j + 1], pw[4 * j + 2], pw[4 * j + 3]);
+          if (keep_grad) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              *reinterpret_cast<uint4*>(pblk + P16_BLOCK_BYTES + sw + (s0 ^ (j << 4))) =
+                  make_uint4(gw[4 * j], gw[4 * j + 1], gw[4 * j + 2], gw[4 * j + 3]);
+          }
           ptx::fence_async_smem();
           __syncwarp();
           if (lane == 0) {
             ptx::tma_store_3d(&tmC, pblk, colw + 4 * (c - 3), row0, ti.g);
+            if (keep_grad)
+              ptx::tma_store_3d(&tmAux, pblk + P16_BLOCK_BYTES, colw + 4 * (c - 3), row0, ti.g);
             ptx::bulk_commit();
           }
         }
@@ -665,6 +681,10 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
       const uint64_t gs = (p.c_group_stride ? p.c_group_stride : int64_t(p.M) * p.ldc) * 2;
       ok = ok && make_map(&mc, p.C, p.N, p.M, p.groups, p.ldc * 2, gs, 16, 32,
                           CU_TENSOR_MAP_SWIZZLE_32B);
+      mx = mc;
+      if (p.adam_grad)  // the gradient, laid out like the parameter
+        ok = ok && make_map(&mx, p.adam_grad, p.N, p.M, p.groups, p.ldc * 2, gs, 16, 32,
+                            CU_TENSOR_MAP_SWIZZLE_32B);
     }
   }
   f0 = f1 = f2 = mc;  // (state blocks move as 1-D bulk copies; the maps are unused)

@@ -89,6 +89,7 @@ struct ted_layer {
       send_base, home_base, seg_off;
   int* seg_valid_view = nullptr;  // [Eloc] view inside seg_off's allocation
   DevBuf<double> loss;
+  DevBuf<int> verdict;  // placement verdict: [0] last forward, [1] sticky (moe.cpp:537-556)
   HostBuf<int> h_kc_all, h_seg;
   // activations
   DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home, dx_asm;
@@ -109,6 +110,10 @@ struct ted_layer {
   // so the expert family's AdamW may run inside the wgrad epilogues (exp_done_fused)
   bool step_follows = false, exp_done_fused = false;
   bool fuse_ok = false;  // expert family unsharded, no DP sync: AdamW may fuse into wgrad
+  // the fused epilogues write the updated parameters; the bf16 expert weight gradients are
+  // stored too only with keep_grads (ted_layer_keep_grads), else get_grad of w1/w2 fails
+  // until the next unfused backward (grads_stale)
+  bool keep_grads = false, grads_stale = false;
 
   // CUDA graph of the whole single-rank training step (ted_layer_step): the step has no
   // host synchronisation, so it is captured once and replayed (removes ~45 launches and
@@ -324,6 +329,12 @@ void zero_asm_pads(ted_layer* L, bf16* buf, cudaStream_t s) {
 }
 
 
+// corrupt_drop on the peer exchange: my rows go to my slot's blocks, sized for my slot's
+// chunk, not for the chunk the fault hook dispatches
+const int* peer_clamp(const ted_layer* L) {
+  return (L->dtd && L->flags.corrupt_drop) ? L->kc.p + size_t(L->t) * L->E : nullptr;
+}
+
 RowSrc pull_src(ted_layer* L, int which) {
   RowSrc r;
   r.pos_home = L->pos_home.p;
@@ -433,6 +444,10 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
                       L->chunk_prefix.p, L->send_base.p, L->home_base.p, L->slot.p,
                       L->pos_send.p, L->pos_home.p, xs, s),
         "dispatch_rows");
+  // the DTD round trip's placement verdict, from the rows the dispatch actually selected
+  check(placement_verdict(L->pos_send.p, L->pos_home.p, L->n, L->Tc, L->dtd ? L->t : -1,
+                          L->verdict.p, s),
+        "placement_verdict");
 
   int64_t rows = 0;  // rows spanned by the assembled buffer
   if (L->local) {
@@ -461,6 +476,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     pd.Tp = L->T;
     pd.my_t = L->t;
     pd.all_replicas = L->dtd ? 1 : 0;
+    pd.clamp_rows = peer_clamp(L);
     check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
           "scatter_rows_peer");
     L->mark("barrier", s);
@@ -520,6 +536,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
       pd.Tp = L->T;
       pd.my_t = L->t;
       pd.all_replicas = L->dtd ? 1 : 0;
+    pd.clamp_rows = peer_clamp(L);
       check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
             "scatter_rows_peer");
       L->mark("barrier", s);
@@ -652,6 +669,7 @@ void bias_adam(ted_layer* L, int64_t off, int64_t len, cudaStream_t s) {
 void set_adam_epilogue(ted_layer* L, GemmParams& g, int64_t off) {
   Family& F = L->fam_exp;
   g.epi = EPI_ADAM;
+  g.adam_grad = L->keep_grads ? g.C : nullptr;  // g.C = the gradient slot of this weight
   g.C = F.param.p + off;
   g.adam_master = F.master.p + off;
   g.adam_m1 = F.m1.p + off;
@@ -680,6 +698,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     pd.Tp = L->T;
     pd.my_t = L->t;
     pd.all_replicas = L->dtd ? 1 : 0;
+    pd.clamp_rows = peer_clamp(L);
     check(combine_backward_peer(L->fhome.p, L->pos_home.p, L->pos_send.p, L->prob.p, L->probs.p,
                                 L->expert.p, L->n, h, E, dy, L->last_y, float(1.0 / nglob), pd,
                                 L->dlogits.p, s),
@@ -760,6 +779,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   // the optimizer follows this backward and the expert family needs no data-parallel sync:
   // AdamW runs inside the wgrad epilogues (W2 is no longer read: dgrad2 ran before)
   const bool fuse_adam = L->step_follows && L->fuse_ok;
+  L->grads_stale = fuse_adam && !L->keep_grads;
   if (fuse_adam) {
     family_begin(L, L->fam_exp, s);
     set_adam_epilogue(L, g, L->off_w2);
@@ -1089,7 +1109,7 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
     NC(ncclCommSplit(L->world_c, L->t, L->ep + L->P * L->d, &L->nonexpdp_c, nullptr));
     NC(ncclCommSplit(L->world_c, L->d, L->t + L->T * L->ep, &L->plane_c, nullptr));
     const char* ex = std::getenv("TED_EXCHANGE");
-    L->direct = !L->local && !flags->corrupt_drop && !(ex && std::strcmp(ex, "nccl") == 0);
+    L->direct = !L->local && !(ex && std::strcmp(ex, "nccl") == 0);
     L->plane_rank = L->t + L->T * L->ep;
     L->plane_size = L->T * L->P;
   }
@@ -1115,6 +1135,11 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->loss_part.alloc(L->nblk + 1);
   L->loss.alloc(1);
   L->loss.zero();
+  L->verdict.alloc(2);
+  {
+    const int one[2] = {1, 1};
+    CU(cudaMemcpy(L->verdict.p, one, sizeof(one), cudaMemcpyHostToDevice));
+  }
   L->expert.alloc(n);
   L->slot.alloc(n);
   L->pos_send.alloc(n);
@@ -1313,6 +1338,7 @@ int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
     std::vector<uint16_t> b(shard.size());
     for (size_t i = 0; i < b.size(); ++i) b[i] = f2bf(shard[i]);
     Family& F = *pl.fam;
+    CU(cudaDeviceSynchronize());  // a step in flight on a non-blocking stream may still write
     CU(cudaMemcpy(F.param.p + pl.off, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
     const int64_t lo = std::max(pl.off, F.begin), hi = std::min(pl.off + int64_t(b.size()), F.end);
     if (state_blocked(L, pl)) {  // unsharded: the whole tensor, state in the blk_off layout
@@ -1339,6 +1365,11 @@ static int get_tensor(ted_layer* L, const char* name, float* out, int64_t* numel
     const int64_t cnt = pl.rows * pl.cols;
     if (numel) *numel = cnt;
     if (!out) return;
+    if (grad && L->grads_stale && pl.fam == &L->fam_exp && pl.rows > 1)
+      throw RuntimeError(std::string("gradient of ") + name +
+                         " was consumed by the AdamW fused into the wgrad GEMM of the last "
+                         "step and not stored (ted_layer_keep_grads(L, 1) stores it; a "
+                         "separate backward() materialises it)");
     std::vector<uint16_t> b{};
     b.resize(size_t(cnt));
     CU(cudaDeviceSynchronize());
@@ -1358,6 +1389,7 @@ int ted_layer_get_grad(ted_layer* L, const char* name, float* out, int64_t* nume
 int ted_layer_init_params(ted_layer* L, uint64_t seed) {
   return guard([&] {
     require(L != nullptr, "null layer");
+    CU(cudaDeviceSynchronize());  // after any step still in flight
     for (const std::string& nm : local_param_names(L)) {
       ParamLoc pl;
       lookup(L, nm, pl);
@@ -1501,6 +1533,16 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
   });
 }
 
+int ted_layer_keep_grads(ted_layer* L, int keep) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    if (L->keep_grads == (keep != 0)) return;
+    CU(cudaDeviceSynchronize());
+    L->keep_grads = keep != 0;
+    for (auto& g : L->graphs) graph_reset(g);  // the captured epilogues change
+  });
+}
+
 int ted_layer_loss(ted_layer* L, double* loss, void* stream) {
   return guard([&] {
     require(L && loss, "null argument");
@@ -1568,7 +1610,10 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
         o->ar_bytes_fwd = 0;  // folded into the pulls
       }
     }
-    o->placement_ok = (L->dtd && L->flags.corrupt_drop) ? 0 : 1;
+    int vd[2] = {1, 1};
+    CU(cudaMemcpy(vd, L->verdict.p, sizeof(vd), cudaMemcpyDeviceToHost));
+    o->placement_ok = vd[0];
+    o->placement_ok_all = vd[1];
   });
 }
 

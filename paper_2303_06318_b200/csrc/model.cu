@@ -654,7 +654,8 @@ int ted_model_set_param(ted_model* M, const char* name, const float* full) {
         if (e / (M->E / M->P) != M->ep) return;
       }
       const int rc = ted_layer_set_param(M->moe[size_t(layer)], moe_name(name).c_str(), full);
-      if (rc != TED_OK) throw ConfigError(last_error());
+      if (rc == TED_ERR_CONFIG) throw ConfigError(last_error());
+      if (rc != TED_OK) throw RuntimeError(last_error());
       return;
     }
     DenseLoc dl;
@@ -691,7 +692,8 @@ static int model_get(ted_model* M, const char* name, float* out, int64_t* numel,
       const std::string nm = moe_name(name);
       const int rc = grad ? ted_layer_get_grad(M->moe[size_t(layer)], nm.c_str(), out, numel)
                           : ted_layer_get_param(M->moe[size_t(layer)], nm.c_str(), out, numel);
-      if (rc != TED_OK) throw ConfigError(last_error());
+      if (rc == TED_ERR_CONFIG) throw ConfigError(last_error());
+      if (rc != TED_OK) throw RuntimeError(last_error());
       return;
     }
     DenseLoc dl;
@@ -712,6 +714,14 @@ int ted_model_get_param(ted_model* M, const char* name, float* out, int64_t* num
 }
 int ted_model_get_grad(ted_model* M, const char* name, float* out, int64_t* numel) {
   return model_get(M, name, out, numel, true);
+}
+
+int ted_model_keep_grads(ted_model* M, int keep) {
+  return guard([&] {
+    require(M != nullptr, "null model");
+    for (ted_layer* L : M->moe)
+      if (L && ted_layer_keep_grads(L, keep) != TED_OK) throw RuntimeError(last_error());
+  });
 }
 
 int ted_model_init_params(ted_model* M, uint64_t seed) {

@@ -1473,6 +1473,38 @@ cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cuda
   return cudaGetLastError();
 }
 
+// Placement verdict of the DTD round trip (moe.cpp:537-556), computed from what the
+// dispatch actually did: the reference records the kept chunk and checks that it is this
+// rank's slot [t*n/T, (t+1)*n/T) -- here every token this rank dispatched (pos_send >= 0)
+// must lie in chunk `slot_chunk` and every capacity-kept token of that chunk must have been
+// dispatched (without DTD: slot_chunk = -1, every kept token).  verdict[0] = this
+// forward's verdict, verdict[1] &= it (the rank's sticky placement_ok_, moe.cpp:553).
+static __global__ void __launch_bounds__(1024) placement_verdict_kernel(
+    const int* __restrict__ pos_send, const int* __restrict__ pos_home, int64_t n, int T,
+    int slot_chunk, int* __restrict__ verdict) {
+  const int64_t chunk = T > 1 ? n / T : n;
+  int ok = 1;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    int c = T > 1 ? int(k / chunk) : 0;
+    if (c >= T) c = T - 1;
+    const bool expect = pos_home[k] >= 0 && (slot_chunk < 0 || c == slot_chunk);
+    if ((pos_send[k] >= 0) != expect) ok = 0;
+  }
+  ok = __syncthreads_and(ok);
+  if (threadIdx.x == 0) {
+    verdict[0] = ok;
+    verdict[1] &= ok;
+  }
+}
+
+cudaError_t placement_verdict(const int* pos_send, const int* pos_home, int64_t n, int T,
+                              int slot_chunk, int* verdict, cudaStream_t s) {
+  if (n < 0 || T < 1) return cudaErrorInvalidValue;
+  placement_verdict_kernel<<<1, 1024, 0, s>>>(pos_send, pos_home, n, T, slot_chunk, verdict);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,
                            cudaStream_t s) {
   if (n == 0) return cudaSuccess;

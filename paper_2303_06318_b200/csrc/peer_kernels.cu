@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kThreads) scatter_peer_kernel(const bf16* __re
     if (ps < 0) continue;
     const int e = expert[k];
     const int64_t r = int64_t(ps) - D.send_base[e];
+    if (D.clamp_rows && r >= D.clamp_rows[e]) continue;
     const float sc = scale ? scale[k] : 1.f;
     const uint4* src = reinterpret_cast<const uint4*>(a + k * h);
     const int t0 = D.all_replicas ? 0 : D.my_t;
@@ -189,8 +190,9 @@ __global__ void __launch_bounds__(kThreads) combine_bwd_peer_kernel(
     const uint4* dsrc = reinterpret_cast<const uint4*>(dsrc_base + k * h);
     const uint4* fsrc = reinterpret_cast<const uint4*>(fhome + k * h);
     const int64_t r = ps >= 0 ? int64_t(ps) - D.send_base[e] : 0;
+    const bool send = ps >= 0 && !(D.clamp_rows && r >= D.clamp_rows[e]);
     const int t0 = D.all_replicas ? 0 : D.my_t;
-    const int t1 = ps < 0 ? t0 : (D.all_replicas ? D.Tp : D.my_t + 1);
+    const int t1 = !send ? t0 : (D.all_replicas ? D.Tp : D.my_t + 1);
     float dot = 0.f;
     for (int base = lane; base < vec; base += 32 * 4) {
       uint4 dv[4], fv[4];

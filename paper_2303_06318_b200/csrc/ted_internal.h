@@ -62,6 +62,7 @@ struct GemmParams {
   float* adam_m1 = nullptr;
   float* adam_m2 = nullptr;
   const float* adam_coef = nullptr;  // device {1/(1-b1^t), 1/(1-b2^t)}
+  bf16* adam_grad = nullptr;  // non-null: also store the bf16 gradient tile (laid out like C)
   // EPI_DGELU (ROWS mode): also write the 32-row column-sum partials of dZ (bias gradient,
   // the colsum_groups partial layout [row split][group][N]) -- skips a pass over dZ
   float* colsum_part = nullptr;
@@ -163,6 +164,10 @@ struct PeerDst {
   const long long* disp_base = nullptr;       // [E]
   const int* send_base = nullptr;             // [E]
   int Eloc = 1, Tp = 1, my_t = 0, all_replicas = 0;
+  // fault injection (corrupt_drop) on the peer exchange: this rank dispatches another
+  // chunk than its slot; rows past the slot's reserved block (clamp_rows[e]) are not
+  // written, so the wrong chunk lands misplaced like the reference's instead of overrunning
+  const int* clamp_rows = nullptr;
 };
 cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* expert, int64_t n,
                               int h, const PeerDst& dst, const float* scale, bool scale_by_prob,
@@ -201,6 +206,10 @@ size_t colsum_part_floats(int w, int G, int max_rows_per_group);
 cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s);
 cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,
                            cudaStream_t s);
+// DTD placement verdict (moe.cpp:537-556) from the dispatch's pos_send / pos_home:
+// verdict[0] = this forward, verdict[1] &= (sticky).  slot_chunk < 0: no DTD.
+cudaError_t placement_verdict(const int* pos_send, const int* pos_home, int64_t n, int T,
+                              int slot_chunk, int* verdict, cudaStream_t s);
 cudaError_t dlogits_from_dchosen(const float* probs, const int* expert, const float* dchosen,
                                  int64_t n, int E, float* dlogits, cudaStream_t s);
 

@@ -1,0 +1,252 @@
+"""Parity at the benched configuration: BASELINE.json configs[2] (C3) on one GPU -- d=4096,
+ffn=16384, 16 experts top-1, 32768 tokens, capacity factor 1.25 -- the exact layer
+`bench.py` times.
+
+The fp64 oracle cannot run the full layer in a test (about 3 TFLOP per pass in numpy), so
+the reference semantics (SerialModel::forward_layer / backward_layer, moe.cpp:989-1064;
+serial equivalence, test_moe.cpp:288-330) are checked where they are cheap and exact:
+  * routing of all 32768 tokens bit-exact against the oracle's argmax/softmax on the GPU's
+    fp32 logits, capacity slots and drops bit-exact (the oracle's capacity restatement);
+  * logits of sampled tokens against fp64 a.Wg on the same bf16 inputs;
+  * y of sampled tokens of two experts against the fp64 expert FFN;
+  * the backward of two whole experts: dW1 / db1 on sampled columns, dW2 on sampled rows,
+    db2 complete, all over every token the expert received; da of sampled tokens; dWg
+    complete.  The upstream gradient is the reference's synthetic objective dy = y / N
+    (moe.cpp:379-391) on the GPU's own y, which is itself checked on samples;
+  * the full-size grouped GEMMs (fwd, dgrad, wgrad shapes) against torch fp32;
+  * the fused AdamW-in-wgrad step against the unfused optimizer path, and the kept
+    gradients of the fused step against the unfused backward, bit for bit.
+Tolerances as tests/test_gpu_layer.py: rel-L2 <= 2e-2 for bf16-stored activations and
+gradients, logits 1e-5, fused vs unfused parameters 1e-3 (the same bf16-rounded gradient
+and the same update expression: in practice identical)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from tests._util import from_dev, rel_l2, to_dev_bf16  # noqa: E402
+
+TOL = 2e-2
+N_TOK, H, E, CF = 32768, 4096, 16, 1.25
+F = 4 * H
+
+
+def _gelu(x):
+    return 0.5 * x * (1.0 + np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def _gelu_grad(x):
+    t = np.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+
+
+def _layer(seed=1234):
+    import paper_2303_06318_b200 as ted
+    L = ted.MoeLayer(ted.MoeModelConfig(1, H, E, N_TOK, 0), ted.TedConfig(), capacity_factor=CF)
+    L.init_params(seed)
+    return L
+
+
+def _tokens(seed=0):
+    rng = np.random.default_rng(seed)
+    a = O.bf16_round(rng.standard_normal((N_TOK, H)).astype(np.float32))
+    return a
+
+
+@pytest.fixture(scope="module")
+def c3_run():
+    """One forward + backward of the C3 layer (no optimizer step: parameters stay put)."""
+    L = _layer()
+    a_np = _tokens()
+    a = to_dev_bf16(a_np)
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    L.forward(a, y)
+    L.backward(None, da)
+    torch.cuda.synchronize()
+    out = {"L": L, "a": a_np, "y": from_dev(y), "da": from_dev(da), "r": L.routing(),
+           "stats": L.stats(), "loss": L.loss()}
+    yield out
+    L.close()
+
+
+def test_c3_routing_bit_exact(c3_run):
+    r = c3_run["r"]
+    oe, oc, op = O.gate_route_logits(r["logits"].astype(np.float64))
+    np.testing.assert_array_equal(r["expert"], oe)
+    slot, keep, _ = O.route_capacity(r["expert"], E, O.capacity(CF, N_TOK, E))
+    np.testing.assert_array_equal(r["slot"], slot)
+    np.testing.assert_array_equal(r["pos_home"] >= 0, keep.astype(bool))
+    assert c3_run["stats"]["dropped"] == int((keep == 0).sum())
+    # chosen / softmax probabilities on the same logits
+    assert rel_l2(r["prob"], oc) < 1e-6
+    assert rel_l2(r["probs"], op) < 1e-6
+
+
+def test_c3_logits_and_loss(c3_run):
+    L, a, r = c3_run["L"], c3_run["a"], c3_run["r"]
+    wg = L.get_param("layer0.gate.w").reshape(H, E).astype(np.float64)
+    idx = np.random.default_rng(1).choice(N_TOK, 256, replace=False)
+    ref = a[idx].astype(np.float64) @ wg
+    assert rel_l2(r["logits"][idx], ref) < 1e-5
+    # loss = sum(y^2) / (2N) (moe.cpp:379-381) over the layer's own bf16 y
+    y = c3_run["y"]
+    assert abs(c3_run["loss"] - float((y * y).sum()) / (2 * N_TOK)) <= 1e-3 * c3_run["loss"]
+
+
+def _experts_to_check(r):
+    cnt = np.bincount(r["expert"], minlength=E)
+    return [int(np.argmax(cnt)), int(np.argmin(cnt))]  # most and least loaded
+
+
+def test_c3_forward_and_backward_two_experts(c3_run):
+    L, a, r, y, da = c3_run["L"], c3_run["a"], c3_run["r"], c3_run["y"], c3_run["da"]
+    rng = np.random.default_rng(2)
+    keep = r["pos_home"] >= 0
+    wg = L.get_param("layer0.gate.w").reshape(H, E).astype(np.float64)
+    dy = y / N_TOK  # synthetic objective on the GPU's y (moe.cpp:390-391)
+    prob = r["prob"].astype(np.float64)
+    probs = r["probs"].astype(np.float64)
+    for e in _experts_to_check(r):
+        w1 = L.get_param(f"layer0.expert{e}.w1").reshape(H, F)
+        b1 = L.get_param(f"layer0.expert{e}.b1").astype(np.float64)
+        w2 = L.get_param(f"layer0.expert{e}.w2").reshape(F, H)
+        b2 = L.get_param(f"layer0.expert{e}.b2").astype(np.float64)
+        rows = np.nonzero((r["expert"] == e) & keep)[0]  # kept tokens of expert e
+        assert len(rows) > 0
+        X = a[rows].astype(np.float64)
+        # ---- forward on sampled tokens of this expert
+        smp = rng.choice(len(rows), min(24, len(rows)), replace=False)
+        Zs = X[smp] @ w1.astype(np.float64) + b1
+        fs = _gelu(Zs) @ w2.astype(np.float64) + b2
+        assert rel_l2(y[rows[smp]], prob[rows[smp], None] * fs) < TOL
+        # ---- backward over every token of the expert
+        dfe = prob[rows, None] * dy[rows]                      # combine backward (moe.cpp:587-597)
+        J = np.sort(rng.choice(F, 8, replace=False))           # sampled ffn columns
+        ZJ = X @ w1[:, J].astype(np.float64) + b1[J]
+        dZJ = (dfe @ w2[J].astype(np.float64).T) * _gelu_grad(ZJ)
+        g_w1 = L.get_grad(f"layer0.expert{e}.w1").reshape(H, F)
+        assert rel_l2(g_w1[:, J], X.T @ dZJ) < TOL             # dW1 = X^T dZ (columns J)
+        g_b1 = L.get_grad(f"layer0.expert{e}.b1")
+        assert rel_l2(g_b1[J], dZJ.sum(0)) < TOL
+        g_w2 = L.get_grad(f"layer0.expert{e}.w2").reshape(F, H)
+        assert rel_l2(g_w2[J], _gelu(ZJ).T @ dfe) < TOL        # dW2 = H^T dFe (rows J)
+        assert rel_l2(L.get_grad(f"layer0.expert{e}.b2"), dfe.sum(0)) < TOL
+        # da of sampled tokens: dX (through the whole expert) + the gate's input gradient
+        dZs = (dfe[smp] @ w2.astype(np.float64).T) * _gelu_grad(Zs)
+        dxs = dZs @ w1.astype(np.float64).T
+        dch = (fs * dy[rows[smp]]).sum(1)                      # dchosen = <f, dy>
+        ks = rows[smp]
+        onehot = np.eye(E)[e]
+        dl = dch[:, None] * prob[ks, None] * (onehot[None, :] - probs[ks])
+        assert rel_l2(da[ks], dxs + dl @ wg.T) < TOL
+        del w1, w2, g_w1, g_w2
+    # dWg = a^T dlogits over all tokens (moe.cpp:205); f = y / p on kept tokens
+    f_all = np.where(keep[:, None], y / np.maximum(prob, 1e-30)[:, None], 0.0)
+    dch = (f_all * dy).sum(1)
+    onehot = np.eye(E)[r["expert"]]
+    dl = dch[:, None] * prob[:, None] * (onehot - probs)
+    dwg = a.astype(np.float64).T @ dl
+    assert rel_l2(L.get_grad("layer0.gate.w").reshape(H, E), dwg) < TOL
+
+
+def _segs(rows):
+    off = [0]
+    for r in rows:
+        off.append(off[-1] + r)
+    return torch.tensor(off, dtype=torch.int32, device="cuda")
+
+
+def _rel_t(a, b):
+    a, b = a.double().flatten(), b.double().flatten()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+# expert segments as the C3 routing pads them (multiples of 128 around 32768*1.0/16 = 2048)
+C3_ROWS = [2048 + 128 * ((7 * g) % 5 - 2) for g in range(E)]
+
+
+def test_c3_gemm_fwd_bias_gelu_full_shape():
+    import paper_2303_06318_b200 as ted
+    torch.manual_seed(0)
+    R = sum(C3_ROWS)
+    A = torch.randn(R, H, device="cuda").bfloat16()
+    B = (torch.randn(E, H, F, device="cuda") / H ** 0.5).bfloat16()
+    bias = torch.randn(E, F, device="cuda").bfloat16()
+    Z = torch.empty(R, F, device="cuda", dtype=torch.bfloat16)
+    Hh = torch.empty_like(Z)
+    seg = _segs(C3_ROWS)
+    ted.grouped_gemm(ted.GEMM_ROWS, ted.EPI_BIAS_GELU, E, 0, F, H, seg, R, A, H, False, B, F,
+                     H * F, True, Z, F, bias=bias, bias_group_stride=F, aux=Hh, ld_aux=F)
+    torch.cuda.synchronize()
+    off = seg.tolist()
+    for g in (0, 7, E - 1):
+        ref = A[off[g]:off[g + 1]].float() @ B[g].float() + bias[g].float()
+        assert _rel_t(Z[off[g]:off[g + 1]].float(), ref) < 1e-2
+        t = torch.tanh(0.7978845608028654 * (ref + 0.044715 * ref ** 3))
+        assert _rel_t(Hh[off[g]:off[g + 1]].float(), 0.5 * ref * (1 + t)) < 1e-2
+
+
+def test_c3_gemm_dgrad_full_shape():
+    import paper_2303_06318_b200 as ted
+    torch.manual_seed(1)
+    R = sum(C3_ROWS)
+    A = torch.randn(R, F, device="cuda").bfloat16()                 # dZ
+    Bt = (torch.randn(E, H, F, device="cuda") / F ** 0.5).bfloat16()  # W1 as [N=h][K=f]
+    C = torch.empty(R, H, device="cuda", dtype=torch.bfloat16)
+    seg = _segs(C3_ROWS)
+    ted.grouped_gemm(ted.GEMM_ROWS, ted.EPI_STORE, E, 0, H, F, seg, R, A, F, False, Bt, F, H * F,
+                     False, C, H)
+    torch.cuda.synchronize()
+    off = seg.tolist()
+    for g in (0, 9, E - 1):
+        ref = A[off[g]:off[g + 1]].float() @ Bt[g].float().T
+        assert _rel_t(C[off[g]:off[g + 1]].float(), ref) < 1e-2
+
+
+def test_c3_gemm_wgrad_full_shape():
+    import paper_2303_06318_b200 as ted
+    torch.manual_seed(2)
+    R = sum(C3_ROWS)
+    X = torch.randn(R, H, device="cuda").bfloat16()
+    dZ = torch.randn(R, F, device="cuda").bfloat16()
+    C = torch.empty(E, H, F, device="cuda", dtype=torch.bfloat16)
+    seg = _segs(C3_ROWS)
+    ted.grouped_gemm(ted.GEMM_KDIM, ted.EPI_STORE, E, H, F, 0, seg, R, X, H, True, dZ, F, 0, True,
+                     C, F, c_group_stride=H * F)
+    torch.cuda.synchronize()
+    off = seg.tolist()
+    for g in (0, 5, E - 1):
+        ref = X[off[g]:off[g + 1]].float().T @ dZ[off[g]:off[g + 1]].float()
+        assert _rel_t(C[g].float(), ref) < 1e-2
+
+
+def test_c3_fused_adam_step_matches_unfused_and_keeps_gradients():
+    """ted_layer_step (AdamW inside the wgrad epilogues, CUDA graph) vs forward + backward
+    + optimizer_step (standalone AdamW kernels) at C3, two steps; with keep_grads the fused
+    step's stored gradients equal the unfused backward's bit for bit."""
+    La, Lb = _layer(77), _layer(77)
+    La.keep_grads(True)
+    a = to_dev_bf16(_tokens(5))
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    for it in range(2):
+        La.step(a, y, da)
+        Lb.forward(a, y)
+        Lb.backward(None, da)
+        torch.cuda.synchronize()
+        if it == 0:
+            for k in ("w1", "w2"):
+                ga = La.get_grad(f"layer0.expert3.{k}")
+                gb = Lb.get_grad(f"layer0.expert3.{k}")
+                np.testing.assert_array_equal(ga, gb)
+        Lb.optimizer_step()
+    torch.cuda.synchronize()
+    for e in (0, 3, E - 1):
+        for k in ("w1", "b1", "w2", "b2"):
+            pa = La.get_param(f"layer0.expert{e}.{k}")
+            pb = Lb.get_param(f"layer0.expert{e}.{k}")
+            assert rel_l2(pa, pb) < 1e-3, (e, k)
+    assert rel_l2(La.get_param("layer0.gate.w"), Lb.get_param("layer0.gate.w")) < 1e-3
+    La.close()
+    Lb.close()

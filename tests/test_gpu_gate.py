@@ -116,3 +116,36 @@ def test_gate_backward_matches_oracle():
                             expert.cpu().numpy(), dchosen.astype(np.float64), n, h, E, dwo, dio)
     assert rel_l2(dwg.float().cpu().numpy(), dwo) < 1e-2
     assert rel_l2(dinput.float().cpu().numpy(), dio) < 1e-2
+
+
+def test_placement_verdict_kernel():
+    """The DTD placement verdict (moe.cpp:537-556) computed on the device from a dispatch's
+    row records: the right chunk passes, the chunk corrupt_drop sends (test_moe.cpp:388-414)
+    fails, and the sticky verdict stays failed."""
+    import paper_2303_06318_b200 as ted
+    rng = np.random.default_rng(4)
+    n, T = 1024, 2
+    chunk = n // T
+    home = np.where(rng.random(n) < 0.8, np.arange(n), -1).astype(np.int32)  # 20 % dropped
+
+    def sent_by(c):
+        s = np.full(n, -1, np.int32)
+        idx = [k for k in range(c * chunk, (c + 1) * chunk) if home[k] >= 0]
+        s[idx] = np.arange(len(idx), dtype=np.int32)
+        return s
+
+    ph = torch.from_numpy(home).cuda()
+    v = torch.ones(2, dtype=torch.int32, device="cuda")
+    ted.placement_verdict(torch.from_numpy(sent_by(1)).cuda(), ph, T, 1, v)
+    assert v.tolist() == [1, 1]
+    ted.placement_verdict(torch.from_numpy(sent_by(0)).cuda(), ph, T, 1, v)  # wrong chunk
+    assert v.tolist() == [0, 0]
+    ted.placement_verdict(torch.from_numpy(sent_by(1)).cuda(), ph, T, 1, v)
+    assert v.tolist() == [1, 0]  # this forward fine, the rank's record stays failed
+    all_kept = np.where(home >= 0, home, -1).astype(np.int32)  # no DTD: every kept token
+    ted.placement_verdict(torch.from_numpy(all_kept).cuda(), ph, 1, -1, v)
+    assert v[0].item() == 1
+    miss = all_kept.copy()
+    miss[np.nonzero(home >= 0)[0][5]] = -1  # a kept token that was never sent
+    ted.placement_verdict(torch.from_numpy(miss).cuda(), ph, 1, -1, v)
+    assert v[0].item() == 0

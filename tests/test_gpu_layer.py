@@ -168,3 +168,34 @@ def test_c_host_program_trains_the_layer(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
     losses = [float(line.split()[-1]) for line in r.stdout.splitlines() if line.startswith("step")]
     assert len(losses) == 3 and all(np.isfinite(losses)) and losses[-1] < losses[0], r.stdout
+
+
+def test_gradients_after_fused_step():
+    """After ted_layer_step the expert w1/w2 gradients were consumed by the AdamW fused into
+    the wgrad epilogues: get_grad fails loudly instead of returning stale values; with
+    keep_grads they are stored and equal the unfused backward's; biases and the gate are
+    always readable."""
+    import paper_2303_06318_b200 as ted
+    n, h, E = 1024, 256, 4
+    La, inp = _make(n, h, E, 1.25, 5)
+    Lb, _ = _make(n, h, E, 1.25, 5)
+    a = to_dev_bf16(inp["a"])
+    y, da = torch.empty_like(a), torch.empty_like(a)
+    La.step(a, y, da)
+    torch.cuda.synchronize()
+    with pytest.raises(ted.TedRuntimeError):
+        La.get_grad("layer0.expert0.w1")
+    assert np.isfinite(La.get_grad("layer0.expert0.b1")).all()
+    La.close()
+    La, _ = _make(n, h, E, 1.25, 5)
+    La.keep_grads(True)
+    La.step(a, y, da)
+    Lb.forward(a, y)
+    Lb.backward(None, da)
+    torch.cuda.synchronize()
+    for e in range(E):
+        for k in ("w1", "w2", "b1", "b2"):
+            np.testing.assert_array_equal(La.get_grad(f"layer0.expert{e}.{k}"),
+                                          Lb.get_grad(f"layer0.expert{e}.{k}"))
+    La.close()
+    Lb.close()

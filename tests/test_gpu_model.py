@@ -45,6 +45,13 @@ def test_stack_parameters_round_trip_and_update():
     M.step(batch)
     assert not np.array_equal(back, M.get_param("layer1.ffn.w1").reshape(256, 1024))
     assert np.abs(M.get_grad("layer0.attn.w2")).max() > 0
+    # the step fused AdamW into the expert wgrad GEMMs: those gradients are not stored
+    # unless asked for (ted_model_keep_grads); biases stay readable
+    with pytest.raises(ted.TedRuntimeError):
+        M.get_grad("layer0.expert1.w1")
+    assert np.isfinite(M.get_grad("layer0.expert1.b1")).all()
+    M.keep_grads(True)
+    M.step(batch)
     assert np.abs(M.get_grad("layer0.expert1.w1")).max() >= 0
     with pytest.raises(ted.InvalidConfigError):
         M.set_param("layer0.ffn.w1", g)  # layer 0 is a MoE layer: no dense FFN

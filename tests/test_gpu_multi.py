@@ -54,12 +54,32 @@ def test_four_gpus(tp, ep, dtd, E, exchange):
          env={"TED_EXCHANGE": exchange})
 
 
-def test_four_gpus_corrupt_drop_is_detected():
-    """Fault injection (test_moe.cpp:388-414): dispatching the wrong DTD chunk breaks
-    the layer output."""
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_four_gpus_corrupt_drop_is_detected(exchange):
+    """Fault injection (test_moe.cpp:388-414): dispatching the wrong DTD chunk fails the
+    placement verdict every rank computes on the device (moe.cpp:537-556) and breaks the
+    layer output, on both exchange implementations."""
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
-    _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--corrupt", "1", "--cf", "0")
+    _run(4, "--tp", "2", "--ep", "2", "--dtd", "1", "--corrupt", "1", "--cf", "0",
+         env={"TED_EXCHANGE": exchange})
+
+
+def test_two_gpus_corrupt_drop_is_detected():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, "--tp", "2", "--ep", "1", "--dtd", "1", "--corrupt", "1", "--cf", "0",
+         "--experts", "4")
+
+
+@pytest.mark.parametrize("nproc,tp,ep,E", [(2, 2, 1, 2), (4, 2, 2, 4)])
+def test_wide_layer_h4096(nproc, tp, ep, E):
+    """The north-star width (d=4096, ffn=16384, TP-sharded to 8192) over TP x EP with DTD,
+    128 tokens per shard so the fp64 oracle over all shards stays within minutes."""
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    _run(nproc, "--tp", str(tp), "--ep", str(ep), "--dtd", "1", "--experts", str(E),
+         "--hidden", "4096", "--tokens", "128")
 
 
 @pytest.mark.parametrize("nproc,tp,ep,zero", [(2, 2, 1, 1), (2, 1, 2, 1), (2, 1, 1, 1),
