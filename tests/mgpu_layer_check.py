@@ -143,7 +143,7 @@ def main():
             print("MGPU-OK " + json.dumps(report), flush=True)
         else:
             assert all(r["stats"]["placement_ok"] == 1 for r in allr), report
-            assert worst < TOL, f"multi-GPU parity failed: {report}""
+            assert worst < TOL, f"multi-GPU parity failed: {report}"
             if args.ledger:
                 # the layer's ledger accounting on the real exchange path == the reference's
                 # predict_comm_volume (cost_model.cpp:346-416) for the same config
