@@ -29,6 +29,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "ted_internal.h"
 #include "ted_ptx.cuh"
 #include "ted_vec.cuh"
@@ -74,17 +78,23 @@ __device__ __forceinline__ void st_state(float* p, float4 v, uint64_t pol) {
                : "memory");
 }
 
-template <int EPI>
+// PAIR: the CTA-pair variant (cta_group::2, KDIM mode): a 2x1 cluster computes a 256 x 256
+// tile, each CTA staging its 128 rows of A and 128 of B's 256 columns -- a third less
+// operand traffic into shared memory per FLOP than a single CTA's 128 x 256 tile, and
+// smaller stages, so a deeper ring.
+template <int EPI, bool PAIR = false>
 struct Cfg {
   static constexpr int EPI_WARPS = EPI == EPI_ADAM ? 16 : 8;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + epilogue warps
   static constexpr int COL_SPAN = BN / (EPI_WARPS / 4);  // tile columns per epilogue warp
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
-  static constexpr int STAGES = 4;
+  static constexpr int B_LOCAL = PAIR ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;  // this CTA's B
+  static constexpr int STAGE_LOCAL = A_STAGE_BYTES + B_LOCAL;
+  static constexpr int STAGES = PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4;
   // AdamW: the parameter half block and (keep-gradients mode) the gradient half block
   static constexpr size_t PER_WARP = EPI == EPI_ADAM ? 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
-  static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_BYTES + STAGING;
+  static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_LOCAL + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
 };
 
@@ -105,8 +115,11 @@ __device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, in
   m_blk = band * kBand + (idx - n_blk * rows);
 }
 
+// PAIR (KDIM only): t numbers 256-row tile pairs; this CTA takes row block 2 m + rank
+template <bool PAIR = false>
 __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_off,
-                                            const int* s_tstart, int total, int t, TileInfo& ti) {
+                                            const int* s_tstart, int total, int t, TileInfo& ti,
+                                            int rank = 0) {
   if (t >= total) return false;
   const int nt = p.N / BN;
   if (p.mode == GEMM_ROWS) {
@@ -116,10 +129,11 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
     raster(t - s_tstart[g], (s_off[g + 1] - s_off[g]) / BM, nt, ti.m_blk, ti.n_blk);
     ti.k_len = p.K;
   } else {
-    const int mt = p.M / BM;
+    const int mt = p.M / (PAIR ? 2 * BM : BM);
     const int per = mt * nt;
     ti.g = t / per;
     raster(t % per, mt, nt, ti.m_blk, ti.n_blk);
+    if (PAIR) ti.m_blk = 2 * ti.m_blk + rank;
     ti.k_len = s_off[ti.g + 1] - s_off[ti.g];
   }
   return true;
@@ -156,8 +170,8 @@ __device__ __forceinline__ uint4* blk_chunk(uint8_t* blk, int r, int j) {
   return reinterpret_cast<uint4*>(blk + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
 }
 
-template <bool A_MN, bool B_MN, int EPI>
-__global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
+template <bool A_MN, bool B_MN, int EPI, bool PAIR>
+__global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
@@ -165,8 +179,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
                         const __grid_constant__ CUtensorMap tmMaster,
                         const __grid_constant__ CUtensorMap tmM1,
                         const __grid_constant__ CUtensorMap tmM2, const GemmParams p) {
-  using CF = Cfg<EPI>;
+  using CF = Cfg<EPI, PAIR>;
+  static_assert(!PAIR || (A_MN && B_MN), "the CTA-pair variant is the KDIM (wgrad) GEMM");
   constexpr int STAGES = CF::STAGES;
+  constexpr int B_LOCAL = CF::B_LOCAL;
   constexpr int EPI_WARPS = CF::EPI_WARPS;
   constexpr int SPAN = CF::COL_SPAN;
   extern __shared__ uint8_t smem_raw[];
@@ -174,7 +190,7 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint8_t* sEpi = smem + STAGES * STAGE_BYTES;  // 1024-aligned staging blocks
+  uint8_t* sEpi = smem + STAGES * CF::STAGE_LOCAL;  // 1024-aligned staging blocks
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -185,6 +201,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
   int* s_tstart = s_off + (MAX_GROUPS + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // CTA pair: both CTAs walk the same tile sequence; rank 0 issues the MMAs
+  const int rank = PAIR ? int(ptx::cluster_rank()) : 0;
+  const int tile0 = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int tstep = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
 
   // group table (device-resident counts: no host sync on the routing result)
   for (int i = threadIdx.x; i <= p.groups; i += blockDim.x) s_off[i] = p.seg_off[i];
@@ -195,7 +215,7 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     for (int g = 0; g < p.groups; ++g) {
       s_tstart[g] = acc;
       if (p.mode == GEMM_ROWS) acc += ((s_off[g + 1] - s_off[g]) / BM) * nt;
-      else acc += (p.M / BM) * nt;
+      else acc += (p.M / (PAIR ? 2 * BM : BM)) * nt;
     }
     s_tstart[p.groups] = acc;
   }
@@ -210,14 +230,20 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], EPI_WARPS);
+      ptx::mbar_init(&tempty[s], EPI_WARPS * (PAIR ? 2 : 1));  // pair: both CTAs' epilogues
     }
     for (int w = 0; w < EPI_WARPS; ++w) ptx::mbar_init(&zbar[w], 1);
     ptx::fence_barrier_init();
   }
-  if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
-  ptx::tc_fence_before();
-  __syncthreads();
+  if (PAIR) {
+    if (warp == 2) ptx::tmem_alloc_pair(s_tmem, TMEM_COLS);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  } else {
+    if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
+    ptx::tc_fence_before();
+    __syncthreads();
+  }
   ptx::tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
   const int total = s_tstart[p.groups];
@@ -231,13 +257,29 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     TileInfo ti;
-    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+    // pair: the completion bytes of both CTAs' loads count on the leader's full barrier
+    const uint32_t lead_full = PAIR ? ptx::mapa(&full[0], 0) : 0;
+    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti, rank); t += tstep) {
       const int kb_n = ti.k_len / BK;
       for (int kb = 0; kb < kb_n; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* a_dst = sA + stage * A_STAGE_BYTES;
-        uint8_t* b_dst = sB + stage * B_STAGE_BYTES;
-        if (ptx::elect_one()) {
+        uint8_t* b_dst = sB + stage * B_LOCAL;
+        if (PAIR) {
+          if (ptx::elect_one()) {
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * CF::STAGE_LOCAL);
+            const uint32_t fb = lead_full + stage * 8;
+            const int krow = s_off[ti.g] + kb * BK;
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              ptx::tma_load_3d_pair(a_dst + i * (64 * BK * 2), &tmA, fb, ti.m_blk * BM + i * 64,
+                                    krow, 0);
+#pragma unroll
+            for (int i = 0; i < BN / 128; ++i)  // this CTA's half of the 256 columns
+              ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb,
+                                    ti.n_blk * BN + rank * (BN / 2) + i * 64, krow, 0);
+          }
+        } else if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           if (p.mode == GEMM_ROWS) {
             const int row0 = s_off[ti.g] + ti.m_blk * BM;
@@ -270,14 +312,14 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && rank == 0) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp walks the schedule (every value below is warp-uniform, so it lives in
     // uniform registers) and one elected lane issues: a single-lane loop made the compiler
     // re-broadcast every descriptor (ELECT + R2UR per MMA), which cost as many issue cycles
     // as the MMAs themselves.  Shared-memory descriptors are built once; a stage or K step
     // only adds to their 16 B-granular start-address field.
-    constexpr uint32_t idesc = ptx::idesc_bf16(BM, BN, A_MN, B_MN);
+    constexpr uint32_t idesc = ptx::idesc_bf16(PAIR ? 2 * BM : BM, BN, A_MN, B_MN);
     const uint64_t a_desc0 = A_MN ? ptx::sdesc_sw128(ptx::smem_u32(sA), 64 * BK * 2, 1024)
                                   : ptx::sdesc_sw128(ptx::smem_u32(sA), 16, 1024);
     const uint64_t b_desc0 = B_MN ? ptx::sdesc_sw128(ptx::smem_u32(sB), 64 * BK * 2, 1024)
@@ -289,7 +331,7 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     TileInfo ti;
-    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti); t += tstep) {
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
@@ -298,12 +340,18 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint64_t ad = a_desc0 + uint64_t(stage) * (A_STAGE_BYTES >> 4);
-        const uint64_t bd = b_desc0 + uint64_t(stage) * (B_STAGE_BYTES >> 4);
+        const uint64_t bd = b_desc0 + uint64_t(stage) * (B_LOCAL >> 4);
         if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            ptx::umma_bf16(tmem_d, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
-          ptx::umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          for (int k = 0; k < BK / 16; ++k) {
+            if (PAIR)
+              ptx::umma_bf16_pair(tmem_d, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
+            else
+              ptx::umma_bf16(tmem_d, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
+          }
+          // frees the smem slot (in both CTAs of a pair) when these MMAs finish
+          if (PAIR) ptx::umma_commit_pair(&empty[stage]);
+          else ptx::umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -311,7 +359,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           phase ^= 1;
         }
       }
-      if (ptx::elect_one()) ptx::umma_commit(&tfull[acc]);  // accumulator ready (k_len 0 too)
+      if (ptx::elect_one()) {  // accumulator ready (k_len 0 too)
+        if (PAIR) ptx::umma_commit_pair(&tfull[acc]);
+        else ptx::umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
@@ -351,17 +402,19 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     };
     int acc = 0;
     uint32_t acc_phase = 0;
-    int t = blockIdx.x;
+    int t = tile0;
     TileInfo ti, tn;
-    bool have = decode_tile(p, s_off, s_tstart, total, t, ti);
+    // the accumulator-empty barrier lives in the leader CTA (pair: both epilogues arrive)
+    const uint32_t lead_tempty = PAIR ? ptx::mapa(&tempty[0], 0) : 0;
+    bool have = decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti, rank);
     int64_t cur = have ? state_base(ti) : 0;
     if (have) {
 #pragma unroll
       for (int c = 0; c < RING - 1; ++c) issue(ring[c], cur + c * 128);
     }
     while (have) {
-      const int tnext = t + gridDim.x;
-      const bool have_next = decode_tile(p, s_off, s_tstart, total, tnext, tn);
+      const int tnext = t + tstep;
+      const bool have_next = decode_tile<PAIR>(p, s_off, s_tstart, total, tnext, tn, rank);
       const int64_t nxt = have_next ? state_base(tn) : 0;
       const int row0 = ti.m_blk * BM + sp * 32;
       const int colw = ti.n_blk * BN + cq * SPAN;
@@ -382,7 +435,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
           if (c == NC - 4) {  // accumulator fully read: the MMA warp may reuse it
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+              if (PAIR) ptx::mbar_arrive_cluster(lead_tempty + acc * 8);
+              else ptx::mbar_arrive(&tempty[acc]);
+            }
           }
         }
         float4* st = ring[c % RING];
@@ -453,7 +509,8 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0, zphase = 0;
     TileInfo ti;
-    for (int t = blockIdx.x; decode_tile(p, s_off, s_tstart, total, t, ti); t += gridDim.x) {
+    const uint32_t lead_tempty = PAIR ? ptx::mapa(&tempty[0], 0) : 0;
+    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti, rank); t += tstep) {
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       int row0, gz;
@@ -554,7 +611,10 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR) ptx::mbar_arrive_cluster(lead_tempty + acc * 8);
+        else ptx::mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -562,8 +622,15 @@ __global__ void __launch_bounds__(Cfg<EPI>::THREADS, 1)
     }
     if (lane == 0) ptx::bulk_wait0();
   }
-  __syncthreads();
-  if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  if (PAIR) {
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // the leader's MMAs read the peer's smem until the last tile
+    ptx::tc_fence_after();
+    if (warp == 2) ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  } else {
+    __syncthreads();
+    if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -597,21 +664,47 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
   return r == CUDA_SUCCESS;
 }
 
-template <bool A_MN, bool B_MN, int EPI>
+template <bool A_MN, bool B_MN, int EPI, bool PAIR = false>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                      const CUtensorMap& mx, const CUtensorMap& m0, const CUtensorMap& m1,
                      const CUtensorMap& m2, const GemmParams& p, int grid, cudaStream_t s) {
-  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI>;
-  static bool attr_set = false;  // per instantiation
+  using CF = Cfg<EPI, PAIR>;
+  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI, PAIR>;
+  static int pair_grid = 0;  // per instantiation: CTAs of the co-resident pairs
+  static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg<EPI>::SMEM));
+                                         int(CF::SMEM));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k<<<grid, Cfg<EPI>::THREADS, Cfg<EPI>::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
+  if (!PAIR) {
+    k<<<grid, CF::THREADS, CF::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
+    count_launch(1);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(CF::THREADS);
+  cfg.dynamicSmemBytes = CF::SMEM;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (pair_grid == 0) {  // one pair per TPC that can hold it
+    cfg.gridDim = dim3(grid & ~1);
+    int clusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, k, &cfg);
+    if (e != cudaSuccess) return e;
+    pair_grid = 2 * std::max(1, std::min(clusters, grid / 2));
+  }
+  cfg.gridDim = dim3(pair_grid);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, ma, mb, mc, mx, m0, m1, m2, p);
   count_launch(1);
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace
@@ -700,6 +793,16 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
     if (p.epi == EPI_DGELU) return launch_t<false, false, EPI_DGELU>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
     if (p.epi == EPI_BIAS) return launch_t<false, false, EPI_BIAS>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
     return launch_t<false, false, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+  }
+  // KDIM (wgrad): CTA pairs (cta_group::2) when M tiles pair up
+  static const bool pair_ok = [] {
+    const char* v = std::getenv("TED_GEMM_PAIR");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  if (pair_ok && p.M % (2 * BM) == 0) {
+    if (p.epi == EPI_ADAM)
+      return launch_t<true, true, EPI_ADAM, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    return launch_t<true, true, EPI_STORE, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
   }
   if (p.epi == EPI_ADAM) return launch_t<true, true, EPI_ADAM>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
   return launch_t<true, true, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);

@@ -101,8 +101,9 @@ def test_rows_dgelu_in_place():
 
 
 @pytest.mark.parametrize("rows,M,N", [([128], 128, 256), ([256, 0, 384], 256, 512),
-                                      ([2048, 1920, 2176], 1024, 1024)])
+                                      ([2048, 1920, 2176], 1024, 1024), ([640, 128], 512, 768)])
 def test_kdim_wgrad(rows, M, N):
+    """M % 256 == 0 runs the CTA-pair (cta_group::2) kernel, M = 128 the single-CTA one."""
     import paper_2303_06318_b200 as ted
     torch.manual_seed(3)
     G, R = len(rows), sum(rows)
