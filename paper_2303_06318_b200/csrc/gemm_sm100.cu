@@ -19,6 +19,11 @@
 // partials of dZ), and AdamW (the wgrad tile is the gradient of a parameter block:
 // master / m / v updated in the tile-major state layout, bf16 parameter written).
 //
+// The wgrad GEMMs run as CTA pairs (cta_group::2): a 2x1 cluster computes a 256 x 256 tile,
+// each CTA staging 128 rows of A and half of B, which cuts the operand traffic into shared
+// memory per FLOP by a third -- under the 1 kW power cap that energy is step time (5.5 %
+// faster step at C3, same-box A/B).
+//
 // Tile 128 x 256 x 64, banded tile order for L2 reuse; warp 0 = TMA producer, warp 1 = MMA
 // issuer (warp-converged, one elected lane issues), warp 2 = TMEM allocator, warps 4.. =
 // epilogue (warp w reads TMEM lanes 32*(w%4)..+31; 8 epilogue warps take one half of the
@@ -100,6 +105,10 @@ struct Cfg {
 
 struct TileInfo {
   int g, m_blk, n_blk, k_len;  // k_len = number of K elements (multiple of 64)
+  // CTA pair, ROWS mode: a group with an odd number of 128-row blocks ends in a pair tile
+  // whose second half lies past the segment; that CTA loads no A rows and stores nothing
+  bool pair_ghost = false;  // the rank-1 half of this pair tile is outside the segment
+  bool ghost = false;       // ... and this CTA is that half
 };
 
 // Tile order inside a group: bands of kBand row blocks (32 measured best of 8/16/32 at C3), walked column block by column
@@ -115,7 +124,7 @@ __device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, in
   m_blk = band * kBand + (idx - n_blk * rows);
 }
 
-// PAIR (KDIM only): t numbers 256-row tile pairs; this CTA takes row block 2 m + rank
+// PAIR: t numbers 256-row tile pairs; this CTA takes row block 2 m + rank
 template <bool PAIR = false>
 __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_off,
                                             const int* s_tstart, int total, int t, TileInfo& ti,
@@ -126,7 +135,13 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
     int g = 0;
     while (g + 1 < p.groups && s_tstart[g + 1] <= t) ++g;
     ti.g = g;
-    raster(t - s_tstart[g], (s_off[g + 1] - s_off[g]) / BM, nt, ti.m_blk, ti.n_blk);
+    const int blocks = (s_off[g + 1] - s_off[g]) / BM;
+    raster(t - s_tstart[g], PAIR ? (blocks + 1) / 2 : blocks, nt, ti.m_blk, ti.n_blk);
+    if (PAIR) {
+      ti.pair_ghost = 2 * ti.m_blk + 1 >= blocks;
+      ti.m_blk = 2 * ti.m_blk + rank;
+      ti.ghost = ti.m_blk >= blocks;
+    }
     ti.k_len = p.K;
   } else {
     const int mt = p.M / (PAIR ? 2 * BM : BM);
@@ -180,7 +195,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
                         const __grid_constant__ CUtensorMap tmM1,
                         const __grid_constant__ CUtensorMap tmM2, const GemmParams p) {
   using CF = Cfg<EPI, PAIR>;
-  static_assert(!PAIR || (A_MN && B_MN), "the CTA-pair variant is the KDIM (wgrad) GEMM");
+  static_assert(!PAIR || A_MN == B_MN || !A_MN, "pair: KDIM (A, B MN-major) or ROWS (A K-major)");
   constexpr int STAGES = CF::STAGES;
   constexpr int B_LOCAL = CF::B_LOCAL;
   constexpr int EPI_WARPS = CF::EPI_WARPS;
@@ -214,7 +229,8 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
     const int nt = p.N / BN;
     for (int g = 0; g < p.groups; ++g) {
       s_tstart[g] = acc;
-      if (p.mode == GEMM_ROWS) acc += ((s_off[g + 1] - s_off[g]) / BM) * nt;
+      const int blocks = (s_off[g + 1] - s_off[g]) / BM;
+      if (p.mode == GEMM_ROWS) acc += (PAIR ? (blocks + 1) / 2 : blocks) * nt;
       else acc += (p.M / (PAIR ? 2 * BM : BM)) * nt;
     }
     s_tstart[p.groups] = acc;
@@ -267,17 +283,33 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
         uint8_t* b_dst = sB + stage * B_LOCAL;
         if (PAIR) {
           if (ptx::elect_one()) {
-            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * CF::STAGE_LOCAL);
+            if (rank == 0)
+              ptx::mbar_arrive_expect_tx(
+                  &full[stage], 2 * CF::STAGE_LOCAL - (ti.pair_ghost ? A_STAGE_BYTES : 0));
             const uint32_t fb = lead_full + stage * 8;
-            const int krow = s_off[ti.g] + kb * BK;
+            const int ncol = ti.n_blk * BN + rank * (BN / 2);  // this CTA's half of B's columns
+            if (A_MN) {  // KDIM
+              const int krow = s_off[ti.g] + kb * BK;
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              ptx::tma_load_3d_pair(a_dst + i * (64 * BK * 2), &tmA, fb, ti.m_blk * BM + i * 64,
-                                    krow, 0);
+              for (int i = 0; i < BM / 64; ++i)
+                ptx::tma_load_3d_pair(a_dst + i * (64 * BK * 2), &tmA, fb,
+                                      ti.m_blk * BM + i * 64, krow, 0);
 #pragma unroll
-            for (int i = 0; i < BN / 128; ++i)  // this CTA's half of the 256 columns
-              ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb,
-                                    ti.n_blk * BN + rank * (BN / 2) + i * 64, krow, 0);
+              for (int i = 0; i < BN / 128; ++i)
+                ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb, ncol + i * 64, krow, 0);
+            } else {  // ROWS
+              const int k0 = kb * BK;
+              if (!ti.ghost)
+                ptx::tma_load_3d_pair(a_dst, &tmA, fb, k0, s_off[ti.g] + ti.m_blk * BM, 0);
+              if (B_MN) {
+#pragma unroll
+                for (int i = 0; i < BN / 128; ++i)
+                  ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb, ncol + i * 64, k0,
+                                        ti.g);
+              } else {
+                ptx::tma_load_3d_pair(b_dst, &tmB, fb, k0, ncol, ti.g);
+              }
+            }
           }
         } else if (ptx::elect_one()) {
           ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -524,7 +556,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
 #pragma unroll 1
-      for (int c0 = cq * SPAN; c0 < (cq + 1) * SPAN; c0 += 32) {
+      for (int c0 = cq * SPAN; c0 < (ti.ghost ? cq * SPAN : (cq + 1) * SPAN); c0 += 32) {
         const int col = ti.n_blk * BN + c0;
         float v[32];
         ptx::tmem_ld32(tbase + c0, v);
@@ -707,6 +739,18 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// CTA-pair variants in use: bit 0 KDIM (wgrad), bit 1 ROWS (forward / dgrad).  Default: the
+// wgrad GEMMs only -- the ROWS pairs measured 4-8 % slower at C3 (a group with an odd number
+// of 128-row blocks ends in a half-empty pair tile, and the pair ran at lower clocks under
+// the power cap).  TED_GEMM_PAIR=<mask> selects (an A/B switch for measurements).
+int pair_mask() {
+  static const int m = [] {
+    const char* v = std::getenv("TED_GEMM_PAIR");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+
 }  // namespace
 
 int sm_count() {
@@ -755,8 +799,9 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
     ok = make_map(&ma, o.A, p.K, rows, 1, o.lda * 2, 0, BK, BM);
     if (o.b_mn)
       ok = ok && make_map(&mb, o.B, p.N, p.K, p.groups, o.ldb * 2, o.b_group_stride * 2, 64, BK);
-    else
-      ok = ok && make_map(&mb, o.B, p.K, p.N, p.groups, o.ldb * 2, o.b_group_stride * 2, BK, BN);
+    else  // a CTA pair stages half of B's columns per CTA
+      ok = ok && make_map(&mb, o.B, p.K, p.N, p.groups, o.ldb * 2, o.b_group_stride * 2, BK,
+                          (pair_mask() & 2) ? BN / 2 : BN);
     ok = ok && make_map(&mc, p.C, p.N, rows, 1, p.ldc * 2, 0, 32, 32, SW64);
     if (p.aux) ok = ok && make_map(&mx, p.aux, p.N, rows, 1, p.ld_aux * 2, 0, 32, 32, SW64);
     else mx = mc;
@@ -784,6 +829,20 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
   if (p.mode == GEMM_ROWS) {
+    if (pair_mask() & 2) {  // CTA pairs over 256-row tiles
+      if (o.b_mn) {
+        if (p.epi == EPI_BIAS_GELU)
+          return launch_t<false, true, EPI_BIAS_GELU, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+        if (p.epi == EPI_BIAS)
+          return launch_t<false, true, EPI_BIAS, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+        return launch_t<false, true, EPI_STORE, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      }
+      if (p.epi == EPI_DGELU)
+        return launch_t<false, false, EPI_DGELU, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      if (p.epi == EPI_BIAS)
+        return launch_t<false, false, EPI_BIAS, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      return launch_t<false, false, EPI_STORE, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    }
     if (o.b_mn) {
       if (p.epi == EPI_BIAS_GELU)
         return launch_t<false, true, EPI_BIAS_GELU>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
@@ -795,11 +854,7 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
     return launch_t<false, false, EPI_STORE>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
   }
   // KDIM (wgrad): CTA pairs (cta_group::2) when M tiles pair up
-  static const bool pair_ok = [] {
-    const char* v = std::getenv("TED_GEMM_PAIR");
-    return !(v && std::strcmp(v, "0") == 0);
-  }();
-  if (pair_ok && p.M % (2 * BM) == 0) {
+  if ((pair_mask() & 1) && p.M % (2 * BM) == 0) {
     if (p.epi == EPI_ADAM)
       return launch_t<true, true, EPI_ADAM, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
     return launch_t<true, true, EPI_STORE, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
