@@ -46,7 +46,9 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 // kernel (the fused wgrad epilogue and the standalone ones) uses this one expression, so
 // fused and unfused steps agree bit for bit.  IEEE sqrt and division: the SFU-approximate
 // pair (sqrt.approx + rcp.approx, a third of the instructions) measured 3-4 % SLOWER in the
-// fused wgrad epilogue inside the power-capped step (tools/ab_lib.sh, same box).
+// fused wgrad epilogue inside the power-capped step (tools/ab_lib.sh, same box), and again
+// 3 % slower for the CTA-pair kernel alone (tools/wgrad_power.sh: 7.23 vs 7.03 ms per
+// launch, although its SM clock settled higher, 1150 vs 1027 MHz).
 __device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g, const AdamK& k,
                                            float c1, float c2) {
   m = k.b1 * m + k.omb1 * g;
