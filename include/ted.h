@@ -16,6 +16,10 @@
  *   ted_grouped_gemm  <- linear_forward/backward over experts  src/nn.cpp:22-90,
  *                        column/row_parallel_*           src/parallel_linear.cpp:8-40
  *   ted_adam_step     <- OptimizerShard::step_owned      src/optimizer.cpp:58-104
+ *   ted_dispatch_*    <- dispatch pack / un-permute      src/moe.cpp:440-476, :661-675
+ *   ted_combine_*     <- combine fwd / bwd               src/moe.cpp:558-563, :587-597
+ *   ted_expert_ffn_*  <- expert FFN (linear + gelu)      src/parallel_linear.cpp:8-40,
+ *                                                        src/nn.cpp:22-121
  *   ted_shard_range   <- shard_range                     src/optimizer.cpp:12-28
  *   ted_layer_*       <- MoeRank::forward_layer / backward_layer (MoE branch),
  *                        run_grad_sync, run_optimizer_step    src/moe.cpp:418-741
@@ -35,6 +39,7 @@
  */
 #ifndef TED_H
 #define TED_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -139,6 +144,70 @@ int ted_adam_step(float* master_dev, float* m1_dev, float* m2_dev, uint16_t* par
 int ted_placement_verdict(const int32_t* pos_send_dev, const int32_t* pos_home_dev, int64_t n,
                           int T, int slot_chunk, int32_t* verdict_dev, void* stream);
 
+/* ---------------------------------------------------------------- single-rank MoE operators
+ * The MoE branch of SerialModel::forward_layer / backward_layer (moe.cpp:989-1064) as
+ * separate stream-ordered operators over caller-owned device buffers, for hosts that drive
+ * the pieces themselves.  "pos" is a token's row in the expert-side (assembled) buffer:
+ * experts ascending, tokens ascending inside an expert (the reference's append order,
+ * moe.cpp:454-462), each expert segment padded to 128 rows (seg_off [E+1] int32, device);
+ * pos = -1 for a token over capacity.  Scratch comes from a per-(device, stream) workspace
+ * that grows on first use and is then reused (ted_ops_reserve pre-sizes it, e.g. before a
+ * CUDA graph capture; ted_ops_release frees every workspace).  Multi-rank exchange (EP
+ * all-to-all, DTD, TP all-reduce) is the ted_layer_* object's job. */
+int ted_ops_reserve(size_t bytes, void* stream);
+int ted_ops_release(void);
+/* rows an assembled buffer needs for n tokens over E experts (capacity <= 0: unlimited) */
+int64_t ted_dispatch_rows_bound(int64_t n, int E, int64_t capacity);
+/* dispatch pack (moe.cpp:440-476, one rank): capacity slots (ted_route's rule), pos [n],
+ * x_asm [bound][h] bf16 (pad rows zeroed), seg_off [E+1], kept_counts [E]; slot nullable. */
+int ted_dispatch_forward(const uint16_t* a_dev, const int32_t* expert_dev, int64_t n, int h, int E,
+                         int64_t capacity, int32_t* slot_dev, int32_t* pos_dev,
+                         uint16_t* x_asm_dev, int32_t* seg_off_dev, int32_t* kept_counts_dev,
+                         void* stream);
+/* the dispatch's input gradient, un-permuted (moe.cpp:661-675): da[k] = dx_asm[pos[k]], 0 if
+ * dropped.  (ted_gate_backward_dlogits can fuse it with the gate's input gradient.) */
+int ted_dispatch_backward(const uint16_t* dx_asm_dev, const int32_t* pos_dev, int64_t n, int h,
+                          uint16_t* da_dev, void* stream);
+/* combine (moe.cpp:558-563): y[k] = prob[k] * f_asm[pos[k]] (0 if dropped) */
+int ted_combine_forward(const uint16_t* f_asm_dev, const int32_t* pos_dev, const float* prob_dev,
+                        int64_t n, int h, uint16_t* y_dev, void* stream);
+/* combine backward (moe.cpp:587-597) with the gate's dlogits (moe.cpp:197-203):
+ * df_asm[pos[k]] = prob[k] dy[k], dchosen_k = <f_asm[pos[k]], dy[k]>,
+ * dlogits[k][j] = dchosen_k p_e (delta_je - p_j) [n][E] fp32; with seg_off and kept_counts
+ * the pad rows of df_asm are zeroed (the wgrad GEMMs reduce over them). */
+int ted_combine_backward(const uint16_t* f_asm_dev, const int32_t* pos_dev, const float* prob_dev,
+                         const float* probs_dev, const int32_t* expert_dev, const uint16_t* dy_dev,
+                         int64_t n, int h, int E, const int32_t* seg_off_dev,
+                         const int32_t* kept_counts_dev, uint16_t* df_asm_dev, float* dlogits_dev,
+                         void* stream);
+/* gate_backward from dlogits (moe.cpp:205-206): dWg = a^T dlogits [h][E] bf16 (nullable),
+ * dinput = dlogits Wg^T (nullable); with dispatch_grad + pos also the un-permuted dispatch
+ * gradient: dinput[k] += dispatch_grad[pos[k]]  (da = da_dispatch + dinput, moe.cpp:685). */
+int ted_gate_backward_dlogits(const uint16_t* a_dev, const uint16_t* wg_dev, const float* dlogits_dev,
+                              int64_t n, int h, int E, uint16_t* dwg_dev, uint16_t* dinput_dev,
+                              const uint16_t* dispatch_grad_dev, const int32_t* pos_dev,
+                              void* stream);
+/* expert FFN forward over the assembled rows (column_parallel_forward + gelu +
+ * row_parallel_forward on one rank, parallel_linear.cpp:8-31): per expert g,
+ * Z = X W1_g + b1_g, H = gelu(Z), F = H W2_g + b2_g.  W1_g [h][f], W2_g [f][h] row-major bf16
+ * at (w1 + g * w1_stride) etc.; rows = the assembled-buffer bound (multiple of 128);
+ * z, hact [rows][f], f_asm [rows][h].  h % 256 == 0, f % 256 == 0. */
+int ted_expert_ffn_forward(const uint16_t* x_asm_dev, const int32_t* seg_off_dev, int64_t rows,
+                           int E, int h, int f, const uint16_t* w1_dev, int64_t w1_stride,
+                           const uint16_t* b1_dev, int64_t b1_stride, const uint16_t* w2_dev,
+                           int64_t w2_stride, const uint16_t* b2_dev, int64_t b2_stride,
+                           uint16_t* z_dev, uint16_t* hact_dev, uint16_t* f_asm_dev, void* stream);
+/* expert FFN backward (row/column_parallel_backward + gelu_backward, parallel_linear.cpp:13-40,
+ * nn.cpp:114-121): dZ = (dF W2^T) gelu'(Z) written over z, dX = dZ W1^T, dW1 = X^T dZ,
+ * db1 = colsum(dZ), dW2 = H^T dF, db2 = colsum(dF) (bf16, per-expert strides). */
+int ted_expert_ffn_backward(const uint16_t* x_asm_dev, uint16_t* z_dev, const uint16_t* hact_dev,
+                            const uint16_t* df_asm_dev, const int32_t* seg_off_dev, int64_t rows,
+                            int E, int h, int f, const uint16_t* w1_dev, int64_t w1_stride,
+                            const uint16_t* w2_dev, int64_t w2_stride, uint16_t* dx_asm_dev,
+                            uint16_t* dw1_dev, int64_t dw1_stride, uint16_t* db1_dev,
+                            int64_t db1_stride, uint16_t* dw2_dev, int64_t dw2_stride,
+                            uint16_t* db2_dev, int64_t db2_stride, void* stream);
+
 /* ---------------------------------------------------------------- MoE layer (MoeRank) */
 
 typedef struct ted_layer ted_layer;
@@ -186,6 +255,14 @@ int ted_layer_step(ted_layer* L, const uint16_t* a_dev, uint16_t* y_dev, uint16_
                    void* stream);
 /* Local loss of the last forward (sum(y^2) / (2 N_global)); synchronises the stream. */
 int ted_layer_loss(ted_layer* L, double* loss, void* stream);
+/* Failure detection (TrainerOptions::collective_timeout, moe.hpp:96; Fabric's TimeoutError,
+ * fabric.cpp:65-96).  A plane member that does not reach an NVLink barrier within `seconds`
+ * (default 120; 0 = wait forever) is recorded by the device in a host-mapped word -- no
+ * trap, the CUDA context survives; a stream wait of ted_layer_loss that exceeds it, or an
+ * asynchronous NCCL error, aborts the layer's communicators (ncclCommAbort).  The next call
+ * returns TED_ERR_RUNTIME with "TimeoutError: ..." (or the NCCL error) in ted_last_error,
+ * and so does every later call: the layer must be destroyed. */
+int ted_layer_set_timeout(ted_layer* L, double seconds);
 
 typedef struct {
   int64_t tokens;            /* n */
@@ -254,6 +331,8 @@ int ted_model_forward(ted_model* M, const uint16_t* batch, void* stream);
 int ted_model_backward(ted_model* M, void* stream);
 int ted_model_optimizer_step(ted_model* M, void* stream);
 int ted_model_loss(ted_model* M, double* loss, void* stream);
+/* ted_layer_set_timeout for the stack (its MoE layers and its own communicators) */
+int ted_model_set_timeout(ted_model* M, double seconds);
 /* last layer's output (tokens_per_shard x hidden bf16, device) */
 int ted_model_output(ted_model* M, uint16_t* y, void* stream);
 /* device memory of this rank (MemoryReport, moe.hpp / moe.cpp:746-757), bytes:

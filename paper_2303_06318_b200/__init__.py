@@ -143,6 +143,24 @@ _sig("ted_layer_backward", _i32, [_vp, _vp, _vp, _vp])
 _sig("ted_layer_optimizer_step", _i32, [_vp, _vp])
 _sig("ted_layer_step", _i32, [_vp, _vp, _vp, _vp, _vp])
 _sig("ted_layer_loss", _i32, [_vp, C.POINTER(_dbl), _vp])
+_sig("ted_layer_set_timeout", _i32, [_vp, _dbl])
+_sig("ted_ops_reserve", _i32, [C.c_size_t, _vp])
+_sig("ted_ops_release", _i32, [])
+_sig("ted_dispatch_rows_bound", _i64, [_i64, _i32, _i64])
+_sig("ted_dispatch_forward", _i32, [_vp, _vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp,
+                                    _vp])
+_sig("ted_dispatch_backward", _i32, [_vp, _vp, _i64, _i32, _vp, _vp])
+_sig("ted_combine_forward", _i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp])
+_sig("ted_combine_backward", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp,
+                                    _vp, _vp, _vp])
+_sig("ted_gate_backward_dlogits", _i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp,
+                                         _vp])
+_sig("ted_expert_ffn_forward", _i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _i64, _vp, _i64,
+                                      _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp])
+_sig("ted_expert_ffn_backward", _i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp,
+                                       _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _i64,
+                                       _vp, _i64, _vp])
+_sig("ted_model_set_timeout", _i32, [_vp, _dbl])
 _sig("ted_layer_get_stats", _i32, [_vp, C.POINTER(LayerStats)])
 _sig("ted_layer_get_routing", _i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp])
 _sig("ted_layer_timing", _i32, [_vp, _i32])
@@ -171,11 +189,15 @@ EXPORTED = [
     "ted_gate_backward", "ted_grouped_gemm", "ted_adam_step", "ted_placement_verdict", "ted_layer_create",
     "ted_layer_destroy", "ted_nccl_unique_id", "ted_layer_set_param", "ted_layer_get_param",
     "ted_layer_get_grad", "ted_layer_keep_grads", "ted_layer_init_params", "ted_layer_forward", "ted_layer_backward",
-    "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_get_stats",
+    "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_set_timeout",
+    "ted_layer_get_stats",
     "ted_layer_get_routing", "ted_layer_timing", "ted_layer_timing_read", "ted_kernel_launches",
     "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
     "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_keep_grads", "ted_model_step",
     "ted_model_forward", "ted_model_backward", "ted_model_optimizer_step", "ted_model_loss",
+    "ted_model_set_timeout", "ted_ops_reserve", "ted_ops_release", "ted_dispatch_rows_bound",
+    "ted_dispatch_forward", "ted_dispatch_backward", "ted_combine_forward", "ted_combine_backward",
+    "ted_gate_backward_dlogits", "ted_expert_ffn_forward", "ted_expert_ffn_backward",
     "ted_model_output", "ted_model_memory"]
 
 
@@ -340,6 +362,102 @@ def gate_backward(a, wg, probs, expert, dchosen, stream=None):
     return dwg, dinput
 
 
+# ---- the MoE branch as single-rank operators (moe.cpp:440-563 / :587-686 on one rank)
+
+def ops_reserve(nbytes: int, stream=None):
+    _check(_lib.ted_ops_reserve(int(nbytes), _stream(stream)))
+
+
+def dispatch_forward(a, expert, E: int, cap: int = 0, stream=None):
+    """Dispatch pack: returns (x_asm [R,h] bf16, pos int32 [n], seg_off int32 [E+1],
+    kept int32 [E], slot int32 [n]); R = dispatch_rows_bound(n, E, cap)."""
+    import torch
+    n, h = a.shape
+    R = int(_lib.ted_dispatch_rows_bound(n, E, cap))
+    dev = a.device
+    x = torch.empty(R, h, dtype=torch.bfloat16, device=dev)
+    pos = torch.empty(n, dtype=torch.int32, device=dev)
+    slot = torch.empty(n, dtype=torch.int32, device=dev)
+    seg = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    kept = torch.empty(E, dtype=torch.int32, device=dev)
+    _check(_lib.ted_dispatch_forward(_p(a), _p(expert), n, h, E, cap, _p(slot), _p(pos), _p(x),
+                                     _p(seg), _p(kept), _stream(stream)))
+    return x, pos, seg, kept, slot
+
+
+def dispatch_backward(dx_asm, pos, n: int, stream=None):
+    import torch
+    h = dx_asm.shape[1]
+    da = torch.empty(n, h, dtype=torch.bfloat16, device=dx_asm.device)
+    _check(_lib.ted_dispatch_backward(_p(dx_asm), _p(pos), n, h, _p(da), _stream(stream)))
+    return da
+
+
+def combine_forward(f_asm, pos, prob, stream=None):
+    import torch
+    n, h = pos.shape[0], f_asm.shape[1]
+    y = torch.empty(n, h, dtype=torch.bfloat16, device=f_asm.device)
+    _check(_lib.ted_combine_forward(_p(f_asm), _p(pos), _p(prob), n, h, _p(y), _stream(stream)))
+    return y
+
+
+def combine_backward(f_asm, pos, prob, probs, expert, dy, seg_off=None, kept=None, stream=None):
+    """Returns (df_asm like f_asm, dlogits fp32 [n,E])."""
+    import torch
+    n, E = probs.shape
+    h = f_asm.shape[1]
+    df = torch.empty_like(f_asm)
+    dl = torch.empty(n, E, dtype=torch.float32, device=f_asm.device)
+    _check(_lib.ted_combine_backward(_p(f_asm), _p(pos), _p(prob), _p(probs), _p(expert), _p(dy),
+                                     n, h, E, _p(seg_off), _p(kept), _p(df), _p(dl),
+                                     _stream(stream)))
+    return df, dl
+
+
+def gate_backward_dlogits(a, wg, dlogits, dispatch_grad=None, pos=None, stream=None):
+    """Returns (dWg [h,E] bf16, da [n,h] bf16 = dlogits Wg^T (+ dispatch_grad[pos]))."""
+    import torch
+    n, h = a.shape
+    E = wg.shape[1]
+    dwg = torch.empty(h, E, dtype=torch.bfloat16, device=a.device)
+    da = torch.empty(n, h, dtype=torch.bfloat16, device=a.device)
+    _check(_lib.ted_gate_backward_dlogits(_p(a), _p(wg), _p(dlogits), n, h, E, _p(dwg), _p(da),
+                                          _p(dispatch_grad), _p(pos), _stream(stream)))
+    return dwg, da
+
+
+def expert_ffn_forward(x_asm, seg_off, w1, b1, w2, b2, stream=None):
+    """w1 [E,h,f], b1 [E,f], w2 [E,f,h], b2 [E,h] bf16.  Returns (Z, H, F)."""
+    import torch
+    R, h = x_asm.shape
+    E, _, f = w1.shape
+    z = torch.empty(R, f, dtype=torch.bfloat16, device=x_asm.device)
+    hh = torch.empty_like(z)
+    fo = torch.empty(R, h, dtype=torch.bfloat16, device=x_asm.device)
+    _check(_lib.ted_expert_ffn_forward(_p(x_asm), _p(seg_off), R, E, h, f, _p(w1), h * f, _p(b1),
+                                       f, _p(w2), f * h, _p(b2), h, _p(z), _p(hh), _p(fo),
+                                       _stream(stream)))
+    return z, hh, fo
+
+
+def expert_ffn_backward(x_asm, z, hact, df_asm, seg_off, w1, w2, stream=None):
+    """z is overwritten with dZ.  Returns (dX, dW1, db1, dW2, db2)."""
+    import torch
+    R, h = x_asm.shape
+    E, _, f = w1.shape
+    dev = x_asm.device
+    dx = torch.empty(R, h, dtype=torch.bfloat16, device=dev)
+    dw1 = torch.empty(E, h, f, dtype=torch.bfloat16, device=dev)
+    db1 = torch.empty(E, f, dtype=torch.bfloat16, device=dev)
+    dw2 = torch.empty(E, f, h, dtype=torch.bfloat16, device=dev)
+    db2 = torch.empty(E, h, dtype=torch.bfloat16, device=dev)
+    _check(_lib.ted_expert_ffn_backward(_p(x_asm), _p(z), _p(hact), _p(df_asm), _p(seg_off), R,
+                                        E, h, f, _p(w1), h * f, _p(w2), f * h, _p(dx), _p(dw1),
+                                        h * f, _p(db1), f, _p(dw2), f * h, _p(db2), h,
+                                        _stream(stream)))
+    return dx, dw1, db1, dw2, db2
+
+
 GEMM_ROWS, GEMM_KDIM = 0, 1
 EPI_STORE, EPI_BIAS, EPI_BIAS_GELU, EPI_DGELU = 0, 1, 2, 3
 
@@ -463,6 +581,11 @@ class MoeLayer:
         v = _dbl()
         _check(_lib.ted_layer_loss(self._h, C.byref(v), _stream(stream)))
         return v.value
+
+    def set_timeout(self, seconds: float):
+        """collective_timeout (moe.hpp:96): a stalled peer raises TedRuntimeError
+        ("TimeoutError: ...") at the next call instead of hanging or trapping."""
+        _check(_lib.ted_layer_set_timeout(self._h, float(seconds)))
 
     def stats(self) -> dict:
         s = LayerStats()
@@ -591,6 +714,9 @@ class TedModel:
         v = _dbl()
         _check(_lib.ted_model_loss(self._h, C.byref(v), _stream(stream)))
         return v.value
+
+    def set_timeout(self, seconds: float):
+        _check(_lib.ted_model_set_timeout(self._h, float(seconds)))
 
     def output(self, y, stream=None):
         _check(_lib.ted_model_output(self._h, _p(y), _stream(stream)))

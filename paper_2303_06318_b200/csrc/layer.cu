@@ -20,8 +20,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -75,6 +77,14 @@ struct ted_layer {
   DevBuf<unsigned> bar_flags;  // plane barrier: slot r written by plane member r (IPC-mapped)
   DevBuf<unsigned> bar_epoch;  // device barrier epoch (advances on graph replays too)
   bool nccl_barrier = false;
+  // failure detection (TrainerOptions::collective_timeout, moe.hpp:96; Fabric's
+  // TimeoutError, fabric.cpp:65-96): the plane barrier records a missing member in a
+  // host-mapped word instead of trapping; host-side waits poll it and NCCL's async errors
+  // and abort the communicators on timeout.  A faulted layer fails every later call.
+  int* fault_h = nullptr;  // host view (mapped pinned memory)
+  int* fault_d = nullptr;  // device view
+  double timeout_s = 120.0;
+  std::string poisoned;
   // peer exchange with the plan built on the device (no host round trip per step, so the
   // multi-GPU step is graph-capturable); the host plan is rebuilt lazily for statistics
   bool devplan = false;
@@ -286,8 +296,63 @@ void plane_barrier(ted_layer* L, cudaStream_t s) {
     return;
   }
   check(plane_barrier_peer(L->peer_tab.p + size_t(4) * L->plane_size, L->plane_size,
-                           L->plane_rank, L->bar_epoch.p, s),
+                           L->plane_rank, L->bar_epoch.p, L->fault_d,
+                           (unsigned long long)(L->timeout_s * 1e9), s),
         "plane_barrier_peer");
+}
+
+void abort_comms(ted_layer* L) {
+  for (ncclComm_t* c : {&L->tp_c, &L->ep_c, &L->expdp_c, &L->nonexpdp_c, &L->plane_c,
+                        &L->world_c})
+    if (*c) {
+      ncclCommAbort(*c);
+      *c = nullptr;
+    }
+}
+
+[[noreturn]] void poison(ted_layer* L, const std::string& why) {
+  L->poisoned = why;
+  abort_comms(L);
+  throw RuntimeError(why);
+}
+
+// the layer's failure state: a faulted earlier call, a plane-barrier timeout recorded by
+// the device, or an asynchronous NCCL error
+void check_fault(ted_layer* L) {
+  if (!L->poisoned.empty()) throw RuntimeError(L->poisoned + " (layer unusable after the failure)");
+  const int f = L->fault_h ? *reinterpret_cast<volatile int*>(L->fault_h) : 0;
+  if (f != 0) {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf),
+                  "TimeoutError: plane barrier of rank %d: member %d of the EP x TP plane did not "
+                  "arrive within %.1f s (collective_timeout)",
+                  L->rank, f - 1, L->timeout_s);
+    poison(L, buf);
+  }
+  for (ncclComm_t c : {L->tp_c, L->ep_c, L->expdp_c, L->nonexpdp_c, L->plane_c, L->world_c}) {
+    if (!c) continue;
+    ncclResult_t r = ncclSuccess;
+    if (ncclCommGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+      poison(L, std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+  }
+}
+
+// stream synchronisation that cannot hang: polls the stream, the fault word and NCCL's
+// async errors; past the timeout the communicators are aborted (TimeoutError, status 1)
+void wait_stream(ted_layer* L, cudaStream_t s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) CU(q);
+    check_fault(L);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (L->timeout_s > 0 && el > L->timeout_s && L->world > 1)
+      poison(L, "TimeoutError: rank " + std::to_string(L->rank) + ": the step did not complete within " +
+                    std::to_string(L->timeout_s) + " s (a peer is stalled or gone; collective_timeout)");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  check_fault(L);
 }
 
 const unsigned long long* peer_table(ted_layer* L, int which) {
@@ -496,7 +561,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
       check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->plane_size * sizeof(int),
                             cudaMemcpyDeviceToHost, s),
             "memcpy");
-      check(cudaStreamSynchronize(s), "sync");
+      wait_stream(L, s);
       for (int src = 0; src < L->P; ++src)  // TP peers hold identical counts: take t = 0
         std::memcpy(cnt.data() + size_t(src) * nc, L->h_kc_all.p + size_t(L->T * src) * nc,
                     nc * sizeof(int));
@@ -510,7 +575,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
       check(cudaMemcpyAsync(L->h_kc_all.p, L->kc_all.p, nc * L->P * sizeof(int),
                             cudaMemcpyDeviceToHost, s),
             "memcpy");
-      check(cudaStreamSynchronize(s), "sync");
+      wait_stream(L, s);
       std::memcpy(cnt.data(), L->h_kc_all.p, nc * L->P * sizeof(int));
     }
     L->plan = build_plan(L->P, L->T, E, L->dtd, L->ep, L->t, cnt.data());
@@ -1092,6 +1157,10 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->cap = cf > 0 ? std::min<int64_t>(L->n, int64_t(std::ceil(cf * L->n / double(L->E)))) : L->n;
   L->nblk = (L->n + kRouteBlock - 1) / kRouteBlock;
   require_device();
+  CU(cudaHostAlloc(reinterpret_cast<void**>(&L->fault_h), sizeof(int),
+                   cudaHostAllocMapped | cudaHostAllocPortable));
+  *L->fault_h = 0;
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&L->fault_d), L->fault_h, 0));
 
   // communicators (topology.cpp:56-93 colours; ascending-rank keys)
   if (L->world > 1) {
@@ -1263,6 +1332,12 @@ void layer_set_forward_mode(ted_layer* L, int mode) {
   if (mode == FWD_RECORD && !L->local) stash_alloc(L);
 }
 
+void layer_check_fault(ted_layer* L) { check_fault(L); }
+void layer_abort(ted_layer* L, const std::string& why) {
+  if (L->poisoned.empty()) L->poisoned = why;
+  abort_comms(L);
+}
+
 void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int64_t* stash) {
   int64_t act = 0;
   for (const DevBuf<bf16>* b : {&L->x_asm, &L->z, &L->hbuf, &L->fe_asm, &L->xsend, &L->fhome,
@@ -1318,7 +1393,18 @@ void ted_layer_destroy(ted_layer* L) {
       ncclCommDestroy(*c);
       *c = nullptr;
     }
+  if (L->fault_h) cudaFreeHost(L->fault_h);
   delete L;
+}
+
+int ted_layer_set_timeout(ted_layer* L, double seconds) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    require(seconds >= 0, "timeout must be >= 0 (0 = no limit)");
+    CU(cudaDeviceSynchronize());
+    L->timeout_s = seconds;
+    for (auto& g : L->graphs) graph_reset(g);  // the barrier kernels carry the timeout
+  });
 }
 
 int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
@@ -1412,6 +1498,7 @@ int ted_layer_init_params(ted_layer* L, uint64_t seed) {
 int ted_layer_forward(ted_layer* L, const uint16_t* a, uint16_t* y, void* stream) {
   return guard([&] {
     require(L && a && y, "null argument");
+    check_fault(L);
     layer_forward(L, reinterpret_cast<const bf16*>(a), reinterpret_cast<bf16*>(y), S(stream));
   });
 }
@@ -1419,6 +1506,7 @@ int ted_layer_forward(ted_layer* L, const uint16_t* a, uint16_t* y, void* stream
 int ted_layer_backward(ted_layer* L, const uint16_t* dy, uint16_t* da, void* stream) {
   return guard([&] {
     require(L && da, "null argument");
+    check_fault(L);
     layer_backward(L, reinterpret_cast<const bf16*>(dy), reinterpret_cast<bf16*>(da), S(stream));
   });
 }
@@ -1426,6 +1514,7 @@ int ted_layer_backward(ted_layer* L, const uint16_t* dy, uint16_t* da, void* str
 int ted_layer_optimizer_step(ted_layer* L, void* stream) {
   return guard([&] {
     require(L != nullptr, "null layer");
+    check_fault(L);
     layer_optimizer(L, S(stream));
   });
 }
@@ -1492,6 +1581,7 @@ extern "C" {
 int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, void* stream) {
   return guard([&] {
     require(L && a && y && da, "null argument");
+    check_fault(L);
     cudaStream_t cs = S(stream);
     cudaStream_t ms = cs;
     if (L->hs) {  // fork onto the layer's own stream (the graph is captured on it)
@@ -1547,7 +1637,7 @@ int ted_layer_loss(ted_layer* L, double* loss, void* stream) {
   return guard([&] {
     require(L && loss, "null argument");
     CU(cudaMemcpyAsync(loss, L->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
-    CU(cudaStreamSynchronize(S(stream)));
+    wait_stream(L, S(stream));
   });
 }
 
@@ -1556,6 +1646,7 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
     require(L && o, "null argument");
     std::memset(o, 0, sizeof(*o));
     CU(cudaDeviceSynchronize());
+    check_fault(L);
     const int E = L->E, Tc = L->Tc;
     std::vector<int> kc(size_t(Tc) * E), cp(size_t(Tc + 1) * E);
     CU(cudaMemcpy(kc.data(), L->kc.p, kc.size() * 4, cudaMemcpyDeviceToHost));

@@ -19,9 +19,11 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ted.h"
@@ -123,9 +125,61 @@ struct ted_model {
   DevBuf<float> col_part;
   DevBuf<double> loss_part, loss;
   bool have_forward = false;
+  double timeout_s = 120.0;  // collective_timeout (moe.hpp:96)
+  std::string poisoned;
 };
 
 namespace {
+
+void model_abort(ted_model* M, const std::string& why) {
+  M->poisoned = why;
+  for (ted_layer* L : M->moe)
+    if (L) layer_abort(L, why);
+  for (ncclComm_t* c : {&M->tp_c, &M->dp_c, &M->world_c})
+    if (*c) {
+      ncclCommAbort(*c);
+      *c = nullptr;
+    }
+  throw RuntimeError(why);
+}
+
+// the stack's failure state: its MoE layers' (plane-barrier timeouts, NCCL async errors)
+// and its own communicators' asynchronous errors
+void model_check(ted_model* M) {
+  if (!M->poisoned.empty()) throw RuntimeError(M->poisoned + " (model unusable after the failure)");
+  for (ted_layer* L : M->moe)
+    if (L) {
+      try {
+        layer_check_fault(L);
+      } catch (const std::exception& e) {
+        model_abort(M, e.what());
+      }
+    }
+  for (ncclComm_t c : {M->tp_c, M->dp_c, M->world_c}) {
+    if (!c) continue;
+    ncclResult_t r = ncclSuccess;
+    if (ncclCommGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress)
+      model_abort(M, std::string("NCCL asynchronous error: ") + ncclGetErrorString(r));
+  }
+}
+
+// stream wait that cannot hang (see layer.cu wait_stream)
+void model_wait(ted_model* M, cudaStream_t s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) CU(q);
+    model_check(M);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (M->timeout_s > 0 && el > M->timeout_s && M->world > 1)
+      model_abort(M, "TimeoutError: rank " + std::to_string(M->rank) +
+                         ": the step did not complete within " + std::to_string(M->timeout_s) +
+                         " s (a peer is stalled or gone; collective_timeout)");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  model_check(M);
+}
 
 void dense_params(ted_model* M, int l, bool ffn, int64_t& off) {
   DenseBlock& B = ffn ? M->ffn[size_t(l)] : M->attn[size_t(l)];
@@ -761,6 +815,7 @@ int ted_model_init_params(ted_model* M, uint64_t seed) {
 int ted_model_forward(ted_model* M, const uint16_t* batch, void* stream) {
   return guard([&] {
     require(M && batch, "null argument");
+    model_check(M);
     model_forward(M, reinterpret_cast<const bf16*>(batch), S(stream));
   });
 }
@@ -768,6 +823,7 @@ int ted_model_forward(ted_model* M, const uint16_t* batch, void* stream) {
 int ted_model_backward(ted_model* M, void* stream) {
   return guard([&] {
     require(M != nullptr, "null model");
+    model_check(M);
     model_backward(M, S(stream));
   });
 }
@@ -775,6 +831,7 @@ int ted_model_backward(ted_model* M, void* stream) {
 int ted_model_optimizer_step(ted_model* M, void* stream) {
   return guard([&] {
     require(M != nullptr, "null model");
+    model_check(M);
     model_optimizer(M, S(stream));
   });
 }
@@ -782,6 +839,7 @@ int ted_model_optimizer_step(ted_model* M, void* stream) {
 int ted_model_step(ted_model* M, const uint16_t* batch, void* stream) {
   return guard([&] {
     require(M && batch, "null argument");
+    model_check(M);
     const cudaStream_t s = S(stream);
     model_forward(M, reinterpret_cast<const bf16*>(batch), s);
     model_backward(M, s, /*step_follows=*/true);
@@ -793,7 +851,20 @@ int ted_model_loss(ted_model* M, double* loss, void* stream) {
   return guard([&] {
     require(M && loss, "null argument");
     CU(cudaMemcpyAsync(loss, M->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
-    CU(cudaStreamSynchronize(S(stream)));
+    model_wait(M, S(stream));
+  });
+}
+
+int ted_model_set_timeout(ted_model* M, double seconds) {
+  return guard([&] {
+    require(M != nullptr, "null model");
+    require(seconds >= 0, "timeout must be >= 0 (0 = no limit)");
+    M->timeout_s = seconds;
+    for (ted_layer* L : M->moe)
+      if (L) {
+        const int rc = ted_layer_set_timeout(L, seconds);
+        if (rc != TED_OK) throw RuntimeError(ted_last_error());
+      }
   });
 }
 

@@ -1465,6 +1465,29 @@ cudaError_t colsum_finish(const float* part, int w, const int* seg_off, int G, b
   return cudaGetLastError();
 }
 
+// out[k] = src[pos[k]] (zero row when pos[k] < 0): the un-permute of the dispatch gradient
+// (moe.cpp:661-675) for the standalone operator; one warp per row, 16 B vectors
+__global__ void __launch_bounds__(256) gather_rows_kernel(const bf16* __restrict__ src,
+                                                          const int* __restrict__ pos, int64_t n,
+                                                          int h, bf16* __restrict__ out) {
+  const int64_t k = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (k >= n) return;
+  const int lane = threadIdx.x & 31, vec = h / 8;
+  const int p = pos[k];
+  uint4* dst = reinterpret_cast<uint4*>(out + k * h);
+  for (int i = lane; i < vec; i += 32)
+    dst[i] = p >= 0 ? ldg_stream(src + int64_t(p) * h + i * 8) : make_uint4(0, 0, 0, 0);
+}
+
+cudaError_t gather_rows(const bf16* src, const int* pos, int64_t n, int h, bf16* out,
+                        cudaStream_t s) {
+  if (h % 8 != 0) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  gather_rows_kernel<<<ceil_div(n, 8), 256, 0, s>>>(src, pos, n, h, out);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s) {
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;

@@ -257,31 +257,52 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
 // Plane barrier over NVLink peer memory: thread i publishes `epoch` into slot `me` of
 // member i's flag array (system-scope release after a system fence, so every earlier
 // peer store of this GPU is visible first), then waits until member i's epoch has
-// arrived in this GPU's own array (system-scope acquire).  A member that never arrives
-// turns into a trapped kernel after ~20 s instead of a hung GPU.
+// arrived in this GPU's own array (system-scope acquire).  A member that does not arrive
+// within timeout_ns (the reference's collective_timeout, moe.hpp:96; 0 = wait forever,
+// measured on the global nanosecond timer, independent of the SM clock) is recorded in
+// *fault (1 + its plane rank; host-mapped, read by the host as TimeoutError) and the
+// kernel returns instead of trapping, so the CUDA context survives.  Once a fault is
+// recorded every later barrier returns at once (the step's data are void; the host
+// reports the error at its next call).
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __global__ void plane_barrier_kernel(const unsigned long long* __restrict__ flags, int PS,
-                                     int me, unsigned* __restrict__ epoch_dev) {
+                                     int me, unsigned* __restrict__ epoch_dev,
+                                     int* __restrict__ fault, unsigned long long timeout_ns) {
   // the epoch lives on the device (every member runs the same barrier sequence), so a
   // captured CUDA graph of the step advances it on every replay
   __shared__ unsigned s_epoch;
+  __shared__ int s_fault;
   const int i = threadIdx.x;
   if (i == 0) {
     s_epoch = *epoch_dev + 1;
     *epoch_dev = s_epoch;
+    s_fault = *reinterpret_cast<volatile int*>(fault);
   }
   __threadfence_system();
   __syncthreads();
+  if (s_fault) return;
   const unsigned epoch = s_epoch;
   if (i < PS) {
     unsigned* dst = reinterpret_cast<unsigned*>(flags[i]) + me;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(dst), "r"(epoch) : "memory");
     const unsigned* mine = reinterpret_cast<const unsigned*>(flags[me]) + i;
-    const long long t0 = clock64();
+    const unsigned long long t0 = global_ns();
     unsigned v = 0;
-    while (true) {
+    for (unsigned spin = 0;; ++spin) {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
       if (int(v - epoch) >= 0) break;
-      if (clock64() - t0 > (1ll << 35)) __trap();  // ~20 s at 1.9 GHz: a peer is gone
+      if ((spin & 255) == 255) {
+        if (timeout_ns != 0 && global_ns() - t0 > timeout_ns) {
+          atomicCAS(fault, 0, 1 + i);  // member i never arrived: a peer is gone or stalled
+          __threadfence_system();
+          break;
+        }
+        if (*reinterpret_cast<volatile int*>(fault)) break;  // another slot timed out
+      }
     }
   }
   __syncthreads();
@@ -289,9 +310,11 @@ __global__ void plane_barrier_kernel(const unsigned long long* __restrict__ flag
 }
 
 cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
-                               unsigned* epoch_dev, cudaStream_t s) {
-  if (PS < 1 || PS > 1024) return cudaErrorInvalidValue;
-  plane_barrier_kernel<<<1, ((PS + 31) / 32) * 32, 0, s>>>(flags, PS, me, epoch_dev);
+                               unsigned* epoch_dev, int* fault, unsigned long long timeout_ns,
+                               cudaStream_t s) {
+  if (PS < 1 || PS > 1024 || fault == nullptr) return cudaErrorInvalidValue;
+  plane_barrier_kernel<<<1, ((PS + 31) / 32) * 32, 0, s>>>(flags, PS, me, epoch_dev, fault,
+                                                          timeout_ns);
   count_launch(1);
   return cudaGetLastError();
 }

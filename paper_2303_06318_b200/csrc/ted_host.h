@@ -184,5 +184,9 @@ void layer_backward_then_step(ted_layer* L, const bf16* dy, bf16* da, cudaStream
 // device bytes this layer owns (activations and workspaces, parameters and optimizer
 // state, CAC stash)
 void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int64_t* stash);
+// failure detection of a layer (plane-barrier timeout word, NCCL async errors, an earlier
+// fault): throws RuntimeError("TimeoutError: ...") and aborts the layer's communicators
+void layer_check_fault(ted_layer* L);
+void layer_abort(ted_layer* L, const std::string& why);
 
 }  // namespace ted

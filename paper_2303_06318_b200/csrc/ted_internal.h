@@ -173,9 +173,12 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
                               int h, const PeerDst& dst, const float* scale, bool scale_by_prob,
                               cudaStream_t s);
 // y[k] = prob[k] * row(k), fhome[k] = row(k) (token order, for the backward), loss partials
-// barrier of the EP x TP plane through IPC-mapped flag arrays (flags[r] = member r's array)
+// barrier of the EP x TP plane through IPC-mapped flag arrays (flags[r] = member r's array);
+// a member missing for timeout_ns (0: no limit) sets *fault = 1 + its plane rank and the
+// barrier returns (no trap); with *fault set every barrier returns at once
 cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
-                               unsigned* epoch_dev, cudaStream_t s);
+                               unsigned* epoch_dev, int* fault, unsigned long long timeout_ns,
+                               cudaStream_t s);
 // the peer-exchange plan on the device: seg = [seg_off Eloc+1][valid rows Eloc],
 // disp_base [E], pull_base [Tc][E] from the plane-gathered counts
 cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep, int my_c,
@@ -202,6 +205,9 @@ cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, 
                           cudaStream_t s);
 size_t colsum_part_floats(int w, int G, int max_rows_per_group);
 
+// out[k] = src[pos[k]], zero when pos[k] < 0 (dispatch backward un-permute)
+cudaError_t gather_rows(const bf16* src, const int* pos, int64_t n, int h, bf16* out,
+                        cudaStream_t s);
 // per-block expert histogram from an expert-id array (ted_route without the gate)
 cudaError_t expert_hist(const int* expert, int64_t n, int E, int* blk_hist, cudaStream_t s);
 cudaError_t keep_from_slot(const int* slot, int64_t n, int64_t cap, uint8_t* keep,

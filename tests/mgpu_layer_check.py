@@ -29,6 +29,46 @@ def rel(x, ref):
     return float(np.linalg.norm(x - ref) / max(np.linalg.norm(ref), 1e-30))
 
 
+def stall_check(L, a, y, da, rank, dist):
+    """Failure detection (Fabric's TimeoutError, fabric.cpp:65-96): every rank runs the
+    forward, then rank 0 alone enters the backward while its peers stall.  Rank 0's NVLink
+    plane barrier gives up after the timeout without trapping (the CUDA context survives),
+    its next call reports TimeoutError with status 1, and every later call fails too."""
+    import time
+
+    import torch
+
+    import paper_2303_06318_b200 as ted
+    timeout = 3.0
+    L.set_timeout(timeout)
+    L.forward(a, y)
+    L.loss()
+    if rank == 0:
+        t0 = time.time()
+        L.backward(None, da)
+        try:
+            L.loss()
+            raise AssertionError("a stalled peer was not detected")
+        except ted.TedRuntimeError as e:
+            msg = str(e)
+        waited = time.time() - t0
+        assert "TimeoutError" in msg, msg
+        assert timeout * 0.8 < waited < timeout * 10, waited
+        try:
+            L.forward(a, y)
+            raise AssertionError("a faulted layer accepted another call")
+        except ted.TedRuntimeError as e:
+            assert "TimeoutError" in str(e), str(e)
+        x = torch.ones(4, device="cuda")  # the context is alive
+        assert float((x * 2).sum().item()) == 8.0
+        print("MGPU-OK " + json.dumps({"stall": True, "waited_s": round(waited, 2), "error": msg}))
+    else:
+        time.sleep(timeout + 6)
+    dist.barrier()
+    sys.stdout.flush()
+    os._exit(0)  # the peers' communicators were aborted: skip the destructors
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", type=int, default=2)
@@ -43,6 +83,7 @@ def main():
     ap.add_argument("--ledger", type=int, default=0)
     ap.add_argument("--skew", type=float, default=0.0)
     ap.add_argument("--step-check", type=int, default=0)
+    ap.add_argument("--stall", type=int, default=0)
     args = ap.parse_args()
 
     import torch
@@ -81,6 +122,9 @@ def main():
             L.set_param(f"layer0.expert{e}.{k}", inp[k][e])
     a = torch.from_numpy(inp["a"][shard * n:(shard + 1) * n].astype(np.float32)).cuda().bfloat16()
     y, da = torch.empty_like(a), torch.empty_like(a)
+    if args.stall:
+        stall_check(L, a, y, da, rank, dist)
+        return
     L.forward(a, y)
     L.backward(None, da)
     torch.cuda.synchronize()

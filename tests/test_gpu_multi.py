@@ -134,3 +134,14 @@ def test_step_graph_matches_separate_calls(nproc, tp, ep, dtd):
     out = _run(nproc, "--tp", str(tp), "--ep", str(ep), "--dtd", str(dtd), "--experts", "8",
                "--step-check", "1")
     assert "step-check" in out
+
+
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_two_gpus_stalled_peer_times_out(exchange):
+    """A peer that never reaches the backward: rank 0 gets TimeoutError (status 1) after the
+    collective timeout instead of a hang or a trapped context (fabric.cpp:65-96)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    out = _run(2, "--tp", "2", "--ep", "1", "--dtd", "1", "--experts", "4", "--stall", "1",
+               env={"TED_EXCHANGE": exchange})
+    assert "TimeoutError" in out
