@@ -154,73 +154,167 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ reference arm (CPU)
 
-def ref_sample_plan(w, sample_tokens):
-    """(tokens, experts) of the bounded CPU sample: top-1 routing makes the per-token cost
-    independent of the expert count, so wide layers are sampled with fewer experts (host
-    memory: 4 fp64 weight/gradient tensors per expert) and fewer tokens (10-30 s)."""
+def host_info():
+    """The box's host CPU, for the CPU baselines."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"nproc": os.cpu_count(), "usable_cpus": usable, "cpu_model": model}
+
+
+class pinned:
+    """Pin this process (and the reference's rank threads it spawns) to the first k usable
+    CPUs for one measurement (the taskset of BASELINE.md section 3)."""
+
+    def __init__(self, k):
+        self.k = k
+
+    def __enter__(self):
+        try:
+            self.old = os.sched_getaffinity(0)
+            cpus = sorted(self.old)[:max(1, self.k)]
+            os.sched_setaffinity(0, cpus)
+            self.cpus = cpus
+        except (AttributeError, OSError):
+            self.old, self.cpus = None, None
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
+def ref_sample_plan(w, threads_wanted):
+    """(experts = threads, token counts of the two timed runs) of the bounded CPU sample.
+    Top-1 routing makes the per-token cost independent of the expert count, so wide layers
+    are sampled with few experts (host memory: 4 fp64 weight / gradient tensors each)."""
     h = w["hidden"]
-    if sample_tokens <= 0:
-        sample_tokens = 256 if h <= 1024 else 24
-    return sample_tokens, (w["experts"] if h <= 1024 else min(w["experts"], 2))
+    cap = 4 if h > 1024 else w["experts"]
+    threads = max(1, min(threads_wanted, cap, w["experts"]))
+    per = 2 if h > 1024 else 16
+    return threads, per * threads, 4 * per * threads
 
 
-def reference_tokens_per_s(w, sample_tokens: int, experts: int, reps: int = 1):
-    """Time the unmodified reference (oracle/_ref) on a bounded sample: the MoE branch
-    (gate_forward + per-expert linear/gelu fwd+bwd + gate_backward, one thread per expert)
-    on `sample_tokens` tokens routed over `experts` experts (`reps` timed repetitions,
-    mean), plus OptimizerShard::step_owned on the layer's full parameter count amortised
-    over the full batch."""
+def reference_tokens_per_s(w, threads: int, k_lo: int, k_hi: int):
+    """Time the unmodified reference (oracle/_ref) on a bounded sample of the layer: the
+    MoE branch (gate_forward + per-expert linear/gelu fwd+bwd + gate_backward, one thread
+    per expert, the reference's rank-thread model) on k_lo and on k_hi tokens over `threads`
+    experts; the marginal time per token (the slope, free of the per-expert fixed costs) +
+    OptimizerShard::step_owned over the layer's parameter count (a 4 M-element probe,
+    scaled) amortised over the full batch."""
     import ctypes as C
 
     import numpy as np
 
     from oracle import oracle as O
     R = O.ref()
-    h, E = w["hidden"], experts
-    threads = experts
+    h, E = w["hidden"], threads
     f = 4 * h
     rng = np.random.default_rng(0)
-    a = rng.standard_normal((sample_tokens, h))
     wg = rng.standard_normal((h, E)) / np.sqrt(h)
     w1 = rng.uniform(-1, 1, (E, h, f)) / np.sqrt(h)
     b1 = rng.uniform(-0.1, 0.1, (E, f))
     w2 = rng.uniform(-1, 1, (E, f, h)) / np.sqrt(f)
     b2 = rng.uniform(-0.1, 0.1, (E, h))
-    dy = rng.standard_normal((sample_tokens, h)) / (sample_tokens * 8)
-    y, da = np.empty((sample_tokens, h)), np.empty((sample_tokens, h))
     dwg, dw1, db1 = np.empty((h, E)), np.empty((E, h, f)), np.empty((E, f))
     dw2, db2 = np.empty((E, f, h)), np.empty((E, h))
-    t_layer = 0.0
-    for _ in range(max(1, reps)):
+    times = {}
+    for k in (k_lo, k_hi):
+        a = rng.standard_normal((k, h))
+        dy = rng.standard_normal((k, h)) / (k * 8)
+        y, da = np.empty((k, h)), np.empty((k, h))
         t0 = time.perf_counter()
-        rc = R.ref_moe_sublayer(sample_tokens, h, f, E, a, wg, w1, b1, w2, b2, dy, y, da, dwg,
-                                dw1, db1, dw2, db2, threads)
-        t_layer += time.perf_counter() - t0
+        rc = R.ref_moe_sublayer(k, h, f, E, a, wg, w1, b1, w2, b2, dy, y, da, dwg, dw1, db1,
+                                dw2, db2, threads)
+        times[k] = time.perf_counter() - t0
         assert rc == 0, R.ref_last_error()
-    t_layer /= max(1, reps)
-    # optimizer over a slice of the family, scaled to the layer's parameter count
+    per_token_layer = max(times[k_hi] - times[k_lo], 1e-9) / (k_hi - k_lo)
     params = w["experts"] * (2 * h * f + f + h) + h * w["experts"]
-    probe = min(params, 4_000_000)
-    vals = rng.standard_normal(probe)
-    grads = rng.standard_normal(probe)
-    out, m, m1, m2 = (np.empty(probe) for _ in range(4))
+    t_probe, probe = ref_step_owned(min(params, 4_000_000))
+    t_adam = t_probe * params / probe
+    per_token = per_token_layer + t_adam / w["tokens"]
+    return 1.0 / per_token, {"layer_s": times, "per_token_layer_s": per_token_layer,
+                             "adam_s_extrapolated": t_adam, "adam_probe_elems": probe}
+
+
+def ref_step_owned(elems: int):
+    """OptimizerShard::step_owned (optimizer.cpp:58-104) over `elems` owned elements, tile
+    1.8 M (TileConfig default), 1 thread: seconds."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as O
+    R = O.ref()
+    rng = np.random.default_rng(1)
+    vals = rng.standard_normal(elems)
+    grads = rng.standard_normal(elems)
+    out, m, m1, m2 = (np.empty(elems) for _ in range(4))
     pk = C.c_uint64()
     t0 = time.perf_counter()
-    R.ref_adam(probe, vals, 1, 0, 1e-4, 0.9, 0.999, 1e-8, 0.01, 1, 1_800_000, 1, grads, out, m,
+    R.ref_adam(elems, vals, 1, 0, 1e-4, 0.9, 0.999, 1e-8, 0.01, 1, 1_800_000, 1, grads, out, m,
                m1, m2, C.byref(pk))
-    t_adam = (time.perf_counter() - t0) * params / probe
-    per_token = t_layer / sample_tokens + t_adam / w["tokens"]
-    return 1.0 / per_token, t_layer, t_adam
+    return time.perf_counter() - t0, elems
+
+
+def reference_entry_points():
+    """the reference's own entry points on this host, each pinned to
+    as many CPUs as it has rank threads -- SerialModel::step at C1 (1 thread), Trainer::step
+    at the reference-expressible (8,2,4) and (4,2,2) layouts (world-size threads, DTD on),
+    OptimizerShard::step_owned at 16.8 M elements."""
+    import numpy as np
+
+    from oracle import oracle as O
+    R = O.ref()
+    out = {}
+    losses = np.zeros(1)
+    with pinned(1) as pn:
+        t0 = time.perf_counter()
+        assert R.ref_serial_step(1, 256, 4, 1024, 1, 2, 1, losses) == 0, R.ref_last_error()
+        dt = time.perf_counter() - t0
+    out["serial_model_c1"] = {"config": "SerialModel::step, d=256, ffn=1024, E=4, 2 shards x "
+                                        "1024 tokens, 1 MoE layer", "threads": 1,
+                              "cpus": pn.cpus, "s_per_step": dt, "tokens_per_s": 2048 / dt}
+    for world, tp, ep, n in ((8, 2, 4, 512), (4, 2, 2, 1024)):
+        for dtd in (1,):
+            a2a, ag = O.C.c_uint64(), O.C.c_uint64()
+            with pinned(world) as pn:
+                t0 = time.perf_counter()
+                rc = R.ref_trainer_step(1, 256, ep, n, 1, world, tp, dtd, 0, 0, 1, losses,
+                                        O.C.byref(a2a), O.C.byref(ag))
+                dt = time.perf_counter() - t0
+            assert rc == 0, R.ref_last_error()
+            tokens = n * (world // tp)
+            out[f"trainer_{world}_{tp}_{ep}_dtd{dtd}"] = {
+                "config": f"Trainer::step world {world}, T={tp}, E={ep}, {n} tokens/shard, "
+                          f"d=256, DTD {'on' if dtd else 'off'}", "threads": world,
+                "cpus": pn.cpus, "s_per_step": dt, "tokens_per_s": tokens / dt,
+                "ledger_a2a_bytes_fwd": a2a.value, "ledger_ag_bytes_fwd": ag.value}
+    with pinned(1) as pn:
+        t, el = ref_step_owned(16_800_000)
+    out["step_owned"] = {"elements": el, "tile": 1_800_000, "threads": 1, "cpus": pn.cpus,
+                         "s": t, "melem_per_s": el / t / 1e6}
+    return out
 
 
 def run_reference(args, w, rank, world):
     if rank != 0:
         return
-    sample, threads = ref_sample_plan(w, args.ref_sample)
-    # one bounded sample per timed step, capped so the whole run stays within minutes
-    reps = max(1, min(args.steps, 3 if w["hidden"] > 1024 else 5))
-    tps, t_layer, t_adam = reference_tokens_per_s(w, sample, threads, reps)
+    hi = host_info()
+    threads, k_lo, k_hi = ref_sample_plan(w, hi["usable_cpus"] or 1)
+    tps, det = reference_tokens_per_s(w, threads, k_lo, k_hi)
     ms = w["tokens"] / tps * 1e3
+    entry = reference_entry_points() if not args.no_entry_points else None
     line = {
         "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -230,15 +324,42 @@ def run_reference(args, w, rank, world):
         "config": {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
                    "experts": w["experts"], "tokens": w["tokens"], "capacity_factor": None},
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
-                         "sample": f"{sample} tokens through the reference MoE branch "
-                                   f"({t_layer:.2f} s mean of {reps} timed repetitions, "
-                                   f"{threads} expert threads) + "
-                                   f"step_owned over the layer's parameters ({t_adam:.2f} s, "
-                                   f"1 thread) amortised over {w['tokens']} tokens"},
+                         "host": hi,
+                         "sample": f"extrapolated: the reference MoE branch on {k_lo} and "
+                                   f"{k_hi} tokens over {threads} experts ({threads} expert "
+                                   f"threads; {det['layer_s'][k_lo]:.2f} s / "
+                                   f"{det['layer_s'][k_hi]:.2f} s, marginal "
+                                   f"{det['per_token_layer_s']:.3f} s per token) + step_owned "
+                                   f"over the layer's parameters ({det['adam_s_extrapolated']:.1f}"
+                                   f" s, from a {det['adam_probe_elems']}-element probe) "
+                                   f"amortised over {w['tokens']} tokens"},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if entry is not None:
+        line["reference_entry_points"] = entry
     print(json.dumps(line), flush=True)
+
+
+def nvlink_bytes(gpu: int):
+    """(tx, rx) NVLink data bytes of this GPU so far (NVML throughput counters, all links),
+    or None when NVML does not expose them."""
+    try:
+        import pynvml as N
+        N.nvmlInit()
+        hd = N.nvmlDeviceGetHandleByIndex(gpu)
+        vals = N.nvmlDeviceGetFieldValues(hd, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                               N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
+        if any(v.nvmlReturn != 0 for v in vals):
+            return None
+        return tuple(int(v.value.ullVal) * 1024 for v in vals)  # KiB counters
+    except Exception:
+        return None
+
+
+def ted_switches():
+    """The TED_* environment switches in effect (A/B knobs that change code paths)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("TED_")}
 
 
 # ------------------------------------------------------------------ our arm
@@ -291,6 +412,7 @@ def run_ours(args, w, rank, world, local_rank, dist):
     barrier()
     torch.cuda.synchronize()
     launches0 = ted.kernel_launches()
+    nv0 = nvlink_bytes(local_rank) if world > 1 else None
     with ClockSampler(local_rank) as clk:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -300,6 +422,7 @@ def run_ours(args, w, rank, world, local_rank, dist):
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue cost per step
         ev1.record(stream)
         torch.cuda.synchronize()
+    nv1 = nvlink_bytes(local_rank) if world > 1 else None
     ms = ev0.elapsed_time(ev1) / args.steps
     launches = (ted.kernel_launches() - launches0) // max(args.steps, 1)
     # per-stage CUDA events (event nodes inside the captured step on one GPU) for the
@@ -355,60 +478,98 @@ def run_ours(args, w, rank, world, local_rank, dist):
     torch.cuda.synchronize()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
 
-    # DTD on vs off on the same workload (all-to-all bytes and time reported separately)
+    # DTD on vs off, on both exchange implementations, on the same workload: step time,
+    # the all-to-all and the DTD all-gather times separately (the peer exchange's fused
+    # scatter is split into its two parts in the timed pass), the reference's ledger bytes
+    # and the NVLink bytes NVML counts (rank 0)
     dtd_cmp = None
     if world > 1 and T > 1 and not args.no_dtd_compare:
-        def exch_ms(st):
-            keys = ["dispatch_peer", "combine_pull", "combine_bwd", "gate_dx", "barrier", "count_exchange",
-                    "a2a_fwd", "ag_fwd", "a2a_ret_fwd", "ag_home_fwd", "a2a_bwd", "ag_bwd",
-                    "a2a_ret_bwd", "ag_home_bwd", "tp_allreduce_fwd", "tp_allreduce_bwd"]
-            return {k: round(v, 4) for k, v in st.items() if k in keys}
-        arms = {}
-        for dtd_flag in (w["dtd"], not w["dtd"]):
-            if dtd_flag == w["dtd"]:
-                Lx, stx, ms_x = L, stages, ms
-            else:
-                L.close()
-                obj = [ted.nccl_unique_id() if rank == 0 else None]  # a fresh id per communicator
-                dist.broadcast_object_list(obj, src=0)
-                Lx = ted.MoeLayer(model, topo, ted.RunFlags(dtd=dtd_flag), capacity_factor=w["cf"],
-                                  rank=rank, nccl_uid=obj[0])
-                Lx.init_params(1234)
-                for _ in range(3):
-                    Lx.step(a, y, da)
-                torch.cuda.synchronize()
-                barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                kx = max(1, min(args.steps, 10))
-                e0.record(stream)
-                for _ in range(kx):
-                    Lx.step(a, y, da)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                ms_x = max_over_ranks(e0.elapsed_time(e1) / kx)
-                Lx.timing(True)
-                for _ in range(kx):
-                    Lx.step(a, y, da)
-                torch.cuda.synchronize()
-                stx = {k: v[0] / kx for k, v in Lx.timing_read().items()}
-                Lx.timing(False)
-                barrier()
-            if dtd_flag == w["dtd"]:
-                stx = {k: v[0] / nprof for k, v in stx.items()}
-            sx = Lx.stats()
-            ex = exch_ms(stx)
-            arms["dtd_on" if dtd_flag else "dtd_off"] = {
-                "ms_per_step": ms_x, "tokens_per_s": w["tokens"] / (ms_x / 1e3),
-                "a2a_bytes_fwd_rank0_ledger": sx["a2a_bytes_fwd"],
-                "a2a_rows_offrank_rank0": sx["a2a_rows_offrank"],
-                "dtd_allgather_bytes_fwd_rank0_ledger": sx["ag_bytes_fwd"],
-                "nvlink_bytes_fwd_rank0": sx["peer_bytes_fwd"],
-                "exchange_ms_rank0": ex, "exchange_ms_total_rank0": round(sum(ex.values()), 4),
-                "stage_ms_rank0": {k: round(v, 4) for k, v in sorted(stx.items())}}
-            if Lx is not L:
-                Lx.close()
-        dtd_cmp = arms
+        L.close()
         L = None
+        kx = max(3, min(args.steps, 10))
+        exchanges = ["peer"] + (["nccl"] if args.exchange_compare else [])
+        saved = os.environ.get("TED_EXCHANGE")
+
+        def arm(ex, dtd_flag):
+            os.environ["TED_EXCHANGE"] = ex
+            obj = [ted.nccl_unique_id() if rank == 0 else None]  # a fresh id per layer
+            dist.broadcast_object_list(obj, src=0)
+            Lx = ted.MoeLayer(model, topo, ted.RunFlags(dtd=dtd_flag), capacity_factor=w["cf"],
+                              rank=rank, nccl_uid=obj[0])
+            Lx.init_params(1234)
+            for _ in range(3):
+                Lx.step(a, y, da)
+            torch.cuda.synchronize()
+            barrier()
+            nv0 = nvlink_bytes(local_rank)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            Lx.ledger(reset=True)
+            e0.record(stream)
+            for _ in range(kx):
+                Lx.step(a, y, da)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            nv1 = nvlink_bytes(local_rank)
+            led = Lx.ledger(reset=True)
+            ms_x = max_over_ranks(e0.elapsed_time(e1) / kx)
+            barrier()
+            Lx.timing(True)
+            for _ in range(kx):
+                Lx.step(a, y, da)
+            torch.cuda.synchronize()
+            stx = {k: v[0] / kx for k, v in Lx.timing_read().items()}
+            Lx.timing(False)
+            barrier()
+            Lx.close()
+
+            def g(*keys):
+                return round(sum(stx.get(k, 0.0) for k in keys), 4)
+            if ex == "peer":
+                a2a, ag = g("dispatch_a2a"), g("dispatch_ag")
+                ret = g("combine_pull")
+                total = g("dispatch_a2a", "dispatch_ag", "combine_pull", "combine_bwd", "gate_dx",
+                          "barrier", "count_exchange")
+            else:
+                a2a, ag = g("a2a_fwd"), g("ag_fwd")
+                ret = g("tp_allreduce_fwd", "a2a_ret_fwd", "ag_home_fwd")
+                total = g("count_exchange", "a2a_fwd", "ag_fwd", "tp_allreduce_fwd", "a2a_ret_fwd",
+                          "ag_home_fwd", "a2a_bwd", "ag_bwd", "tp_allreduce_bwd", "a2a_ret_bwd",
+                          "ag_home_bwd")
+
+            def per_step(key):
+                return led.get(key, {}).get("payload_bytes", 0) // kx
+            return {
+                "ms_per_step": ms_x, "tokens_per_s": w["tokens"] / (ms_x / 1e3),
+                "a2a_ms_fwd_rank0": a2a, "dtd_allgather_ms_fwd_rank0": ag,
+                "return_ms_fwd_rank0": ret, "exchange_ms_total_rank0": total,
+                "ledger_bytes_per_step_rank0": {
+                    "a2a_fwd": per_step("forward.all_to_all"),
+                    "allgather_fwd": per_step("forward.all_gather"),
+                    "allreduce_fwd": per_step("forward.all_reduce"),
+                    "a2a_bwd": per_step("backward.all_to_all")},
+                "nvlink_tx_bytes_per_step_rank0_nvml":
+                    (nv1[0] - nv0[0]) // kx if nv0 and nv1 else None,
+                "stage_ms_rank0": {k: round(v, 4) for k, v in sorted(stx.items())}}
+
+        arms = {}
+        try:
+            for ex in exchanges:
+                for dtd_flag in (True, False):
+                    arms[f"{ex}_dtd_{'on' if dtd_flag else 'off'}"] = arm(ex, dtd_flag)
+        finally:
+            if saved is None:
+                os.environ.pop("TED_EXCHANGE", None)
+            else:
+                os.environ["TED_EXCHANGE"] = saved
+        for ex in exchanges:
+            on, off = arms[f"{ex}_dtd_on"], arms[f"{ex}_dtd_off"]
+            arms[f"{ex}_dtd_ratio_off_over_on"] = {
+                "a2a_ms_fwd": round(off["a2a_ms_fwd_rank0"] / on["a2a_ms_fwd_rank0"], 3)
+                if on["a2a_ms_fwd_rank0"] else None,
+                "a2a_ledger_bytes": round(off["ledger_bytes_per_step_rank0"]["a2a_fwd"] /
+                                          max(1, on["ledger_bytes_per_step_rank0"]["a2a_fwd"]), 3),
+                "step_ms": round(off["ms_per_step"] / on["ms_per_step"], 3)}
+        dtd_cmp = arms
     if rank != 0:
         if L is not None:
             L.close()
@@ -484,6 +645,7 @@ def run_ours(args, w, rank, world, local_rank, dist):
                        "step's tokens copied under this step); loss read back every step"},
         "routing": {"dropped_tokens_rank0": stats["dropped"], "loss_rank0": loss},
         "clocks": clk.summary(),
+        "switches": ted_switches(),
     }
     if dtd_cmp is not None:
         line["dtd_compare"] = dtd_cmp
@@ -493,17 +655,27 @@ def run_ours(args, w, rank, world, local_rank, dist):
                         "peer_exchange": bool(stats["peer_exchange"]),
                         "a2a_rows_offrank_rank0": stats["a2a_rows_offrank"],
                         "ag_bytes_fwd_rank0": stats["ag_bytes_fwd"],
-                        "ar_bytes_fwd_rank0": stats["ar_bytes_fwd"]}
+                        "ar_bytes_fwd_rank0": stats["ar_bytes_fwd"],
+                        "nvlink_tx_bytes_per_step_rank0_nvml":
+                            (nv1[0] - nv0[0]) // args.steps if nv0 and nv1 else None,
+                        "nvlink_rx_bytes_per_step_rank0_nvml":
+                            (nv1[1] - nv0[1]) // args.steps if nv0 and nv1 else None}
     if not args.no_cpu_baseline and world == 1:
-        sample, nexp = ref_sample_plan(w, args.ref_sample)
-        tps, t_layer, t_adam = reference_tokens_per_s(w, sample, nexp)
-        line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": nexp,
-                                "kind": "reference",
-                                "sample": f"{sample} tokens over {nexp} experts through the "
-                                          f"reference MoE branch ({t_layer:.2f} s, {nexp} "
-                                          f"expert threads) + step_owned over the layer's "
-                                          f"{w['experts']} experts' parameters "
-                                          f"({t_adam:.2f} s) amortised over {w['tokens']} tokens"}
+        # a single reference rank-thread on a bounded sample (the reference arm,
+        # --impl reference, uses the host's cores)
+        threads, k_lo, k_hi = ref_sample_plan(w, 1)
+        with pinned(threads):
+            tps, det = reference_tokens_per_s(w, threads, k_lo, k_hi)
+        line["cpu_baseline"] = {
+            "value": tps, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "host": host_info(),
+            "sample": f"extrapolated: the reference MoE branch on {k_lo} and {k_hi} tokens "
+                      f"over {threads} expert(s) ({det['layer_s'][k_lo]:.2f} s / "
+                      f"{det['layer_s'][k_hi]:.2f} s: marginal {det['per_token_layer_s']:.3f} s "
+                      f"per token, {threads} thread(s) pinned) + step_owned over the layer's "
+                      f"parameters ({det['adam_s_extrapolated']:.1f} s from a "
+                      f"{det['adam_probe_elems']}-element probe) amortised over "
+                      f"{w['tokens']} tokens"}
     if world == 1 and w["name"].startswith("C3") and not args.no_c2:
         line["c2_single_gpu"] = quick_layer_bench(workload(1, False, "c2"), 200, 10)
     print(json.dumps(line), flush=True)
@@ -580,7 +752,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtd", type=int, default=1)
-    ap.add_argument("--ref-sample", type=int, default=0, help="0: automatic (10-30 s)")
+    ap.add_argument("--no-entry-points", action="store_true",
+                    help="reference arm: skip BASELINE.md section 3's entry points (~1 min)")
+    ap.add_argument("--exchange-compare", type=int, default=1,
+                    help="N>1: also time the NCCL send/recv exchange (DTD on and off)")
     ap.add_argument("--workload", default="c3", choices=["c3", "c2", "c4"])
     ap.add_argument("--layers", type=int, default=2, help="c4: layers of the stack")
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] side line")

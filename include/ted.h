@@ -283,6 +283,22 @@ typedef struct {
 } ted_layer_stats;
 int ted_layer_get_stats(ted_layer* L, ted_layer_stats* out);
 
+/* The reference's communication ledger (CommLedger, ledger.hpp:46-77; accounting of
+ * fabric.cpp:163-287 and predict_comm_volume, cost_model.cpp:346-416) of this rank:
+ * out[phase * TED_LEDGER_OPS + op] for phases Forward, Recompute, Backward, GradSync, Optim
+ * and ops AllReduce, AllGather, AllToAll (types.hpp:32-40).  Each entry counts the
+ * collectives the reference runs for the same data -- calls (+1 per collective this rank
+ * joins) and this rank's payload bytes (2-byte elements; summing over ranks gives the
+ * reference's group totals) -- whatever the exchange implementation (the NVLink kernels
+ * fold several of them into one).  reset = 1 zeroes it after reading. */
+#define TED_LEDGER_PHASES 5
+#define TED_LEDGER_OPS 3
+typedef struct {
+  uint64_t calls;
+  uint64_t payload_bytes;
+} ted_ledger_entry;
+int ted_layer_ledger(ted_layer* L, ted_ledger_entry* out, int reset);
+
 /* Live per-stage timing with CUDA events recorded on the launching stream (negligible
  * overhead; for bench.py's roofline).  enable resets the accumulators.  read returns
  * JSON {"stage": [total_ms, intervals], ...} and synchronises the device. */
@@ -333,6 +349,9 @@ int ted_model_optimizer_step(ted_model* M, void* stream);
 int ted_model_loss(ted_model* M, double* loss, void* stream);
 /* ted_layer_set_timeout for the stack (its MoE layers and its own communicators) */
 int ted_model_set_timeout(ted_model* M, double seconds);
+/* ted_layer_ledger of the whole stack: the MoE layers' entries plus the dense blocks' TP
+ * all-reduces, the dense family's grad sync and ZeRO-1 completion */
+int ted_model_ledger(ted_model* M, ted_ledger_entry* out, int reset);
 /* last layer's output (tokens_per_shard x hidden bf16, device) */
 int ted_model_output(ted_model* M, uint16_t* y, void* stream);
 /* device memory of this rank (MemoryReport, moe.hpp / moe.cpp:746-757), bytes:

@@ -144,6 +144,8 @@ _sig("ted_layer_optimizer_step", _i32, [_vp, _vp])
 _sig("ted_layer_step", _i32, [_vp, _vp, _vp, _vp, _vp])
 _sig("ted_layer_loss", _i32, [_vp, C.POINTER(_dbl), _vp])
 _sig("ted_layer_set_timeout", _i32, [_vp, _dbl])
+_sig("ted_layer_ledger", _i32, [_vp, _vp, _i32])
+_sig("ted_model_ledger", _i32, [_vp, _vp, _i32])
 _sig("ted_ops_reserve", _i32, [C.c_size_t, _vp])
 _sig("ted_ops_release", _i32, [])
 _sig("ted_dispatch_rows_bound", _i64, [_i64, _i32, _i64])
@@ -195,10 +197,26 @@ EXPORTED = [
     "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
     "ted_model_get_param", "ted_model_get_grad", "ted_model_init_params", "ted_model_keep_grads", "ted_model_step",
     "ted_model_forward", "ted_model_backward", "ted_model_optimizer_step", "ted_model_loss",
-    "ted_model_set_timeout", "ted_ops_reserve", "ted_ops_release", "ted_dispatch_rows_bound",
+    "ted_model_set_timeout", "ted_layer_ledger", "ted_model_ledger", "ted_ops_reserve", "ted_ops_release", "ted_dispatch_rows_bound",
     "ted_dispatch_forward", "ted_dispatch_backward", "ted_combine_forward", "ted_combine_backward",
     "ted_gate_backward_dlogits", "ted_expert_ffn_forward", "ted_expert_ffn_backward",
     "ted_model_output", "ted_model_memory"]
+
+
+LEDGER_PHASES = ("forward", "recompute", "backward", "grad_sync", "optim")  # types.hpp:32
+LEDGER_OPS = ("all_reduce", "all_gather", "all_to_all")  # types.hpp:39
+
+
+def _ledger(fn, h, reset):
+    buf = (C.c_uint64 * 30)()
+    _check(fn(h, C.cast(buf, _vp), int(reset)))
+    out = {}
+    for ph, pn in enumerate(LEDGER_PHASES):
+        for op, on in enumerate(LEDGER_OPS):
+            calls, byts = buf[(ph * 3 + op) * 2], buf[(ph * 3 + op) * 2 + 1]
+            if calls or byts:
+                out[f"{pn}.{on}"] = {"calls": int(calls), "payload_bytes": int(byts)}
+    return out
 
 
 def lib():
@@ -582,6 +600,10 @@ class MoeLayer:
         _check(_lib.ted_layer_loss(self._h, C.byref(v), _stream(stream)))
         return v.value
 
+    def ledger(self, reset: bool = False) -> dict:
+        """This rank's CommLedger entries {"<phase>.<op>": {calls, payload_bytes}}."""
+        return _ledger(_lib.ted_layer_ledger, self._h, reset)
+
     def set_timeout(self, seconds: float):
         """collective_timeout (moe.hpp:96): a stalled peer raises TedRuntimeError
         ("TimeoutError: ...") at the next call instead of hanging or trapping."""
@@ -717,6 +739,9 @@ class TedModel:
 
     def set_timeout(self, seconds: float):
         _check(_lib.ted_model_set_timeout(self._h, float(seconds)))
+
+    def ledger(self, reset: bool = False) -> dict:
+        return _ledger(_lib.ted_model_ledger, self._h, reset)
 
     def output(self, y, stream=None):
         _check(_lib.ted_model_output(self._h, _p(y), _stream(stream)))

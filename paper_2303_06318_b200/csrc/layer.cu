@@ -56,6 +56,13 @@ struct ted_layer {
   int T = 1, P = 1, D = 1;  // tensor, expert-parallel, expert-data degrees
   int t = 0, ep = 0, d = 0;
   int n = 0, h = 0, E = 0, f = 0, fT = 0, Eloc = 1, Tc = 1;
+  // Shapes below the tensor-core tiles (the reference's own verify sweep runs hidden = 8):
+  // the layer computes on h and fT zero-padded to multiples of 256 (padded weight rows /
+  // columns, biases and optimizer state stay exactly zero, so every result is the
+  // unpadded one); hu / fTu are the reference's shapes, io_h the width of the caller's
+  // token buffers (hu for ted_layer_create, the padded h inside a padded model stack).
+  int hu = 0, fTu = 0, io_h = 0;
+  DevBuf<bf16> pad_a, pad_y, pad_dy, pad_da;  // [n][h] staging when io_h != h
   bool dtd = false, local = true;
   int64_t cap = 0;
   int my_chunk = -1;
@@ -85,6 +92,13 @@ struct ted_layer {
   int* fault_d = nullptr;  // device view
   double timeout_s = 120.0;
   std::string poisoned;
+  // the reference's CommLedger (ledger.hpp:46-77) of this rank: [phase][op][calls, bytes],
+  // phases Forward, Recompute, Backward, GradSync, Optim, ops AllReduce, AllGather,
+  // AllToAll (types.hpp:32-40).  The routing-dependent MoE entries accumulate on the
+  // device (one tiny kernel per pass, graph-safe), the static ones on the host.
+  DevBuf<unsigned long long> led;
+  unsigned long long led_host[5][3][2] = {};
+  int ledger_phase = 0;  // Forward, or Recompute while a model stack recomputes
   // peer exchange with the plan built on the device (no host round trip per step, so the
   // multi-GPU step is graph-capturable); the host plan is rebuilt lazily for statistics
   bool devplan = false;
@@ -101,6 +115,7 @@ struct ted_layer {
   DevBuf<double> loss;
   DevBuf<int> verdict;  // placement verdict: [0] last forward, [1] sticky (moe.cpp:537-556)
   HostBuf<int> h_kc_all, h_seg;
+  HostBuf<double> h_loss;
   // activations
   DevBuf<bf16> x_asm, z, hbuf, fe_asm, xsend, fhome, dfe_send, dfe_asm, dx_home, dx_asm;
   ted_layer* share = nullptr;     // activation buffers borrowed from this layer (ckpt)
@@ -182,15 +197,16 @@ namespace {
 struct ParamLoc {
   Family* fam;
   int64_t off;       // element offset of the local shard in the family
-  int64_t rows, cols;  // local shard shape (rows=1 for vectors)
+  int64_t rows, cols;  // local shard shape (rows=1 for vectors), the reference's shape
   int64_t full_rows, full_cols;
   int axis;  // 0 none, 1 column, 2 row
   double scale;
+  int64_t ld;  // row stride in the family (>= cols: zero-padded columns)
 };
 
 bool lookup(ted_layer* L, const std::string& name, ParamLoc& out) {
   if (name == "layer0.gate.w") {
-    out = {&L->fam_non, 0, L->h, L->E, L->h, L->E, 0, 1.0 / std::sqrt(double(L->h))};
+    out = {&L->fam_non, 0, L->hu, L->E, L->hu, L->E, 0, 1.0 / std::sqrt(double(L->hu)), L->E};
     return true;
   }
   const std::string pre = "layer0.expert";
@@ -203,11 +219,12 @@ bool lookup(ted_layer* L, const std::string& name, ParamLoc& out) {
   if (e / L->Eloc != L->ep) return false;  // not housed on this rank
   const int le = e % L->Eloc;
   const int64_t base = int64_t(le) * L->per_expert;
-  const double sin = 1.0 / std::sqrt(double(L->h)), sout = 1.0 / std::sqrt(double(L->f));
-  if (leaf == "w1") out = {&L->fam_exp, base + L->off_w1, L->h, L->fT, L->h, L->f, 1, sin};
-  else if (leaf == "b1") out = {&L->fam_exp, base + L->off_b1, 1, L->fT, 1, L->f, 1, 0.1};
-  else if (leaf == "w2") out = {&L->fam_exp, base + L->off_w2, L->fT, L->h, L->f, L->h, 2, sout};
-  else if (leaf == "b2") out = {&L->fam_exp, base + L->off_b2, 1, L->h, 1, L->h, 0, 0.1};
+  const double sin = 1.0 / std::sqrt(double(L->hu)), sout = 1.0 / std::sqrt(double(L->f));
+  const int hu = L->hu, fTu = L->fTu;
+  if (leaf == "w1") out = {&L->fam_exp, base + L->off_w1, hu, fTu, hu, L->f, 1, sin, L->fT};
+  else if (leaf == "b1") out = {&L->fam_exp, base + L->off_b1, 1, fTu, 1, L->f, 1, 0.1, L->fT};
+  else if (leaf == "w2") out = {&L->fam_exp, base + L->off_w2, fTu, hu, L->f, hu, 2, sout, L->h};
+  else if (leaf == "b2") out = {&L->fam_exp, base + L->off_b2, 1, hu, 1, hu, 0, 0.1, L->h};
   else return false;
   return true;
 }
@@ -219,8 +236,9 @@ bool state_blocked(const ted_layer* L, const ParamLoc& pl) {
 
 
 __global__ void init_family_kernel(bf16* param, float* master, int64_t begin, int64_t end,
-                                   int64_t off, int64_t rows, int64_t cols, int64_t full_cols,
-                                   int64_t col0, uint64_t seed, float scale, int blocked) {
+                                   int64_t off, int64_t rows, int64_t cols, int64_t ld,
+                                   int64_t full_cols, int64_t col0, uint64_t seed, float scale,
+                                   int blocked) {
   const int64_t n = rows * cols;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -231,9 +249,9 @@ __global__ void init_family_kernel(bf16* param, float* master, int64_t begin, in
     z ^= z >> 31;
     const float u = float(z >> 40) * (1.0f / 16777216.0f);
     const float v = (2.f * u - 1.f) * scale;
-    param[off + i] = __float2bfloat16(v);
-    const int64_t fi = off + i;
-    if (blocked) master[off + blk_off(r, c, cols)] = v;  // unsharded family (begin == 0)
+    const int64_t fi = off + r * ld + c;  // padded columns (c >= cols) stay zero
+    param[fi] = __float2bfloat16(v);
+    if (blocked) master[off + blk_off(r, c, ld)] = v;  // unsharded family (begin == 0)
     else if (fi >= begin && fi < end) master[fi - begin] = v;
   }
 }
@@ -355,6 +373,30 @@ void wait_stream(ted_layer* L, cudaStream_t s) {
   check_fault(L);
 }
 
+// ledger entries of this pass's MoE collectives (see ledger_moe_pass_kernel)
+void ledger_pass(ted_layer* L, int phase, cudaStream_t s) {
+  if (L->local) return;
+  check(ledger_moe_pass(L->led.p, phase, L->P, L->T, L->dtd ? 1 : 0, L->Tc, L->E, L->Eloc, L->t,
+                        L->ep, L->kc.p, L->kc_all.p, L->direct ? L->T : 1, L->seg_valid_view,
+                        L->hu, s),
+        "ledger_moe_pass");
+}
+
+// grad sync + ZeRO-1 completion entries (static sizes, moe.cpp:699-734)
+void ledger_host_optim(ted_layer* L) {
+  // the reference's family sizes (zero padding of small shapes excluded)
+  const int64_t exp_u = int64_t(L->Eloc) * (2 * int64_t(L->hu) * L->fTu + L->fTu + L->hu);
+  const int64_t non_u = int64_t(L->hu) * L->E;
+  auto add = [&](int phase, int op, int64_t elems) {
+    L->led_host[phase][op][0] += 1;
+    L->led_host[phase][op][1] += uint64_t(elems) * 2;
+  };
+  if (L->D > 1) add(3, 0, exp_u);
+  if (L->P * L->D > 1) add(3, 0, non_u);
+  if (L->fam_exp.group > 1) add(4, 1, (exp_u + L->fam_exp.group - 1) / L->fam_exp.group);
+  if (L->fam_non.group > 1) add(4, 1, (non_u + L->fam_non.group - 1) / L->fam_non.group);
+}
+
 const unsigned long long* peer_table(ted_layer* L, int which) {
   return L->peer_tab.p + size_t(which) * L->plane_size;
 }
@@ -474,7 +516,7 @@ void layer_forward_replay(ted_layer* L, const bf16* a, cudaStream_t s) {
   L->have_forward = true;
 }
 
-void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
+void layer_forward_impl(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   if (L->fwd_mode == FWD_REPLAY && !L->local) {
     layer_forward_replay(L, a, s);
     return;
@@ -532,7 +574,6 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(plan_peer(L->kc_all.p, L->T, L->P, E, L->Tc, L->ep, L->dtd ? L->t : 0, L->seg_off.p,
                     L->disp_base.p, L->disp_base.p + E, s),
           "plan_peer");
-    L->mark("dispatch_peer", s);
     PeerDst pd;
     pd.peers = peer_table(L, 0);
     pd.disp_base = L->disp_base.p;
@@ -542,8 +583,25 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     pd.my_t = L->t;
     pd.all_replicas = L->dtd ? 1 : 0;
     pd.clamp_rows = peer_clamp(L);
-    check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
-          "scatter_rows_peer");
+    if (L->timing) {
+      // timed pass: the fused scatter as two launches, the reference's all-to-all (rows to
+      // replica my_t of each expert rank) and, with DTD, its TP all-gather (the other
+      // replicas), so their times are reported separately
+      L->mark("dispatch_a2a", s);
+      pd.part = 1;
+      check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
+            "scatter_rows_peer");
+      if (L->dtd) {
+        L->mark("dispatch_ag", s);
+        pd.part = 2;
+        check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
+              "scatter_rows_peer");
+      }
+    } else {
+      L->mark("dispatch_peer", s);
+      check(scatter_rows_peer(a, L->pos_send.p, L->expert.p, L->n, h, pd, nullptr, false, s),
+            "scatter_rows_peer");
+    }
     L->mark("barrier", s);
     plane_barrier(L, s);
     L->mark("zero_pad", s);
@@ -620,6 +678,7 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     rows = asm_rows_bound(L);
   }
 
+  ledger_pass(L, L->ledger_phase, s);
   if (L->fwd_mode == FWD_RECORD && !L->local) {  // CAC: stash the exchanged expert rows
     stash_alloc(L);
     L->stash_rows = rows;
@@ -701,6 +760,23 @@ void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
 
 namespace {
 
+// [n][w_src] -> [n][w_dst] rows (the zero-padded staging of small shapes)
+void copy_rows_2d(bf16* dst, int w_dst, const bf16* src, int w_src, int64_t n, cudaStream_t s) {
+  check(cudaMemcpy2DAsync(dst, size_t(w_dst) * 2, src, size_t(w_src) * 2,
+                          size_t(std::min(w_dst, w_src)) * 2, size_t(n), cudaMemcpyDeviceToDevice, s),
+        "pad copy");
+}
+
+void layer_forward(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
+  if (L->io_h == L->h) {
+    layer_forward_impl(L, a, y, s);
+    return;
+  }
+  copy_rows_2d(L->pad_a.p, L->h, a, L->io_h, L->n, s);
+  layer_forward_impl(L, L->pad_a.p, L->pad_y.p, s);
+  if (L->fwd_mode != FWD_REPLAY || L->local) copy_rows_2d(y, L->io_h, L->pad_y.p, L->h, L->n, s);
+}
+
 // set_param resets the family's optimizer state (reset_master, optimizer.cpp:46-56)
 void family_reset_if_needed(Family& F, cudaStream_t s) {
   if (!F.reset) return;
@@ -746,7 +822,18 @@ void set_adam_epilogue(ted_layer* L, GemmParams& g, int64_t off) {
 }
 
 // --------------------------------------------------------------- backward
+void layer_backward_impl(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s);
 void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
+  if (L->io_h == L->h) {
+    layer_backward_impl(L, dy, da, s);
+    return;
+  }
+  if (dy) copy_rows_2d(L->pad_dy.p, L->h, dy, L->io_h, L->n, s);
+  layer_backward_impl(L, dy ? L->pad_dy.p : nullptr, L->pad_da.p, s);
+  copy_rows_2d(da, L->io_h, L->pad_da.p, L->h, L->n, s);
+}
+
+void layer_backward_impl(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
   if (!L->have_forward) throw ConfigError("backward called before forward");
   const int h = L->h, E = L->E;
   const double nglob = double(L->n) * L->P * L->D;
@@ -800,6 +887,7 @@ void layer_backward(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s) {
     zero_asm_pads(L, L->dfe_asm.p, s);
     rows = asm_rows_bound(L);
   }
+  ledger_pass(L, 2, s);
   bf16* P = L->fam_exp.param.p;
   bf16* G = L->fam_exp.grad.p;
   GemmOperands o{};
@@ -997,6 +1085,7 @@ void family_step(ted_layer* L, Family& F, cudaStream_t s) {
 }
 
 void layer_optimizer(ted_layer* L, cudaStream_t s) {
+  if (!L->capturing) ledger_host_optim(L);  // graph replays add it per launch
   L->mark("grad_sync", s);
   // run_grad_sync (moe.cpp:699-711): sum over the data groups
   if (L->D > 1)
@@ -1110,7 +1199,8 @@ void setup_peer_exchange(ted_layer* L) {
 void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* topo,
                   const ted_flags* flags, const ted_adam_cfg* adam, const ted_tile_cfg* tiles,
                   double cf, int shard_opt, int rank, const void* uid,
-                  ncclComm_t parent = nullptr, ted_layer* share = nullptr) {
+                  ncclComm_t parent = nullptr, ted_layer* share = nullptr,
+                  bool io_internal = false) {
   require(model && topo && flags && adam && tiles, "null config pointer");
   L->model = *model;
   L->topo = *topo;
@@ -1125,10 +1215,12 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   require(flags->cac == 0 && flags->ckpt == 0,
           "flags: ckpt/cac (activation checkpointing, CAC) are not implemented in this build");
   require(model->experts <= 64, "model: at most 64 experts");
-  L->h = model->hidden;
+  L->hu = model->hidden;
+  L->h = (L->hu + 255) / 256 * 256;  // tensor-core N tile; zero-padded beyond hu
+  L->io_h = io_internal ? L->h : L->hu;
   L->E = model->experts;
   L->n = model->tokens_per_shard;
-  L->f = 4 * L->h;  // kFfnMultiple (moe.hpp:33)
+  L->f = 4 * L->hu;  // kFfnMultiple (moe.hpp:33)
   L->T = topo->tensor_parallel;
   L->P = topo->experts;
   L->world = topo->world_size;
@@ -1142,9 +1234,8 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
                                 std::to_string(L->P) + ")");
   L->Eloc = L->E / L->P;
   require(L->f % L->T == 0, "tensor_parallel does not divide the block inner width");
-  L->fT = L->f / L->T;
-  require(L->h % 256 == 0, "hidden must be a multiple of 256 (tensor-core N tile)");
-  require(L->fT % 256 == 0, "4*hidden/tensor_parallel must be a multiple of 256");
+  L->fTu = L->f / L->T;
+  L->fT = (L->fTu + 255) / 256 * 256;
   L->dtd = flags->dtd && L->T > 1;
   require(!L->dtd || L->n % L->T == 0,
           "token dropping needs tensor_parallel to divide tokens_per_shard (moe.cpp:775-779)");
@@ -1204,6 +1295,9 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->loss_part.alloc(L->nblk + 1);
   L->loss.alloc(1);
   L->loss.zero();
+  L->h_loss.alloc(1);
+  L->led.alloc(5 * 3 * 2);
+  L->led.zero();
   L->verdict.alloc(2);
   {
     const int one[2] = {1, 1};
@@ -1258,6 +1352,12 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
       L->dx_home.alloc(size_t(n) * h);
     }
   }
+  if (L->io_h != L->h) {  // zero-padded staging of the caller's [n][hu] token buffers
+    for (DevBuf<bf16>* b : {&L->pad_a, &L->pad_y, &L->pad_dy, &L->pad_da}) {
+      b->alloc(size_t(n) * h);
+      b->zero();
+    }
+  }
   if (L->direct) setup_peer_exchange(L);
   {
     const char* gv = std::getenv("TED_GRAPH");
@@ -1306,8 +1406,9 @@ int layer_create_child(const ted_model_cfg* model, const ted_topo_cfg* topo,
     require(out != nullptr, "null output pointer");
     auto* L = new ted_layer();
     try {
+      // the stack passes its own zero-padded [n][h] buffers: no staging copies
       create_layer(L, model, topo, flags, adam, tiles, capacity_factor, shard_optimizer, rank,
-                   nullptr, parent, share);
+                   nullptr, parent, share, /*io_internal=*/true);
       fix_views(L);
     } catch (...) {
       delete L;
@@ -1333,6 +1434,7 @@ void layer_set_forward_mode(ted_layer* L, int mode) {
 }
 
 void layer_check_fault(ted_layer* L) { check_fault(L); }
+void layer_set_ledger_phase(ted_layer* L, int phase) { L->ledger_phase = phase; }
 void layer_abort(ted_layer* L, const std::string& why) {
   if (L->poisoned.empty()) L->poisoned = why;
   abort_comms(L);
@@ -1413,13 +1515,14 @@ int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
     require(L && name && full, "null argument");
     require(lookup(L, name, pl), std::string("no parameter named ") + name + " on rank " +
                                      std::to_string(L->rank));
-    std::vector<float> shard(size_t(pl.rows * pl.cols));
+    // the shard in the family's (possibly column-padded) layout: rows x ld, pads zero
+    std::vector<float> shard(size_t(pl.rows * pl.ld), 0.f);
     for (int64_t r = 0; r < pl.rows; ++r)
       for (int64_t c = 0; c < pl.cols; ++c) {
         int64_t fr = r, fc = c;
         if (pl.axis == 1) fc = c + int64_t(L->t) * pl.cols;
         if (pl.axis == 2) fr = r + int64_t(L->t) * pl.rows;
-        shard[size_t(r * pl.cols + c)] = full[fr * pl.full_cols + fc];
+        shard[size_t(r * pl.ld + c)] = full[fr * pl.full_cols + fc];
       }
     std::vector<uint16_t> b(shard.size());
     for (size_t i = 0; i < b.size(); ++i) b[i] = f2bf(shard[i]);
@@ -1428,10 +1531,12 @@ int ted_layer_set_param(ted_layer* L, const char* name, const float* full) {
     CU(cudaMemcpy(F.param.p + pl.off, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
     const int64_t lo = std::max(pl.off, F.begin), hi = std::min(pl.off + int64_t(b.size()), F.end);
     if (state_blocked(L, pl)) {  // unsharded: the whole tensor, state in the blk_off layout
-      std::vector<float> blk(shard.size());
+      const int64_t prow = (pl.rows + 127) / 128 * 128;  // padded rows of the blocked tile grid
+      std::vector<float> blk(size_t(std::min<int64_t>(prow, pl.axis == 2 ? L->fT : L->h) * pl.ld),
+                             0.f);
       for (int64_t r = 0; r < pl.rows; ++r)
         for (int64_t c = 0; c < pl.cols; ++c)
-          blk[size_t(blk_off(r, c, pl.cols))] = shard[size_t(r * pl.cols + c)];
+          blk[size_t(blk_off(r, c, pl.ld))] = shard[size_t(r * pl.ld + c)];
       CU(cudaMemcpy(F.master.p + pl.off, blk.data(), sizeof(float) * blk.size(),
                     cudaMemcpyHostToDevice));
     } else if (hi > lo)
@@ -1457,11 +1562,12 @@ static int get_tensor(ted_layer* L, const char* name, float* out, int64_t* numel
                          "step and not stored (ted_layer_keep_grads(L, 1) stores it; a "
                          "separate backward() materialises it)");
     std::vector<uint16_t> b{};
-    b.resize(size_t(cnt));
+    b.resize(size_t(pl.rows * pl.ld));
     CU(cudaDeviceSynchronize());
-    CU(cudaMemcpy(b.data(), (grad ? pl.fam->grad.p : pl.fam->param.p) + pl.off, cnt * 2,
+    CU(cudaMemcpy(b.data(), (grad ? pl.fam->grad.p : pl.fam->param.p) + pl.off, b.size() * 2,
                   cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < cnt; ++i) out[i] = bf2f(b[size_t(i)]);
+    for (int64_t r = 0; r < pl.rows; ++r)
+      for (int64_t c = 0; c < pl.cols; ++c) out[r * pl.cols + c] = bf2f(b[size_t(r * pl.ld + c)]);
   });
 }
 
@@ -1484,7 +1590,7 @@ int ted_layer_init_params(ted_layer* L, uint64_t seed) {
       if (pl.axis == 2) col0 = int64_t(L->t) * pl.rows * pl.cols;
       Family& F = *pl.fam;
       init_family_kernel<<<sm_count() * 4, 256>>>(F.param.p, F.master.p, F.begin, F.end, pl.off,
-                                                  pl.rows, pl.cols, pl.full_cols, col0,
+                                                  pl.rows, pl.cols, pl.ld, pl.full_cols, col0,
                                                   name_seed(seed, nm), float(pl.scale),
                                                   state_blocked(L, pl) ? 1 : 0);
       CU(cudaGetLastError());
@@ -1608,6 +1714,7 @@ int ted_layer_step(ted_layer* L, const uint16_t* a, uint16_t* y, uint16_t* da, v
       g.used = ++L->graph_clock;
       CU(cudaGraphLaunch(g.exec, L->hs));
       count_launch(int(g.launches));
+      ledger_host_optim(L);
       L->fam_non.steps += 1;
       L->fam_exp.steps += 1;
       L->have_forward = true;
@@ -1636,8 +1743,12 @@ int ted_layer_keep_grads(ted_layer* L, int keep) {
 int ted_layer_loss(ted_layer* L, double* loss, void* stream) {
   return guard([&] {
     require(L && loss, "null argument");
-    CU(cudaMemcpyAsync(loss, L->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    // into pinned memory: a copy to the caller's pageable double would block the host behind
+    // a stalled collective, out of reach of the timeout
+    CU(cudaMemcpyAsync(L->h_loss.p, L->loss.p, sizeof(double), cudaMemcpyDeviceToHost,
+                       S(stream)));
     wait_stream(L, S(stream));
+    *loss = *L->h_loss.p;
   });
 }
 
@@ -1655,7 +1766,7 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
     for (int v : kc) kept += v;
     o->tokens = L->n;
     o->dropped = L->n - kept;
-    const int64_t hb = int64_t(L->h) * 2;
+    const int64_t hb = int64_t(L->hu) * 2;  // the reference's rows of hu elements
     if (L->local) {
       o->send_rows = kept;
       std::vector<int> so(E + 1);
@@ -1705,6 +1816,25 @@ int ted_layer_get_stats(ted_layer* L, ted_layer_stats* o) {
     CU(cudaMemcpy(vd, L->verdict.p, sizeof(vd), cudaMemcpyDeviceToHost));
     o->placement_ok = vd[0];
     o->placement_ok_all = vd[1];
+  });
+}
+
+int ted_layer_ledger(ted_layer* L, ted_ledger_entry* out, int reset) {
+  return guard([&] {
+    require(L != nullptr, "null layer");
+    CU(cudaDeviceSynchronize());
+    unsigned long long d[5 * 3 * 2];
+    CU(cudaMemcpy(d, L->led.p, sizeof(d), cudaMemcpyDeviceToHost));
+    if (out)
+      for (int ph = 0; ph < 5; ++ph)
+        for (int op = 0; op < 3; ++op) {
+          out[ph * 3 + op].calls = d[(ph * 3 + op) * 2] + L->led_host[ph][op][0];
+          out[ph * 3 + op].payload_bytes = d[(ph * 3 + op) * 2 + 1] + L->led_host[ph][op][1];
+        }
+    if (reset) {
+      L->led.zero();
+      std::memset(L->led_host, 0, sizeof(L->led_host));
+    }
   });
 }
 

@@ -35,8 +35,8 @@ using namespace ted;
 namespace {
 
 __global__ void dense_init_kernel(bf16* param, float* master, int64_t begin, int64_t end,
-                                  int64_t off, int64_t rows, int64_t cols, int64_t full_cols,
-                                  int64_t col0, uint64_t seed, float scale) {
+                                  int64_t off, int64_t rows, int64_t cols, int64_t ld,
+                                  int64_t full_cols, int64_t col0, uint64_t seed, float scale) {
   const int64_t n = rows * cols;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -47,8 +47,9 @@ __global__ void dense_init_kernel(bf16* param, float* master, int64_t begin, int
     z ^= z >> 31;
     const float u = float(z >> 40) * (1.0f / 16777216.0f);
     const float v = (2.f * u - 1.f) * scale;
-    param[off + i] = __float2bfloat16(v);
-    if (off + i >= begin && off + i < end) master[off + i - begin] = v;
+    const int64_t fi = off + r * ld + c;  // padded columns stay zero
+    param[fi] = __float2bfloat16(v);
+    if (fi >= begin && fi < end) master[fi - begin] = v;
   }
 }
 
@@ -112,6 +113,10 @@ struct ted_model {
   int shard_opt = 0, rank = 0;
   int layers = 0, h = 0, f = 0, fT = 0, E = 0, T = 1, P = 1, D = 1, world = 1, t = 0, ep = 0,
       d = 0;
+  // the reference's hidden / inner widths; h and fT are zero-padded to the 256 tile (see
+  // ted_layer: pads stay exactly zero, results are the unpadded ones)
+  int hu = 0, fTu = 0;
+  int64_t fam_u = 0;  // the reference's dense-family length (no padding)
   int64_t n = 0, np = 0, per_block = 0;
   ncclComm_t world_c = nullptr, tp_c = nullptr, dp_c = nullptr;
   std::vector<DenseBlock> attn, ffn;  // ffn used on odd layers
@@ -124,9 +129,14 @@ struct ted_model {
   DevBuf<int> seg;                    // {0, np}
   DevBuf<float> col_part;
   DevBuf<double> loss_part, loss;
+  HostBuf<double> h_loss;
   bool have_forward = false;
   double timeout_s = 120.0;  // collective_timeout (moe.hpp:96)
   std::string poisoned;
+  // CommLedger entries of the dense blocks and the dense family ([phase][op][calls, bytes],
+  // see ted_layer_ledger); the MoE layers keep their own
+  unsigned long long led[5][3][2] = {};
+  int phase = 0;  // ledger phase of the dense passes running now
 };
 
 namespace {
@@ -266,8 +276,11 @@ void dense_forward(ted_model* M, DenseBlock& B, const bf16* X, bf16* Y, cudaStre
   g.bias = (M->t == 0) ? P + ob2 : nullptr;
   g.aux = nullptr;
   run_gemm(o, g, M->np, s);
-  if (M->T > 1)  // row-parallel partial sums (parallel_linear.cpp:28)
+  if (M->T > 1) {  // row-parallel partial sums (parallel_linear.cpp:28)
     NC(ncclAllReduce(Y, Y, size_t(M->n) * M->h, ncclBfloat16, ncclSum, M->tp_c, s));
+    M->led[M->phase][0][0] += 1;
+    M->led[M->phase][0][1] += uint64_t(M->n) * M->hu * 2;
+  }
   zero_pad_rows(M, Y, s);
 }
 
@@ -356,8 +369,11 @@ void dense_backward(ted_model* M, DenseBlock& B, const bf16* X, const bf16* dY, 
   run_gemm(o, g, M->np, s);
   check(colsum_groups(B.z.p, fT, fT, M->seg.p, 1, int(M->np), M->col_part.p, G + ob1, 0, s),
         "colsum db1");
-  if (M->T > 1)  // column-parallel input gradient (parallel_linear.cpp:19)
+  if (M->T > 1) {  // column-parallel input gradient (parallel_linear.cpp:19)
     NC(ncclAllReduce(dX, dX, size_t(M->n) * h, ncclBfloat16, ncclSum, M->tp_c, s));
+    M->led[2][0][0] += 1;
+    M->led[2][0][1] += uint64_t(M->n) * M->hu * 2;
+  }
   zero_pad_rows(M, dX, s);
 }
 
@@ -370,6 +386,7 @@ struct DenseLoc {
   int64_t off, rows, cols, full_cols;
   int axis;
   double scale;
+  int64_t ld;  // row stride in the family (padded columns)
 };
 
 // name -> (layer, dense block or MoE); dense parameters are sliced like slice_tensor
@@ -396,13 +413,13 @@ bool dense_lookup(ted_model* M, int layer, const std::string& blk, const std::st
   const bool moe_layer = (layer % 2) == 0;  // layer_has_experts (moe.cpp)
   if (!(blk == "attn" || (blk == "ffn" && !moe_layer))) return false;
   const int64_t base = (blk == "attn" ? M->attn : M->ffn)[size_t(layer)].off;
-  const int h = M->h, fT = M->fT, f = M->f;
-  const double sin = 1.0 / std::sqrt(double(h)), sout = 1.0 / std::sqrt(double(f));
+  const int h = M->h, fT = M->fT, f = M->f, hu = M->hu, fTu = M->fTu;
+  const double sin = 1.0 / std::sqrt(double(hu)), sout = 1.0 / std::sqrt(double(f));
   const int64_t ob1 = int64_t(h) * fT, ow2 = ob1 + fT, ob2 = ow2 + int64_t(fT) * h;
-  if (leaf == "w1") out = {base, h, fT, f, 1, sin};
-  else if (leaf == "b1") out = {base + ob1, 1, fT, f, 1, 0.1};
-  else if (leaf == "w2") out = {base + ow2, fT, h, h, 2, sout};
-  else if (leaf == "b2") out = {base + ob2, 1, h, h, 0, 0.1};
+  if (leaf == "w1") out = {base, hu, fTu, f, 1, sin, fT};
+  else if (leaf == "b1") out = {base + ob1, 1, fTu, f, 1, 0.1, fT};
+  else if (leaf == "w2") out = {base + ow2, fTu, hu, hu, 2, sout, h};
+  else if (leaf == "b2") out = {base + ob2, 1, hu, hu, 0, 0.1, h};
   else return false;
   return true;
 }
@@ -432,6 +449,8 @@ void family_adam(ted_model* M, cudaStream_t s) {
     CU(cudaMemcpyAsync(gbuf + F.pos * F.chunk, F.param.p + F.begin, sizeof(bf16) * owned,
                        cudaMemcpyDeviceToDevice, s));
     NC(ncclAllGather(gbuf + F.pos * F.chunk, gbuf, size_t(F.chunk), ncclBfloat16, M->dp_c, s));
+    M->led[4][1][0] += 1;
+    M->led[4][1][1] += uint64_t((M->fam_u + F.group - 1) / F.group) * 2;
     for (int q = 0; q < F.group; ++q) {
       if (q == F.pos) continue;
       const int64_t b = shard_lo(F.elems, F.group, q), e = shard_lo(F.elems, F.group, q + 1);
@@ -463,8 +482,9 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   M->ckpt = flags->ckpt != 0;
   M->cac = M->ckpt && flags->cac != 0;
   M->layers = model->layers;
-  M->h = model->hidden;
-  M->f = 4 * M->h;
+  M->hu = model->hidden;
+  M->h = (M->hu + 255) / 256 * 256;
+  M->f = 4 * M->hu;
   M->E = model->experts;
   M->n = model->tokens_per_shard;
   M->T = topo->tensor_parallel;
@@ -475,9 +495,8 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   M->D = M->world / (M->T * M->P);
   require(rank >= 0 && rank < M->world, "rank out of range");
   require(M->f % M->T == 0, "4*hidden must divide by tensor_parallel");
-  M->fT = M->f / M->T;
-  require(M->h % 256 == 0 && M->fT % 256 == 0,
-          "dense blocks: hidden and 4*hidden/tensor_parallel must be multiples of 256");
+  M->fTu = M->f / M->T;
+  M->fT = (M->fTu + 255) / 256 * 256;
   M->t = rank % M->T;
   M->ep = (rank / M->T) % M->P;
   M->d = rank / (M->T * M->P);
@@ -504,6 +523,7 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   }
   Family& F = M->fam;
   F.elems = off;
+  M->fam_u = int64_t(M->layers + M->layers / 2) * (2 * int64_t(M->hu) * M->fTu + M->fTu + M->hu);
   F.group = shard_opt ? M->P * M->D : 1;
   F.pos = shard_opt ? M->ep + M->P * M->d : 0;
   F.begin = shard_lo(F.elems, F.group, F.pos);
@@ -565,13 +585,16 @@ void create_model(ted_model* M, const ted_model_cfg* model, const ted_topo_cfg* 
   M->loss_part.alloc(kLossCtas);
   M->loss.alloc(1);
   M->loss.zero();
+  M->h_loss.alloc(1);
   CU(cudaDeviceSynchronize());
 }
 
 void model_forward(ted_model* M, const bf16* batch, cudaStream_t s) {
   const int h = M->h;
-  CU(cudaMemcpyAsync(M->xin[0].p, batch, sizeof(bf16) * size_t(M->n) * h,
-                     cudaMemcpyDeviceToDevice, s));
+  M->phase = 0;
+  // the caller's [n][hu] batch into the zero-padded [np][h] input
+  CU(cudaMemcpy2DAsync(M->xin[0].p, size_t(h) * 2, batch, size_t(M->hu) * 2, size_t(M->hu) * 2,
+                       size_t(M->n), cudaMemcpyDeviceToDevice, s));
   for (int l = 0; l < M->layers; ++l) {
     dense_forward(M, M->attn[size_t(l)], M->xin[size_t(l)].p, M->abuf[size_t(l)].p, s);
     if (l % 2 == 0) {
@@ -599,14 +622,17 @@ void model_forward(ted_model* M, const bf16* batch, cudaStream_t s) {
 // stash), in which case only the GEMM1 + GELU the backward reads are recomputed
 void recompute_layer(ted_model* M, int l, cudaStream_t s) {
   const bool replay = M->cac && M->world > 1;
+  M->phase = 1;  // Phase::Recompute
   DenseBlock& A = M->attn[size_t(l)];
   if (replay) dense_gemm1(M, A, M->xin[size_t(l)].p, s);
   else dense_forward(M, A, M->xin[size_t(l)].p, M->abuf[size_t(l)].p, s);
   if (l % 2 == 0) {
     ted_layer* L = M->moe[size_t(l)];
     layer_set_forward_mode(L, M->cac ? FWD_REPLAY : FWD_LIVE);
+    layer_set_ledger_phase(L, 1);
     const int rc = ted_layer_forward(L, reinterpret_cast<const uint16_t*>(M->abuf[size_t(l)].p),
                                      reinterpret_cast<uint16_t*>(M->dpart.p), s);
+    layer_set_ledger_phase(L, 0);
     layer_set_forward_mode(L, FWD_LIVE);
     if (rc != TED_OK) throw RuntimeError(last_error());
   } else if (replay) {
@@ -628,6 +654,7 @@ void model_backward(ted_model* M, cudaStream_t s, bool step_follows = false) {
   bf16* dx = M->dy1.p;
   for (int l = M->layers - 1; l >= 0; --l) {
     if (M->ckpt) recompute_layer(M, l, s);
+    M->phase = 2;  // Phase::Backward
     if (l % 2 == 0) {
       if (step_follows) {
         layer_backward_then_step(M->moe[size_t(l)], dy, M->dmid.p, s);
@@ -649,9 +676,12 @@ void model_backward(ted_model* M, cudaStream_t s, bool step_follows = false) {
 void model_optimizer(ted_model* M, cudaStream_t s) {
   // run_grad_sync (moe.cpp:699-711) for the dense family, then AdamW; the MoE layers sync
   // and step their own families (gate + experts)
-  if (M->P * M->D > 1)
+  if (M->P * M->D > 1) {
     NC(ncclAllReduce(M->fam.grad.p, M->fam.grad.p, size_t(M->fam.elems), ncclBfloat16, ncclSum,
                      M->dp_c, s));
+    M->led[3][0][0] += 1;
+    M->led[3][0][1] += uint64_t(M->fam_u) * 2;
+  }
   family_adam(M, s);
   for (ted_layer* L : M->moe)
     if (L && ted_layer_optimizer_step(L, s) != TED_OK) throw RuntimeError(last_error());
@@ -714,13 +744,13 @@ int ted_model_set_param(ted_model* M, const char* name, const float* full) {
     }
     DenseLoc dl;
     require(dense_lookup(M, layer, blk, leaf, dl), std::string("no parameter named ") + name);
-    std::vector<float> shard(size_t(dl.rows * dl.cols));
+    std::vector<float> shard(size_t(dl.rows * dl.ld), 0.f);  // family layout, pads zero
     for (int64_t r = 0; r < dl.rows; ++r)
       for (int64_t c = 0; c < dl.cols; ++c) {
         int64_t fr = r, fc = c;
         if (dl.axis == 1) fc = c + int64_t(M->t) * dl.cols;
         if (dl.axis == 2) fr = r + int64_t(M->t) * dl.rows;
-        shard[size_t(r * dl.cols + c)] = full[fr * dl.full_cols + fc];
+        shard[size_t(r * dl.ld + c)] = full[fr * dl.full_cols + fc];
       }
     std::vector<uint16_t> b(shard.size());
     for (size_t i = 0; i < b.size(); ++i) b[i] = f2bf(shard[i]);
@@ -755,11 +785,12 @@ static int model_get(ted_model* M, const char* name, float* out, int64_t* numel,
     const int64_t cnt = dl.rows * dl.cols;
     if (numel) *numel = cnt;
     if (!out) return;
-    std::vector<uint16_t> b(static_cast<size_t>(cnt));
+    std::vector<uint16_t> b(static_cast<size_t>(dl.rows * dl.ld));
     CU(cudaDeviceSynchronize());
-    CU(cudaMemcpy(b.data(), (grad ? M->fam.grad.p : M->fam.param.p) + dl.off, cnt * 2,
+    CU(cudaMemcpy(b.data(), (grad ? M->fam.grad.p : M->fam.param.p) + dl.off, b.size() * 2,
                   cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < cnt; ++i) out[i] = bf2f(b[size_t(i)]);
+    for (int64_t r = 0; r < dl.rows; ++r)
+      for (int64_t c = 0; c < dl.cols; ++c) out[r * dl.cols + c] = bf2f(b[size_t(r * dl.ld + c)]);
   });
 }
 
@@ -795,7 +826,7 @@ int ted_model_init_params(ted_model* M, uint64_t seed) {
           for (unsigned char c : nm) hs = (hs ^ c) * 1099511628211ULL;
           dense_init_kernel<<<sm_count() * 4, 256>>>(M->fam.param.p, M->fam.master.p,
                                                      M->fam.begin, M->fam.end, dl.off, dl.rows,
-                                                     dl.cols, dl.full_cols, col0,
+                                                     dl.cols, dl.ld, dl.full_cols, col0,
                                                      seed * 0x9E3779B97F4A7C15ULL + hs,
                                                      float(dl.scale));
           CU(cudaGetLastError());
@@ -850,8 +881,33 @@ int ted_model_step(ted_model* M, const uint16_t* batch, void* stream) {
 int ted_model_loss(ted_model* M, double* loss, void* stream) {
   return guard([&] {
     require(M && loss, "null argument");
-    CU(cudaMemcpyAsync(loss, M->loss.p, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    CU(cudaMemcpyAsync(M->h_loss.p, M->loss.p, sizeof(double), cudaMemcpyDeviceToHost,
+                       S(stream)));  // pinned: see ted_layer_loss
     model_wait(M, S(stream));
+    *loss = *M->h_loss.p;
+  });
+}
+
+int ted_model_ledger(ted_model* M, ted_ledger_entry* out, int reset) {
+  return guard([&] {
+    require(M != nullptr, "null model");
+    ted_ledger_entry acc[15] = {};
+    for (int ph = 0; ph < 5; ++ph)
+      for (int op = 0; op < 3; ++op) {
+        acc[ph * 3 + op].calls = M->led[ph][op][0];
+        acc[ph * 3 + op].payload_bytes = M->led[ph][op][1];
+      }
+    for (ted_layer* L : M->moe)
+      if (L) {
+        ted_ledger_entry one[15];
+        if (ted_layer_ledger(L, one, reset) != TED_OK) throw RuntimeError(last_error());
+        for (int i = 0; i < 15; ++i) {
+          acc[i].calls += one[i].calls;
+          acc[i].payload_bytes += one[i].payload_bytes;
+        }
+      }
+    if (out) std::memcpy(out, acc, sizeof(acc));
+    if (reset) std::memset(M->led, 0, sizeof(M->led));
   });
 }
 
@@ -903,8 +959,8 @@ int ted_model_memory(ted_model* M, int64_t* out) {
 int ted_model_output(ted_model* M, uint16_t* y, void* stream) {
   return guard([&] {
     require(M && y, "null argument");
-    CU(cudaMemcpyAsync(y, M->xin[size_t(M->layers)].p, sizeof(bf16) * size_t(M->n) * M->h,
-                       cudaMemcpyDeviceToDevice, S(stream)));
+    CU(cudaMemcpy2DAsync(y, size_t(M->hu) * 2, M->xin[size_t(M->layers)].p, size_t(M->h) * 2,
+                         size_t(M->hu) * 2, size_t(M->n), cudaMemcpyDeviceToDevice, S(stream)));
   });
 }
 

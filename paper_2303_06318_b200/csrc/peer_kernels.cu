@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kThreads) scatter_peer_kernel(const bf16* __re
         }
       }
       for (int tr = t0; tr < t1; ++tr) {
+        if ((D.part == 1 && tr != D.my_t) || (D.part == 2 && tr == D.my_t)) continue;
         uint4* dst = reinterpret_cast<uint4*>(dst_row(D, tr, e, r, h));
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -338,6 +339,55 @@ cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep,
   if (E < 1 || E > 1024 || E % P != 0) return cudaErrorInvalidValue;
   plan_peer_kernel<<<1, ((E + 31) / 32) * 32, 0, s>>>(kc_all, T, P, E, Tc, my_ep, my_c, seg,
                                                      disp_base, pull_base);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
+// The reference's CommLedger entries of one MoE pass on this rank (fabric.cpp:163-287
+// accounting, per member: calls + 1 and this member's payload per collective; summing the
+// members gives the reference's group records).  The exchange itself may be fused into
+// NVLink kernels; the ledger records the collectives the reference runs for the same data
+// (moe.cpp:435-563 / :582-686): dispatch and return all-to-all over EP (P > 1), the DTD
+// expert-side and home all-gathers over TP, the expert block's TP all-reduce (T > 1).
+// led: [phase][op][calls, bytes], op order AllReduce, AllGather, AllToAll (types.hpp:39).
+__global__ void ledger_moe_pass_kernel(unsigned long long* __restrict__ led, int phase, int P,
+                                       int T, int dtd, int Tc, int E, int Eloc, int my_t,
+                                       int my_ep, const int* __restrict__ kc,
+                                       const int* __restrict__ kc_all, int src_stride,
+                                       const int* __restrict__ seg_valid, int h) {
+  if (threadIdx.x != 0) return;
+  long long valid = 0, send = 0, recv = 0;
+  for (int le = 0; le < Eloc; ++le) valid += seg_valid[le];
+  const int my_c = dtd ? my_t : 0;
+  for (int e = 0; e < E; ++e) send += kc[my_c * E + e];
+  if (dtd) {  // my block of the expert-side rows: chunk my_t of every EP source
+    for (int s = 0; s < P; ++s)
+      for (int le = 0; le < Eloc; ++le)
+        recv += kc_all[(size_t(src_stride) * s * Tc + my_t) * E + my_ep * Eloc + le];
+  } else {
+    recv = valid;
+  }
+  const unsigned long long hb = 2ull * h;
+  unsigned long long* row = led + size_t(phase) * 3 * 2;
+  if (T > 1) {  // AllReduce (expert block, row-parallel partial sums)
+    row[0] += 1;
+    row[1] += (unsigned long long)valid * hb;
+  }
+  if (dtd) {  // AllGather: the expert-side block and the home chunk
+    row[2] += 2;
+    row[3] += (unsigned long long)(recv + send) * hb;
+  }
+  if (P > 1) {  // AllToAll: dispatch (my rows, self segments included) and return
+    row[4] += 2;
+    row[5] += (unsigned long long)(send + recv) * hb;
+  }
+}
+
+cudaError_t ledger_moe_pass(unsigned long long* led, int phase, int P, int T, int dtd, int Tc,
+                            int E, int Eloc, int my_t, int my_ep, const int* kc, const int* kc_all,
+                            int src_stride, const int* seg_valid, int h, cudaStream_t s) {
+  ledger_moe_pass_kernel<<<1, 32, 0, s>>>(led, phase, P, T, dtd, Tc, E, Eloc, my_t, my_ep, kc,
+                                          kc_all, src_stride, seg_valid, h);
   count_launch(1);
   return cudaGetLastError();
 }

@@ -187,6 +187,8 @@ void layer_memory(const ted_layer* L, int64_t* activations, int64_t* params, int
 // failure detection of a layer (plane-barrier timeout word, NCCL async errors, an earlier
 // fault): throws RuntimeError("TimeoutError: ...") and aborts the layer's communicators
 void layer_check_fault(ted_layer* L);
+// ledger phase of the layer's next forwards (0 Forward, 1 Recompute)
+void layer_set_ledger_phase(ted_layer* L, int phase);
 void layer_abort(ted_layer* L, const std::string& why);
 
 }  // namespace ted

@@ -168,6 +168,10 @@ struct PeerDst {
   // chunk than its slot; rows past the slot's reserved block (clamp_rows[e]) are not
   // written, so the wrong chunk lands misplaced like the reference's instead of overrunning
   const int* clamp_rows = nullptr;
+  // all_replicas: 0 = every replica; 1 = replica my_t only (the reference's EP all-to-all);
+  // 2 = the other replicas only (its DTD all-gather) -- the timed pass splits the fused
+  // scatter into these two launches to report all-to-all and all-gather time separately
+  int part = 0;
 };
 cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* expert, int64_t n,
                               int h, const PeerDst& dst, const float* scale, bool scale_by_prob,
@@ -179,6 +183,11 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
 cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
                                unsigned* epoch_dev, int* fault, unsigned long long timeout_ns,
                                cudaStream_t s);
+// CommLedger entries of one MoE pass (forward / recompute / backward) of this rank, from
+// the device-resident routed counts: led[phase][op][calls, bytes] += ...
+cudaError_t ledger_moe_pass(unsigned long long* led, int phase, int P, int T, int dtd, int Tc,
+                            int E, int Eloc, int my_t, int my_ep, const int* kc, const int* kc_all,
+                            int src_stride, const int* seg_valid, int h, cudaStream_t s);
 // the peer-exchange plan on the device: seg = [seg_off Eloc+1][valid rows Eloc],
 // disp_base [E], pull_base [Tc][E] from the plane-gathered counts
 cudaError_t plan_peer(const int* kc_all, int T, int P, int E, int Tc, int my_ep, int my_c,

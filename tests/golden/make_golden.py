@@ -110,6 +110,11 @@ def main():
     # SerialModel losses for the model-stack parity tests (layers, h, E, n, seed, shards)
     stacks = [(2, 256, 4, 128, 1, 1), (4, 256, 4, 128, 5, 1), (2, 256, 4, 128, 3, 2),
               (2, 256, 4, 128, 3, 1)]
+    # the reference's verify sweep shape (harness.cpp:254-278: hidden 8, 8 tokens per
+    # shard, 1 layer) for every (experts, data shards) a 1-4 GPU layout produces, and a
+    # 2-layer variant
+    stacks += [(1, 8, e, 8, 1, s) for e in (1, 2, 4) for s in (1, 2, 4)]
+    stacks += [(2, 8, 2, 8, 7, 1), (2, 8, 2, 8, 7, 2)]
     sl = []
     for (L_, h_, E_, n_, s_, S_) in stacks:
         ls = np.empty(3)

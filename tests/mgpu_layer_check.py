@@ -40,18 +40,24 @@ def stall_check(L, a, y, da, rank, dist):
 
     import paper_2303_06318_b200 as ted
     timeout = 3.0
+
+    def note(m):
+        print(f"[rank {rank}] {m}", flush=True)
     L.set_timeout(timeout)
     L.forward(a, y)
     L.loss()
+    note("forward done")
     if rank == 0:
         t0 = time.time()
         L.backward(None, da)
+        note("backward enqueued")
         try:
             L.loss()
             raise AssertionError("a stalled peer was not detected")
         except ted.TedRuntimeError as e:
             msg = str(e)
         waited = time.time() - t0
+        note(f"detected after {waited:.1f} s: {msg}")
         assert "TimeoutError" in msg, msg
         assert timeout * 0.8 < waited < timeout * 10, waited
         try:
@@ -139,6 +145,7 @@ def main():
     L.optimizer_step()
     torch.cuda.synchronize()
     mine["w1_after"] = L.get_param(f"layer0.expert{ep * Eloc}.w1")
+    mine["ledger"] = L.ledger()
     allr = [None] * world
     dist.gather_object(mine, allr if rank == 0 else None, dst=0)
     if rank == 0:
@@ -198,7 +205,19 @@ def main():
                 a2a = sum(r["stats"]["a2a_bytes_fwd"] for r in allr)
                 ag = sum(r["stats"]["ag_bytes_fwd"] for r in allr)
                 assert (a2a, ag) == (int(row[0][6]), int(row[0][7])), (a2a, ag, row[0])
-                report.update(ledger_a2a=a2a, ledger_ag=ag)
+
+                def tot(key):
+                    return sum(r["ledger"].get(key, {}).get("payload_bytes", 0) for r in allr)
+                # the per-phase ledger: forward = predict_comm_volume (its all-reduce figure
+                # counts the attention block's too: the expert block's is half), the
+                # backward mirrors the forward
+                fwd = {op: tot(f"forward.{op}") for op in ("all_to_all", "all_gather", "all_reduce")}
+                assert fwd["all_to_all"] == int(row[0][6]), (fwd, row[0])
+                assert fwd["all_gather"] == int(row[0][7]), (fwd, row[0])
+                assert fwd["all_reduce"] == int(row[0][8]) // 2, (fwd, row[0])
+                for op, v in fwd.items():
+                    assert tot(f"backward.{op}") == v, (op, v)
+                report.update(ledger_a2a=a2a, ledger_ag=ag, ledger_fwd=fwd)
             print("MGPU-OK " + json.dumps(report), flush=True)
     dist.barrier()
     L.close()

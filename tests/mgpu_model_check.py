@@ -17,6 +17,27 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def check_ledger(led, layers, T, P, D, dtd, ckpt, cac, steps, world):
+    """Per-rank collective counts of the reference's schedule (acceptance_test.cpp:134-162,
+    predict_comm_volume cost_model.cpp:346-416): per pass 2 TP all-reduces per layer, 2 EP
+    all-to-alls and (DTD) 2 TP all-gathers per MoE layer; passes = forward + backward, plus
+    the recompute under checkpointing unless CAC replays it (6 + 6 -> 4 + 4 for one MoE
+    layer).  A recompute moves exactly the forward's bytes."""
+    moe_layers = (layers + 1) // 2
+    passes = ["forward", "backward"] + (["recompute"] if ckpt and not (cac and world > 1) else [])
+    per_pass = {"all_reduce": 2 * layers if T > 1 else 0,
+                "all_to_all": 2 * moe_layers if P > 1 else 0,
+                "all_gather": 2 * moe_layers if dtd else 0}
+    for ph in ("forward", "recompute", "backward"):
+        for op, k in per_pass.items():
+            got = led.get(f"{ph}.{op}", {"calls": 0})["calls"]
+            want = steps * k if ph in passes else 0
+            assert got == want, (ph, op, got, want, led)
+    if "recompute" in passes:
+        for op in per_pass:
+            assert led.get(f"recompute.{op}") == led.get(f"forward.{op}"), (op, led)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", type=int, default=2)
@@ -55,9 +76,12 @@ def main():
     a = stack_batch(model, shards)[shard * n:(shard + 1) * n]
     batch = torch.tensor(a, dtype=torch.float32).bfloat16().cuda()
     losses = []
-    for _ in range(3):
+    steps = 3
+    for _ in range(steps):
         M.step(batch)
         losses.append(M.loss())
+    check_ledger(M.ledger(), layers, T, P, D, bool(args.dtd) and T > 1, bool(args.ckpt),
+                 bool(args.cac) and bool(args.ckpt), steps, world)
     allv = [None] * world
     dist.all_gather_object(allv, (t, losses))
     M.close()

@@ -101,8 +101,8 @@ def test_model_config_errors_are_config_status():
     device work, like the reference's validate_model (moe.cpp:100-113)."""
     with pytest.raises(ted.InvalidConfigError, match="layers must be >= 1"):
         ted.TedModel(ted.MoeModelConfig(0, 256, 4, 64, 1), ted.TedConfig())
-    with pytest.raises(ted.InvalidConfigError, match="multiples of 256"):
-        ted.TedModel(ted.MoeModelConfig(2, 200, 4, 64, 1), ted.TedConfig())
+    with pytest.raises(ted.InvalidConfigError, match="tensor_parallel"):
+        ted.TedModel(ted.MoeModelConfig(2, 1, 8, 64, 1), ted.derive_config(8, 8, 1))
 
 
 def test_plan_library_loads():

@@ -21,13 +21,18 @@ def _port():
     return p
 
 
-def _run(nproc, *args, env=None, script="mgpu_layer_check.py"):
+def _run(nproc, *args, env=None, script="mgpu_layer_check.py", timeout=600):
     for _attempt in range(3):  # a freshly probed port can be taken before torchrun binds it
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
                os.path.join(HERE, script), *args]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                           env=dict(os.environ, **(env or {})))
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout,
+                               env=dict(os.environ, **(env or {})))
+        except subprocess.TimeoutExpired as e:
+            out = (e.stdout or b"").decode(errors="replace") if isinstance(e.stdout, bytes) else (e.stdout or "")
+            err = (e.stderr or b"").decode(errors="replace") if isinstance(e.stderr, bytes) else (e.stderr or "")
+            raise AssertionError(f"timed out after {timeout} s\n" + out[-4000:] + err[-4000:])
         if "EADDRINUSE" not in r.stderr + r.stdout:
             break
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
@@ -143,5 +148,5 @@ def test_two_gpus_stalled_peer_times_out(exchange):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     out = _run(2, "--tp", "2", "--ep", "1", "--dtd", "1", "--experts", "4", "--stall", "1",
-               env={"TED_EXCHANGE": exchange})
+               env={"TED_EXCHANGE": exchange, "NCCL_DEBUG": "WARN"}, timeout=180)
     assert "TimeoutError" in out
