@@ -46,6 +46,11 @@ def main():
     ap.add_argument("--zero", type=int, default=1)
     ap.add_argument("--ckpt", type=int, default=0)
     ap.add_argument("--cac", type=int, default=0)
+    ap.add_argument("--layers", type=int, default=2)
+    ap.add_argument("--hidden", type=int, default=256)
+    ap.add_argument("--experts", type=int, default=4)
+    ap.add_argument("--tokens", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=3)
     args = ap.parse_args()
 
     import torch
@@ -62,7 +67,7 @@ def main():
     T, P = args.tp, args.ep
     D = world // (T * P)
     shards = P * D
-    layers, h, E, n, seed = 2, 256, 4, 128, 3
+    layers, h, E, n, seed = args.layers, args.hidden, args.experts, args.tokens, args.seed
     model = ted.MoeModelConfig(layers, h, E, n, seed)
     obj = [ted.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)

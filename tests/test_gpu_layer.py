@@ -33,7 +33,11 @@ def _make(n, h, E, cf, seed):
 
 @pytest.mark.parametrize("n,h,E,cf,seed", [(1024, 256, 4, 0.0, 1), (1024, 256, 4, 1.25, 1),
                                            (1024, 256, 4, 1.25, 11), (2048, 512, 8, 1.0, 7),
-                                           (640, 256, 16, 2.0, 3)])
+                                           (640, 256, 16, 2.0, 3),
+                                           # below the 256 tensor-core tile: zero-padded
+                                           # (the reference's verify sweep: hidden 8)
+                                           (8, 8, 2, 0.0, 1), (64, 100, 3, 1.5, 2),
+                                           (256, 320, 4, 0.0, 4)])
 def test_layer_forward_backward_matches_oracle(n, h, E, cf, seed):
     L, inp = _make(n, h, E, cf, seed)
     f = 4 * h

@@ -13,7 +13,11 @@ from tests._stack import golden_losses, stack_batch, stack_params  # noqa: E402
 TOL = 2e-2
 
 
-@pytest.mark.parametrize("layers,h,E,n,seed", [(2, 256, 4, 128, 1), (4, 256, 4, 128, 5)])
+@pytest.mark.parametrize("layers,h,E,n,seed", [(2, 256, 4, 128, 1), (4, 256, 4, 128, 5),
+                                               # the reference's verify-sweep shape (hidden 8,
+                                               # 8 tokens), zero-padded to the 256 tile
+                                               (1, 8, 1, 8, 1), (1, 8, 2, 8, 1), (1, 8, 4, 8, 1),
+                                               (2, 8, 2, 8, 7)])
 def test_stack_matches_reference_serial_model(layers, h, E, n, seed):
     import paper_2303_06318_b200 as ted
     model = ted.MoeModelConfig(layers, h, E, n, seed)

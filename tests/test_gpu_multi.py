@@ -150,3 +150,20 @@ def test_two_gpus_stalled_peer_times_out(exchange):
     out = _run(2, "--tp", "2", "--ep", "1", "--dtd", "1", "--experts", "4", "--stall", "1",
                env={"TED_EXCHANGE": exchange, "NCCL_DEBUG": "WARN"}, timeout=180)
     assert "TimeoutError" in out
+
+
+# The reference's verify sweep (harness.cpp:254-278): every valid (tensor, experts) split of
+# worlds 2 and 4 at hidden 8, 8 tokens per shard, 1 layer, DTD when T > 1, with
+# checkpointing + CAC -- losses against the reference SerialModel (the shapes run
+# zero-padded to the 256 tensor-core tile).
+SWEEP = [(w, t, e) for w in (2, 4) for t in range(1, w + 1) if w % t == 0
+         for e in range(1, min(w // t, 4) + 1) if (w // t) % e == 0]
+
+
+@pytest.mark.parametrize("world,tp,ep", SWEEP)
+def test_verify_sweep_small_shapes(world, tp, ep):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    _run(world, "--tp", str(tp), "--ep", str(ep), "--dtd", str(int(tp > 1)), "--ckpt", "1",
+         "--cac", "1", "--layers", "1", "--hidden", "8", "--experts", str(ep), "--tokens", "8",
+         "--seed", "1", script="mgpu_model_check.py")
