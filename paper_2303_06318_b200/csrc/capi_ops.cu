@@ -155,9 +155,13 @@ int ted_gate_forward(const uint16_t* a, const uint16_t* wg, int64_t n, int h, in
     device_ok();
     const int nblk = int((n + kRouteBlock - 1) / kRouteBlock);
     int* hist = nullptr;
-    Carve().add(&hist, size_t(nblk) * E).take(S(stream));
+    bf16* wgT = nullptr;
+    Carve()
+        .add(&hist, size_t(nblk) * E)
+        .add(&wgT, std::max<size_t>(gate_wgt_elems(h, E), 1))
+        .take(S(stream));
     cuda_ok(gate_forward(reinterpret_cast<const bf16*>(a), reinterpret_cast<const bf16*>(wg), n,
-                         h, E, logits, probs, expert, prob, hist, S(stream)),
+                         h, E, logits, probs, expert, prob, hist, wgT, S(stream)),
             "gate_forward");
   });
 }

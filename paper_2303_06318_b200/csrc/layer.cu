@@ -109,6 +109,7 @@ struct ted_layer {
 
   // routing
   DevBuf<float> logits, probs, prob, loss_part, dlogits, gate_part, col_part;
+  DevBuf<bf16> wgT;  // the gate weight transposed for the L1-resident gate kernel
   DevBuf<int> expert, slot, pos_send, pos_home, blk_hist, blk_prefix, chunk_prefix, kc, kc_all,
       send_base, home_base, seg_off;
   int* seg_valid_view = nullptr;  // [Eloc] view inside seg_off's allocation
@@ -527,7 +528,7 @@ void layer_forward_impl(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   const bf16* wg = L->fam_non.param.p;
   L->mark("gate", s);
   check(gate_forward(a, wg, L->n, h, E, L->logits.p, L->probs.p, L->expert.p, L->prob.p,
-                     L->blk_hist.p, s),
+                     L->blk_hist.p, L->wgT.n ? L->wgT.p : nullptr, s),
         "gate_forward");
   L->mark("route_dispatch", s);
   RouteScanArgs ra{};
@@ -1296,6 +1297,7 @@ void create_layer(ted_layer* L, const ted_model_cfg* model, const ted_topo_cfg* 
   L->loss.alloc(1);
   L->loss.zero();
   L->h_loss.alloc(1);
+  if (size_t wt = gate_wgt_elems(L->h, L->E)) L->wgT.alloc(wt);
   L->led.alloc(5 * 3 * 2);
   L->led.zero();
   L->verdict.alloc(2);

@@ -222,6 +222,100 @@ __global__ void __launch_bounds__(kThreads, 2) gate_fwd_mma_kernel(
   if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
 }
 
+// Same logits (bit for bit: identical products, K permutation and accumulation order),
+// with Wg^T read straight from global memory -- pre-transposed once per call into
+// wgT [EMAX][h] (zero rows e >= E), small enough (<= 128 KB) to stay in L1 / L2 -- instead
+// of being re-staged into shared memory by every 64-token CTA behind two barriers: the
+// token rows stream from HBM without stalls, U 32-element K steps in flight per warp.
+template <int EMAX, int U>
+__global__ void __launch_bounds__(kThreads, 2) gate_fwd_l1_kernel(
+    const bf16* __restrict__ a, const bf16* __restrict__ wgT, int64_t n, int h, int E,
+    float* __restrict__ logits, float* __restrict__ probs, int* __restrict__ expert,
+    float* __restrict__ prob, int* __restrict__ blk_hist) {
+  constexpr int NT = EMAX / 8;
+  __shared__ float s_part[2][kRouteBlock][EMAX];
+  __shared__ int s_hist[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int tt = warp & 3, ks = warp >> 2;
+  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
+  const int64_t ta = tok0 + tt * 16 + g, tb = ta + 8;
+  const bf16* pa = a + (ta < n ? ta : 0) * int64_t(h) + 8 * c;
+  const bf16* pb = a + (tb < n ? tb : 0) * int64_t(h) + 8 * c;
+  const bool va = ta < n, vb = tb < n;
+  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
+  float acc[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  const bf16* wb = wgT + int64_t(g) * h + 8 * c;  // expert nt*8 + g, K offset 8c
+  const int steps = h / 32;  // this warp takes K steps ks, ks + 2, ...
+  uint4 cur[U][2], nxt[U][2];
+  auto load = [&](int s0, uint4 (&d)[U][2]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int st = s0 + 2 * u;
+      const int64_t off = int64_t(st) * 32;
+      const bool in = st < steps;
+      d[u][0] = (in && va) ? ldg_stream(pa + off) : make_uint4(0, 0, 0, 0);
+      d[u][1] = (in && vb) ? ldg_stream(pb + off) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  load(ks, cur);
+  for (int s0 = ks; s0 < steps; s0 += 2 * U) {
+    load(s0 + 2 * U, nxt);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int st = s0 + 2 * u;
+      if (st >= steps) break;
+      const uint32_t* xa = reinterpret_cast<const uint32_t*>(&cur[u][0]);
+      const uint32_t* xb = reinterpret_cast<const uint32_t*>(&cur[u][1]);
+      const bf16* wrow = wb + st * 32;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint2 bw = __ldg(reinterpret_cast<const uint2*>(wrow + int64_t(nt) * 8 * h + 4 * m));
+          mma_bf16_16816(acc[nt], xa[2 * m], xb[2 * m], xa[2 * m + 1], xb[2 * m + 1], bw.x, bw.y);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      cur[u][0] = nxt[u][0];
+      cur[u][1] = nxt[u][1];
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int e = nt * 8 + 2 * c;
+    s_part[ks][tt * 16 + g][e] = acc[nt][0];
+    s_part[ks][tt * 16 + g][e + 1] = acc[nt][1];
+    s_part[ks][tt * 16 + g + 8][e] = acc[nt][2];
+    s_part[ks][tt * 16 + g + 8][e + 1] = acc[nt][3];
+  }
+  __syncthreads();
+  for (int t = 0; t < kWarpTok; ++t) {
+    const int lt = warp * kWarpTok + t;
+    const int64_t k = tok0 + lt;
+    if (k >= n) break;
+    const float l0v = lane < E ? s_part[0][lt][lane] + s_part[1][lt][lane] : 0.f;
+    const float l1v = 0.f;  // EMAX <= 32
+    const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
+    if (lane == 0) atomicAdd(&s_hist[best], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
+}
+
+// wgT[e][k] = Wg[k][e] (e < E), 0 (E <= e < EMAX)
+__global__ void wg_transpose_kernel(const bf16* __restrict__ wg, int h, int E, int EMAX,
+                                    bf16* __restrict__ wgT) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= h) return;
+  for (int e = 0; e < EMAX; ++e)
+    wgT[int64_t(e) * h + k] = e < E ? wg[int64_t(k) * E + e] : __float2bfloat16(0.f);
+}
+
 __global__ void __launch_bounds__(kThreads) route_logits_kernel(const float* __restrict__ L,
                                                                 int64_t n, int E,
                                                                 float* __restrict__ probs,
@@ -1268,11 +1362,29 @@ void smem_attr(K k, size_t bytes) {
 }  // namespace
 
 // ================================================================== launchers
+size_t gate_wgt_elems(int h, int E) {
+  const int em = E <= 8 ? 8 : 16;
+  return (E <= 16 && size_t(em) * h * 2 <= (128u << 10)) ? size_t(em) * h : 0;
+}
+
 cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
-                         float* probs, int* expert, float* prob, int* blk_hist, cudaStream_t s) {
+                         float* probs, int* expert, float* prob, int* blk_hist, bf16* wgT,
+                         cudaStream_t s) {
   if (E < 1 || E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
+  if (wgT != nullptr && gate_wgt_elems(h, E) > 0) {
+    const int em = E <= 8 ? 8 : 16;
+    wg_transpose_kernel<<<ceil_div(h, 256), 256, 0, s>>>(wg, h, E, em, wgT);
+    if (em == 8)
+      gate_fwd_l1_kernel<8, 4><<<grid, kThreads, 0, s>>>(a, wgT, n, h, E, logits, probs, expert,
+                                                         prob, blk_hist);
+    else
+      gate_fwd_l1_kernel<16, 4><<<grid, kThreads, 0, s>>>(a, wgT, n, h, E, logits, probs, expert,
+                                                          prob, blk_hist);
+    count_launch(2);
+    return cudaGetLastError();
+  }
 #define TED_GATE(EM, U)                                                                       \
   {                                                                                           \
     const int HC = std::min(((h + 255) / 256) * 256, EM <= 16 ? 2048 : (EM <= 32 ? 1024 : 512)); \

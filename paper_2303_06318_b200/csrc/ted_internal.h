@@ -90,8 +90,12 @@ constexpr int kRouteBlock = 64;  // tokens per routing block (gate / scan / disp
 constexpr int kPad = 128;         // expert segments are padded to the GEMM M tile
 
 // top-1 gate: logits = a Wg (fp32 accumulate), argmax (lowest index on ties), softmax.
+// wgT: scratch of gate_wgt_elems(h, E) bf16 (0: not used -- the shared-memory-staged
+// variant runs); with it Wg^T is transposed once and read from L1 by every CTA.
+size_t gate_wgt_elems(int h, int E);
 cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
-                         float* probs, int* expert, float* prob, int* blk_hist, cudaStream_t s);
+                         float* probs, int* expert, float* prob, int* blk_hist, bf16* wgT,
+                         cudaStream_t s);
 // Routing from caller-provided fp32 logits (same selection/softmax code path).
 cudaError_t gate_route_logits(const float* logits, int64_t n, int E, float* probs, int* expert,
                               float* prob, int* blk_hist, cudaStream_t s);
