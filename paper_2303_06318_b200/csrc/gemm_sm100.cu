@@ -87,7 +87,11 @@ __device__ __forceinline__ void st_state(float* p, float4 v, uint64_t pol) {
 // tile, each CTA staging its 128 rows of A and 128 of B's 256 columns -- a third less
 // operand traffic into shared memory per FLOP than a single CTA's 128 x 256 tile, and
 // smaller stages, so a deeper ring.
-template <int EPI, bool PAIR = false>
+// PUSH (ROWS mode, store / bias epilogues): the output rows are not stored locally but
+// pushed over NVLink into the home ranks' receive buffers (see push_rows below); each
+// epilogue warp stages its 32 rows x 128 columns (8 KB) in shared memory so the remote
+// stores go out as 256 B row segments; one stage fewer to make room.
+template <int EPI, bool PAIR = false, bool PUSH = false>
 struct Cfg {
   static constexpr int EPI_WARPS = EPI == EPI_ADAM ? 16 : 8;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;  // 4 control warps + epilogue warps
@@ -95,9 +99,11 @@ struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
   static constexpr int B_LOCAL = PAIR ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;  // this CTA's B
   static constexpr int STAGE_LOCAL = A_STAGE_BYTES + B_LOCAL;
-  static constexpr int STAGES = PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4;
+  static constexpr int STAGES = PUSH ? 3 : (PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4);
   // AdamW: the parameter half block and (keep-gradients mode) the gradient half block
-  static constexpr size_t PER_WARP = EPI == EPI_ADAM ? 2 * P16_BLOCK_BYTES : NOUT * EPI_BLOCK_BYTES;
+  static constexpr size_t PER_WARP = PUSH ? 32 * COL_SPAN * 2
+                                          : (EPI == EPI_ADAM ? 2 * P16_BLOCK_BYTES
+                                                             : NOUT * EPI_BLOCK_BYTES);
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
   static constexpr size_t BAR_OFF = size_t(STAGES) * STAGE_LOCAL + STAGING;
   static constexpr size_t SMEM = 1024 + BAR_OFF + 512 + 2 * (MAX_GROUPS + 1) * sizeof(int);
@@ -185,8 +191,8 @@ __device__ __forceinline__ uint4* blk_chunk(uint8_t* blk, int r, int j) {
   return reinterpret_cast<uint4*>(blk + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
 }
 
-template <bool A_MN, bool B_MN, int EPI, bool PAIR>
-__global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
+template <bool A_MN, bool B_MN, int EPI, bool PAIR, bool PUSH = false>
+__global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC,
@@ -194,8 +200,10 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
                         const __grid_constant__ CUtensorMap tmMaster,
                         const __grid_constant__ CUtensorMap tmM1,
                         const __grid_constant__ CUtensorMap tmM2, const GemmParams p) {
-  using CF = Cfg<EPI, PAIR>;
+  using CF = Cfg<EPI, PAIR, PUSH>;
   static_assert(!PAIR || A_MN == B_MN || !A_MN, "pair: KDIM (A, B MN-major) or ROWS (A K-major)");
+  static_assert(!PUSH || (!A_MN && !PAIR && (EPI == EPI_STORE || EPI == EPI_BIAS)),
+                "push: single-CTA ROWS GEMMs with the store / bias epilogue");
   constexpr int STAGES = CF::STAGES;
   constexpr int B_LOCAL = CF::B_LOCAL;
   constexpr int EPI_WARPS = CF::EPI_WARPS;
@@ -555,6 +563,80 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
       }
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
+      if constexpr (PUSH) {
+        // ---- push return: stage this warp's 32 rows x SPAN columns (bf16, 16 B chunks
+        // XOR-swizzled by row), free the accumulator, then store whole row segments into
+        // the home ranks' receive buffers over NVLink
+        uint8_t* pst = blk0;
+        const int rowA = row0 + lane;  // this lane's assembled row
+        const int my_home = p.row_home[rowA];
+        const int my_src = my_home >= 0 ? p.row_src[rowA] : 0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < SPAN; c0 += 32) {
+          float v[32];
+          ptx::tmem_ld32(tbase + cq * SPAN + c0, v);
+          if (zero) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          }
+          if (EPI == EPI_BIAS && p.bias != nullptr) {
+            const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride +
+                                     ti.n_blk * BN + cq * SPAN + c0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+              const uint4 bv = *reinterpret_cast<const uint4*>(b + i);
+              const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 f = unpack_bf16(bw[j]);
+                v[i + 2 * j] += f.x;
+                v[i + 2 * j + 1] += f.y;
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 o;
+            o.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+            o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+            o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+            o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+            const int ch = c0 / 8 + j;  // 16 B chunk of the row (SPAN / 8 per row)
+            *reinterpret_cast<uint4*>(pst + lane * (SPAN * 2) + ((ch ^ (lane & 15)) << 4)) = o;
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // the accumulator is in shared memory now
+          if (PAIR) ptx::mbar_arrive_cluster(lead_tempty + acc * 8);
+          else ptx::mbar_arrive(&tempty[acc]);
+        }
+        // 16 lanes per row: 256 B segments, two rows per store instruction
+        const int col0 = ti.n_blk * BN + cq * SPAN;
+        constexpr int CPR = SPAN / 8;  // 16 B chunks per row
+        const int half = lane / CPR, ch = lane % CPR;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; rr += 32 / CPR) {
+          const int r = rr + half;
+          const int dh = __shfl_sync(0xffffffffu, my_home, r);
+          const int src = __shfl_sync(0xffffffffu, my_src, r);
+          if (dh >= 0 && !ti.ghost) {
+            const uint4 o = *reinterpret_cast<const uint4*>(pst + r * (SPAN * 2) +
+                                                              ((ch ^ (r & 15)) << 4));
+            for (int td = 0; td < p.push_T; ++td) {
+              bf16* dst = reinterpret_cast<bf16*>(p.push_peers[td + p.push_T * src]) +
+                          p.push_slot * p.push_slot_stride + int64_t(dh) * p.N + col0 + ch * 8;
+              *reinterpret_cast<uint4*>(dst) = o;
+            }
+          }
+        }
+        __syncwarp();  // the staging is rewritten by the next tile
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = cq * SPAN; c0 < (ti.ghost ? cq * SPAN : (cq + 1) * SPAN); c0 += 32) {
         const int col = ti.n_blk * BN + c0;
@@ -653,6 +735,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR>::THREADS, 1)
       }
     }
     if (lane == 0) ptx::bulk_wait0();
+    if (PUSH) __threadfence_system();  // the pushed rows are visible before the plane barrier
   }
   if (PAIR) {
     ptx::tc_fence_before();
@@ -696,12 +779,12 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
   return r == CUDA_SUCCESS;
 }
 
-template <bool A_MN, bool B_MN, int EPI, bool PAIR = false>
+template <bool A_MN, bool B_MN, int EPI, bool PAIR = false, bool PUSH = false>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                      const CUtensorMap& mx, const CUtensorMap& m0, const CUtensorMap& m1,
                      const CUtensorMap& m2, const GemmParams& p, int grid, cudaStream_t s) {
-  using CF = Cfg<EPI, PAIR>;
-  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI, PAIR>;
+  using CF = Cfg<EPI, PAIR, PUSH>;
+  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI, PAIR, PUSH>;
   static int pair_grid = 0;  // per instantiation: CTAs of the co-resident pairs
   static bool attr_set = false;
   if (!attr_set) {
@@ -828,6 +911,13 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   f0 = f1 = f2 = mc;  // (state blocks move as 1-D bulk copies; the maps are unused)
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
+  if (p.mode == GEMM_ROWS && p.push_peers != nullptr) {  // push return over NVLink
+    if (o.b_mn && p.epi == EPI_BIAS)
+      return launch_t<false, true, EPI_BIAS, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    if (!o.b_mn && p.epi == EPI_STORE)
+      return launch_t<false, false, EPI_STORE, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    return fail("gemm: the push return needs the bias (B MN-major) or store (B K-major) epilogue");
+  }
   if (p.mode == GEMM_ROWS) {
     if (pair_mask() & 2) {  // CTA pairs over 256-row tiles
       if (o.b_mn) {

@@ -102,6 +102,13 @@ struct ted_layer {
   // peer exchange with the plan built on the device (no host round trip per step, so the
   // multi-GPU step is graph-capturable); the host plan is rebuilt lazily for statistics
   bool devplan = false;
+  // push return (device plan only): GEMM2 / dgrad1 epilogues store their TP-partial output
+  // rows straight into the home ranks' receive slots (ret: [T][n][h], IPC-mapped, peer
+  // table 5) over NVLink, overlapped with the GEMM; the combine / gate-dx then read and sum
+  // the T slots locally.  row_home / row_src map assembled rows to home rows / shards.
+  bool push = false;
+  DevBuf<bf16> ret;
+  DevBuf<int> row_home, row_src;
 
   // parameters: expert family (local experts: w1,b1,w2,b2 each) + non-expert (gate)
   Family fam_exp, fam_non;
@@ -443,6 +450,26 @@ const int* peer_clamp(const ted_layer* L) {
   return (L->dtd && L->flags.corrupt_drop) ? L->kc.p + size_t(L->t) * L->E : nullptr;
 }
 
+// push return: the epilogue's destination (receive slots of the home shard's TP members)
+void set_push(ted_layer* L, GemmParams& g) {
+  g.push_peers = peer_table(L, 5);
+  g.row_home = L->row_home.p;
+  g.row_src = L->row_src.p;
+  g.push_T = L->T;
+  g.push_slot = L->t;
+  g.push_slot_stride = int64_t(L->n) * L->h;
+}
+
+// the T pushed partial rows of every token, in this rank's receive slots
+RowSrc ret_src(ted_layer* L) {
+  RowSrc r;
+  r.local = L->ret.p;
+  r.pos_home = L->pos_home.p;
+  r.slot_stride = int64_t(L->n) * L->h;
+  r.nsum = L->T;
+  return r;
+}
+
 RowSrc pull_src(ted_layer* L, int which) {
   RowSrc r;
   r.pos_home = L->pos_home.p;
@@ -575,6 +602,10 @@ void layer_forward_impl(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     check(plan_peer(L->kc_all.p, L->T, L->P, E, L->Tc, L->ep, L->dtd ? L->t : 0, L->seg_off.p,
                     L->disp_base.p, L->disp_base.p + E, s),
           "plan_peer");
+    if (L->push)
+      check(push_map(L->kc_all.p, L->T, L->P, E, L->Tc, L->ep, L->seg_off.p, L->row_home.p,
+                     L->row_src.p, s),
+            "push_map");
     PeerDst pd;
     pd.peers = peer_table(L, 0);
     pd.disp_base = L->disp_base.p;
@@ -705,6 +736,7 @@ void layer_forward_impl(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
   g.ldc = h;
   g.bias = (L->t == 0) ? P + L->off_b2 : nullptr;  // bias after the reduce (parallel_linear.cpp:29)
   g.aux = nullptr;
+  if (L->push) set_push(L, g);  // the return trip inside the epilogue
   run_gemm(o, g, rows, s);
 
   const bf16* fh;
@@ -716,7 +748,7 @@ void layer_forward_impl(ted_layer* L, const bf16* a, bf16* y, cudaStream_t s) {
     // parallel_linear.cpp:28) + combine: every token pulls and sums its expert's T partial
     // rows straight from the replicas' buffers
     L->mark("combine_pull", s);
-    RowSrc src = pull_src(L, 2);
+    RowSrc src = L->push ? ret_src(L) : pull_src(L, 2);
     src.nsum = L->T;
     check(combine_pull(src, L->prob.p, L->n, h, y, L->fhome.p, L->loss_part.p, s),
           "combine_pull");
@@ -972,6 +1004,7 @@ void layer_backward_impl(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s)
   o.ldb = L->fT;
   o.b_group_stride = L->per_expert;
   o.b_mn = false;
+  if (L->push) set_push(L, g);  // dX partials straight to the home ranks
   run_gemm(o, g, rows, s);
   L->mark("wgrad1", s);
   // wgrad of GEMM1: dW1 = X^T dZ
@@ -1005,7 +1038,7 @@ void layer_backward_impl(ted_layer* L, const bf16* dy, bf16* da, cudaStream_t s)
     L->mark("gate_dx", s);
     // return trip of dX pulled from the expert ranks, TP partial sums of the
     // column-parallel dgrad folded in (parallel_linear.cpp:19), + dl Wg^T (moe.cpp:660-685)
-    RowSrc src = pull_src(L, 3);
+    RowSrc src = L->push ? ret_src(L) : pull_src(L, 3);
     src.nsum = L->T;
     check(gate_backward_input(src, L->dlogits.p, L->fam_non.param.p, L->n, h, E, da, s),
           "gate_backward_input");
@@ -1140,8 +1173,19 @@ void setup_peer_exchange(ted_layer* L) {
   L->devplan = !(dp && std::strcmp(dp, "0") == 0);
   const char* bv = std::getenv("TED_BARRIER");
   L->nccl_barrier = bv && std::strcmp(bv, "nccl") == 0;
-  constexpr int NB = 5;  // x_asm, dfe_asm, fe_asm, dx_asm, barrier flags
-  void* mine[NB] = {L->x_asm.p, L->dfe_asm.p, L->fe_asm.p, L->dx_asm.p, L->bar_flags.p};
+  {
+    const char* pv = std::getenv("TED_PUSH");
+    L->push = L->devplan && !(pv && std::strcmp(pv, "0") == 0);
+  }
+  if (L->push) {
+    L->ret.alloc(size_t(L->T) * L->n * L->h);
+    L->row_home.alloc(size_t(L->R_max));
+    L->row_src.alloc(size_t(L->R_max));
+  } else {
+    L->ret.alloc(8);  // (mapped like the others; unused)
+  }
+  constexpr int NB = 6;  // x_asm, dfe_asm, fe_asm, dx_asm, barrier flags, receive slots
+  void* mine[NB] = {L->x_asm.p, L->dfe_asm.p, L->fe_asm.p, L->dx_asm.p, L->bar_flags.p, L->ret.p};
   const int PS = L->plane_size;
   const size_t HB = sizeof(cudaIpcMemHandle_t);
   std::vector<char> hmine(NB * HB), hall(size_t(PS) * NB * HB);
@@ -1163,7 +1207,7 @@ void setup_peer_exchange(ted_layer* L) {
     std::vector<unsigned long long> tab(size_t(NB) * PS);
     for (int r = 0; r < PS; ++r)
       for (int b = 0; b < NB; ++b) {
-        if (b < 4) {
+        if (b < 4) {  // (the receive slots, 5, stay per layer like the barrier flags)
           tab[size_t(b) * PS + r] = st[size_t(b) * PS + r];
           continue;
         }

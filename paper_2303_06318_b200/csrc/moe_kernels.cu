@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) combine_bwd_kernel(
 __device__ __forceinline__ const bf16* src_row(const RowSrc& R, int64_t k, int h, int rep = 0) {
   const int ph = R.pos_home ? R.pos_home[k] : -1;
   if (ph < 0) return nullptr;
-  if (R.peers == nullptr) return R.local + int64_t(ph) * h;
+  if (R.peers == nullptr) return R.local + int64_t(rep) * R.slot_stride + int64_t(ph) * h;
   const int e = R.expert[k];
   int c = 0;
   if (R.Tc > 1) {

@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(kThreads) scatter_peer_kernel(const bf16* __re
 __device__ __forceinline__ const bf16* pull_row(const RowSrc& R, int64_t k, int h, int rep) {
   const int ph = R.pos_home[k];
   if (ph < 0) return nullptr;
+  if (R.peers == nullptr)  // pushed partials in this rank's receive slots
+    return R.local + int64_t(rep) * R.slot_stride + int64_t(ph) * h;
   const int e = R.expert[k];
   int c = 0;
   if (R.Tc > 1) {
@@ -392,9 +394,60 @@ cudaError_t ledger_moe_pass(unsigned long long* led, int phase, int P, int T, in
   return cudaGetLastError();
 }
 
+// Where every row of this rank's assembled buffer goes back to (the push return of the
+// GEMM2 / dgrad1 epilogues): local expert le's segment holds blocks (chunk c, source s)
+// of C(s, c, e) rows in that order (peer_plan_expert); their home rows on every TP member
+// of source shard s are home_base_s(c, e) + i, home_base_s(c, e) = rows of source s's
+// chunks before c + rows of chunk c for experts before e (route_scan's home layout).
+// row_home = -1 for the segment's pad rows.  One CTA per local expert.
+__global__ void push_map_kernel(const int* __restrict__ kc_all, int T, int P, int E, int Tc,
+                                int my_ep, const int* __restrict__ seg, int* __restrict__ row_home,
+                                int* __restrict__ row_src) {
+  const int Eloc = E / P, le = blockIdx.x, e = my_ep * Eloc + le;
+  auto C = [&](int s_, int c, int ee) { return kc_all[(int64_t(T) * s_ * Tc + c) * E + ee]; };
+  __shared__ int s_start[64 * 8], s_cnt[64 * 8], s_home[64 * 8];
+  const int nb = Tc * P;  // <= 8 * 64
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const int c = b / P, s_ = b % P;
+    int hb = 0;
+    for (int c2 = 0; c2 < c; ++c2)
+      for (int e2 = 0; e2 < E; ++e2) hb += C(s_, c2, e2);
+    for (int e2 = 0; e2 < e; ++e2) hb += C(s_, c, e2);
+    s_home[b] = hb;
+    s_cnt[b] = C(s_, c, e);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int r = seg[le];
+    for (int b = 0; b < nb; ++b) {
+      s_start[b] = r;
+      r += s_cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int b = 0; b < nb; ++b) {
+    const int st = s_start[b], cnt = s_cnt[b], hb = s_home[b], s_ = b % P;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      row_home[st + i] = hb + i;
+      row_src[st + i] = s_;
+    }
+  }
+  const int end = seg[le] + seg[Eloc + 1 + le];
+  const int seg_end = le + 1 < Eloc ? seg[le + 1] : seg[Eloc];
+  for (int r = end + threadIdx.x; r < seg_end; r += blockDim.x) row_home[r] = -1;
+}
+
+cudaError_t push_map(const int* kc_all, int T, int P, int E, int Tc, int my_ep, const int* seg,
+                     int* row_home, int* row_src, cudaStream_t s) {
+  if (E % P != 0 || Tc * P > 64 * 8) return cudaErrorInvalidValue;
+  push_map_kernel<<<E / P, 256, 0, s>>>(kc_all, T, P, E, Tc, my_ep, seg, row_home, row_src);
+  count_launch(1);
+  return cudaGetLastError();
+}
+
 cudaError_t combine_pull(const RowSrc& src, const float* prob, int64_t n, int h, bf16* y,
                          bf16* fhome, float* loss_part, cudaStream_t s) {
-  if (h % 8 != 0 || src.peers == nullptr) return cudaErrorInvalidValue;
+  if (h % 8 != 0 || (src.peers == nullptr && src.local == nullptr)) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
   combine_pull_kernel<<<grid, kThreads, 0, s>>>(src, prob, n, h, y, fhome, loss_part);

@@ -68,6 +68,15 @@ struct GemmParams {
   float* colsum_part = nullptr;
   // (EPI_ADAM: master/m1/m2 use the blk_off layout per group, group stride c_group_stride)
   AdamK adam{};
+  // push return (ROWS mode, EPI_STORE / EPI_BIAS): output row r of the assembled buffer is
+  // not stored in C but sent over NVLink to row row_home[r] of slot push_slot in the receive
+  // buffer of every TP member td of its home shard row_src[r]:
+  // push_peers[td + push_T * row_src[r]] + push_slot * push_slot_stride + row_home[r] * N
+  const unsigned long long* push_peers = nullptr;
+  const int* row_home = nullptr;
+  const int* row_src = nullptr;
+  int push_T = 1, push_slot = 0;
+  int64_t push_slot_stride = 0;
 };
 
 struct GemmOperands {
@@ -154,6 +163,9 @@ struct RowSrc {
   // 1: read replica my_t (already TP-reduced);  Tp: sum the row over every TP replica
   // (the row-parallel all-reduce of parallel_linear.cpp:28 folded into the consumer)
   int nsum = 1;
+  // local mode with nsum > 1: the T partial rows were pushed into this rank's receive
+  // buffer by the experts' GEMM epilogues, slot t at local + t * slot_stride
+  int64_t slot_stride = 0;
 };
 // da[k] = row(k) + sum_j dlogits[k][j] Wg[:, j]
 cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const bf16* wg,
@@ -187,6 +199,9 @@ cudaError_t scatter_rows_peer(const bf16* a, const int* pos_send, const int* exp
 cudaError_t plane_barrier_peer(const unsigned long long* flags, int PS, int me,
                                unsigned* epoch_dev, int* fault, unsigned long long timeout_ns,
                                cudaStream_t s);
+// home row (-1: pad) and source EP member of every assembled row, for the push return
+cudaError_t push_map(const int* kc_all, int T, int P, int E, int Tc, int my_ep, const int* seg,
+                     int* row_home, int* row_src, cudaStream_t s);
 // CommLedger entries of one MoE pass (forward / recompute / backward) of this rank, from
 // the device-resident routed counts: led[phase][op][calls, bytes] += ...
 cudaError_t ledger_moe_pass(unsigned long long* led, int phase, int P, int T, int dtd, int Tc,
