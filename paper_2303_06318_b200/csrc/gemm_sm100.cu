@@ -99,9 +99,10 @@ struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
   static constexpr int B_LOCAL = PAIR ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;  // this CTA's B
   static constexpr int STAGE_LOCAL = A_STAGE_BYTES + B_LOCAL;
-  static constexpr int STAGES = PUSH ? 3 : (PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4);
+  static constexpr int STAGES = PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4;
   // AdamW: the parameter half block and (keep-gradients mode) the gradient half block
-  static constexpr size_t PER_WARP = PUSH ? 32 * COL_SPAN * 2
+  static constexpr int PUSH_COLS = 64;  // columns per staged push round (128 B rows)
+  static constexpr size_t PER_WARP = PUSH ? 32 * PUSH_COLS * 2
                                           : (EPI == EPI_ADAM ? 2 * P16_BLOCK_BYTES
                                                              : NOUT * EPI_BLOCK_BYTES);
   static constexpr size_t STAGING = size_t(EPI_WARPS) * PER_WARP;
@@ -564,73 +565,70 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
       const bool zero = ti.k_len == 0;
       const uint32_t tbase = tmem_base + acc * BN + (uint32_t(sp * 32) << 16);
       if constexpr (PUSH) {
-        // ---- push return: stage this warp's 32 rows x SPAN columns (bf16, 16 B chunks
-        // XOR-swizzled by row), free the accumulator, then store whole row segments into
-        // the home ranks' receive buffers over NVLink
+        // ---- push return: in rounds of 64 columns, stage this warp's 32 rows (128 B each)
+        // in shared memory and let every lane send its row segment to each TP member of
+        // the row's home shard with one bulk (TMA-engine) copy over NVLink; the MMAs of the
+        // next tile run meanwhile (the accumulator is released after the last TMEM read)
+        constexpr int PC = CF::PUSH_COLS;
         uint8_t* pst = blk0;
         const int rowA = row0 + lane;  // this lane's assembled row
         const int my_home = p.row_home[rowA];
         const int my_src = my_home >= 0 ? p.row_src[rowA] : 0;
+        const bool send = my_home >= 0 && !ti.ghost;
 #pragma unroll 1
-        for (int c0 = 0; c0 < SPAN; c0 += 32) {
-          float v[32];
-          ptx::tmem_ld32(tbase + cq * SPAN + c0, v);
-          if (zero) {
+        for (int r0 = 0; r0 < SPAN; r0 += PC) {
+          ptx::bulk_wait_read0();  // this lane's previous row copies have read the staging
+          __syncwarp();
+#pragma unroll 1
+          for (int c0 = r0; c0 < r0 + PC; c0 += 32) {
+            float v[32];
+            ptx::tmem_ld32(tbase + cq * SPAN + c0, v);
+            if (zero) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          if (EPI == EPI_BIAS && p.bias != nullptr) {
-            const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride +
-                                     ti.n_blk * BN + cq * SPAN + c0;
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            }
+            if (EPI == EPI_BIAS && p.bias != nullptr) {
+              const __nv_bfloat16* b = p.bias + int64_t(ti.g) * p.bias_group_stride +
+                                       ti.n_blk * BN + cq * SPAN + c0;
 #pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-              const uint4 bv = *reinterpret_cast<const uint4*>(b + i);
-              const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
+              for (int i = 0; i < 32; i += 8) {
+                const uint4 bv = *reinterpret_cast<const uint4*>(b + i);
+                const uint32_t bw[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float2 f = unpack_bf16(bw[j]);
-                v[i + 2 * j] += f.x;
-                v[i + 2 * j + 1] += f.y;
+                for (int j = 0; j < 4; ++j) {
+                  const float2 f = unpack_bf16(bw[j]);
+                  v[i + 2 * j] += f.x;
+                  v[i + 2 * j + 1] += f.y;
+                }
               }
             }
-          }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 o;
-            o.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-            o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-            o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-            o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-            const int ch = c0 / 8 + j;  // 16 B chunk of the row (SPAN / 8 per row)
-            *reinterpret_cast<uint4*>(pst + lane * (SPAN * 2) + ((ch ^ (lane & 15)) << 4)) = o;
-          }
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {  // the accumulator is in shared memory now
-          if (PAIR) ptx::mbar_arrive_cluster(lead_tempty + acc * 8);
-          else ptx::mbar_arrive(&tempty[acc]);
-        }
-        // 16 lanes per row: 256 B segments, two rows per store instruction
-        const int col0 = ti.n_blk * BN + cq * SPAN;
-        constexpr int CPR = SPAN / 8;  // 16 B chunks per row
-        const int half = lane / CPR, ch = lane % CPR;
-#pragma unroll 4
-        for (int rr = 0; rr < 32; rr += 32 / CPR) {
-          const int r = rr + half;
-          const int dh = __shfl_sync(0xffffffffu, my_home, r);
-          const int src = __shfl_sync(0xffffffffu, my_src, r);
-          if (dh >= 0 && !ti.ghost) {
-            const uint4 o = *reinterpret_cast<const uint4*>(pst + r * (SPAN * 2) +
-                                                              ((ch ^ (r & 15)) << 4));
-            for (int td = 0; td < p.push_T; ++td) {
-              bf16* dst = reinterpret_cast<bf16*>(p.push_peers[td + p.push_T * src]) +
-                          p.push_slot * p.push_slot_stride + int64_t(dh) * p.N + col0 + ch * 8;
-              *reinterpret_cast<uint4*>(dst) = o;
+            for (int j = 0; j < 4; ++j) {
+              uint4 o;
+              o.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+              o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+              o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+              o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+              *reinterpret_cast<uint4*>(pst + lane * (PC * 2) + ((c0 - r0) / 8 + j) * 16) = o;
             }
           }
+          ptx::fence_async_smem();  // the staged rows are visible to the bulk-copy engine
+          if (r0 + PC == SPAN) ptx::tc_fence_before();
+          __syncwarp();
+          if (r0 + PC == SPAN && lane == 0) {  // the accumulator is fully read
+            if (PAIR) ptx::mbar_arrive_cluster(lead_tempty + acc * 8);
+            else ptx::mbar_arrive(&tempty[acc]);
+          }
+          if (send) {
+            const int col0 = ti.n_blk * BN + cq * SPAN + r0;
+            for (int td = 0; td < p.push_T; ++td) {
+              bf16* dst = reinterpret_cast<bf16*>(p.push_peers[td + p.push_T * my_src]) +
+                          p.push_slot * p.push_slot_stride + int64_t(my_home) * p.N + col0;
+              ptx::bulk_store_1d(dst, pst + lane * (PC * 2), PC * 2);
+            }
+            ptx::bulk_commit();
+          }
         }
-        __syncwarp();  // the staging is rewritten by the next tile
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -734,7 +732,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
         acc_phase ^= 1;
       }
     }
-    if (lane == 0) ptx::bulk_wait0();
+    if (PUSH || lane == 0) ptx::bulk_wait0();  // (push: every lane tracks its own rows)
     if (PUSH) __threadfence_system();  // the pushed rows are visible before the plane barrier
   }
   if (PAIR) {
