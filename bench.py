@@ -68,6 +68,54 @@ def workload(n_gpus: int, dtd: bool, which: str = "c3"):
                 tokens=32768, tp=tp, ep=ep, cf=1.25, dtd=dtd and tp > 1)
 
 
+def rooflines(w, stage_avg_ms, stats, T, P, D, world):
+    """(roofline, extra) of the step's dominant kernels from the per-stage CUDA-event times.
+    With the expert family unsharded (D = 1) AdamW runs inside the two wgrad GEMMs and that
+    kernel dominates the step (HBM-bound on the optimizer state: 26 B per parameter + the
+    operands once); the four forward / dgrad GEMMs are reported beside it against the
+    sustained tensor-core peak (algorithmic FLOPs 2 x rows x h x f/T per GEMM).  `traffic`
+    comes from a committed ncu --set full capture of the same workload (profiles/)."""
+    pk = peaks()
+
+    def st(k):
+        return stage_avg_ms.get(k, 0.0)
+    Eloc = max(1, w["experts"] // P)
+    kept_rows = sum(stats["kept_per_expert"][:Eloc])
+    f_t = 4 * w["hidden"] // T
+    h_ = w["hidden"]
+    tc_ms = sum(st(k) for k in ["gemm1_fwd", "gemm2_fwd", "dgrad2", "dgrad1"])
+    tc_flops = 8.0 * kept_rows * h_ * f_t
+    tc_ach = tc_flops / (tc_ms / 1e3) / 1e12 if tc_ms > 0 else None
+    peak_tc = pk["bf16_tflops_sustained"]
+    tj = None
+    for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic*.json"))):
+        with open(tp) as f:
+            cand = json.load(f)
+        if cand.get("workload") == w["name"] and cand.get("n_gpus", 1) == world:
+            tj = cand
+    roof_tc = {"bound": "tensor", "kernel": "expert FFN fwd + dgrad tcgen05 GEMMs (4/step)",
+               "achieved": tc_ach, "peak": peak_tc, "unit": "TFLOP/s",
+               "frac": (tc_ach / peak_tc) if tc_ach else None,
+               "traffic": tj.get("tc_per_launch") if tj else None,
+               "flops_per_launch": tc_flops / 4, "ms_per_launch": tc_ms / 4,
+               "peak_source": pk["source"] + " bf16_tflops_sustained"}
+    if D != 1:
+        return roof_tc, {}
+    wg_ms = (st("wgrad1") + st("wgrad2")) / 2
+    params = Eloc * h_ * f_t
+    rows = int(stats["asm_rows"])
+    wg_bytes = 26.0 * params + 2.0 * rows * (h_ + f_t)
+    wg_ach = wg_bytes / (wg_ms / 1e3) / 1e9 if wg_ms > 0 else None
+    roofline = {"bound": "hbm", "kernel": "wgrad GEMM + fused AdamW (2/step)",
+                "achieved": wg_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": (wg_ach / pk["hbm_gbs"]) if wg_ach else None,
+                "traffic": tj.get("wgrad_per_launch") if tj else None,
+                "bytes_per_launch": wg_bytes, "ms_per_launch": wg_ms,
+                "unit_work": "26 B per parameter + 2 B per operand element",
+                "peak_source": pk["source"] + " hbm_gbs (copy)"}
+    return roofline, {"roofline_gemm": roof_tc}
+
+
 def quick_layer_bench(w, steps: int, warmup: int):
     """ms/step of one more single-GPU workload in the same process (graph-replayed step,
     CUDA events), plus its per-stage times from an eager timed pass."""
@@ -97,12 +145,14 @@ def quick_layer_bench(w, steps: int, warmup: int):
     for _ in range(k):
         L.step(a, y, da)
     torch.cuda.synchronize()
-    st = {kk: round(v[0] / k, 4) for kk, v in sorted(L.timing_read().items())}
+    raw = L.timing_read()
+    st = {kk: round(v[0] / k, 4) for kk, v in sorted(raw.items())}
+    roof, extra = rooflines(w, {kk: v[0] / k for kk, v in raw.items()}, L.stats(), 1, 1, 1, 1)
     L.close()
     return {"workload": w["name"], "hidden": w["hidden"], "ffn": 4 * w["hidden"],
             "experts": w["experts"], "tokens": w["tokens"], "capacity_factor": w["cf"],
             "ms_per_step": ms, "tokens_per_s": w["tokens"] / (ms / 1e3), "steps": steps,
-            "stage_ms": st}
+            "stage_ms": st, "roofline": roof, **extra}
 
 
 class ClockSampler:
@@ -577,51 +627,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
     tokens_global = w["tokens"]
     value = tokens_global / (ms / 1e3)
     pk = peaks()
-    # roofline.  With the expert family unsharded (D = 1) AdamW runs inside the two wgrad
-    # GEMMs and that kernel dominates the step (47 % of the GPU time at C3, N=1,
-    # profiles/r02_ncu_summary.md): it is HBM-bound on the optimizer state.  The four
-    # forward / dgrad GEMMs are reported beside it against the tensor-core peak.
-    def st(k):
-        return stages.get(k, (0.0, 0))[0] / nprof
-    Eloc = max(1, w["experts"] // P)
-    kept_rows = sum(stats["kept_per_expert"][:Eloc])
-    f_t = 4 * w["hidden"] // T
-    h_ = w["hidden"]
-    tc_names = ["gemm1_fwd", "gemm2_fwd", "dgrad2", "dgrad1"]
-    tc_ms = sum(st(k) for k in tc_names)
-    tc_flops = 8.0 * kept_rows * h_ * f_t  # 4 GEMMs x 2 flops x rows x h x f/T, algorithmic
-    tc_ach = tc_flops / (tc_ms / 1e3) / 1e12 if tc_ms > 0 else None
-    peak_tc = pk["bf16_tflops_sustained"]
-    tj = None
-    for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gemm_traffic*.json"))):
-        with open(tp) as f:  # from a committed ncu --set full capture of this workload
-            cand = json.load(f)
-        if cand.get("workload") == w["name"] and cand.get("n_gpus", 1) == world:
-            tj = cand
-    roof_tc = {"bound": "tensor", "kernel": "expert FFN fwd + dgrad tcgen05 GEMMs (4/step)",
-               "achieved": tc_ach, "peak": peak_tc, "unit": "TFLOP/s",
-               "frac": (tc_ach / peak_tc) if tc_ach else None,
-               "traffic": (sum(tj["per_launch"][i] for i in (0, 1, 2, 4)) / 4) if tj else None,
-               "flops_per_launch": tc_flops / 4, "ms_per_launch": tc_ms / 4,
-               "peak_source": pk["source"] + " bf16_tflops_sustained"}
-    if D == 1:
-        wg_ms = (st("wgrad1") + st("wgrad2")) / 2
-        params = Eloc * h_ * f_t
-        rows = int(stats["asm_rows"])
-        # 26 B per parameter (fp32 master/m/v read + write, bf16 parameter write) + the
-        # wgrad operands read once (rows x (h + f/T) bf16)
-        wg_bytes = 26.0 * params + 2.0 * rows * (h_ + f_t)
-        wg_ach = wg_bytes / (wg_ms / 1e3) / 1e9 if wg_ms > 0 else None
-        roofline = {"bound": "hbm", "kernel": "wgrad GEMM + fused AdamW (2/step)",
-                    "achieved": wg_ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": (wg_ach / pk["hbm_gbs"]) if wg_ach else None,
-                    "traffic": (sum(tj["per_launch"][i] for i in (3, 5)) / 2) if tj else None,
-                    "bytes_per_launch": wg_bytes, "ms_per_launch": wg_ms,
-                    "unit_work": "26 B per parameter + 2 B per operand element",
-                    "peak_source": pk["source"] + " hbm_gbs (copy)"}
-        extra_roof = {"roofline_gemm": roof_tc}
-    else:
-        roofline, extra_roof = roof_tc, {}
+    roofline, extra_roof = rooflines(w, {k: v[0] / nprof for k, v in stages.items()}, stats, T, P,
+                                     D, world)
     stage_ms = {k: round(v[0] / nprof, 4) for k, v in sorted(stages.items())}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,

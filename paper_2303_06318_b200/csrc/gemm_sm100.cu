@@ -123,12 +123,13 @@ struct TileInfo {
 // k-slices in L2 (row-major order would cover ~2 row blocks x every column block and
 // stream a wide B from HBM once per two row blocks).
 constexpr int kBand = 32;
-__device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, int& n_blk) {
-  const int band = local / (kBand * nt);
-  const int idx = local - band * (kBand * nt);
-  const int rows = min(kBand, mt - band * kBand);
+__device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, int& n_blk,
+                                       int kb = kBand) {
+  const int band = local / (kb * nt);
+  const int idx = local - band * (kb * nt);
+  const int rows = min(kb, mt - band * kb);
   n_blk = idx / rows;
-  m_blk = band * kBand + (idx - n_blk * rows);
+  m_blk = band * kb + (idx - n_blk * rows);
 }
 
 // PAIR: t numbers 256-row tile pairs; this CTA takes row block 2 m + rank
@@ -154,7 +155,7 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
     const int mt = p.M / (PAIR ? 2 * BM : BM);
     const int per = mt * nt;
     ti.g = t / per;
-    raster(t % per, mt, nt, ti.m_blk, ti.n_blk);
+    raster(t % per, mt, nt, ti.m_blk, ti.n_blk, p.band > 0 ? p.band : kBand);
     if (PAIR) ti.m_blk = 2 * ti.m_blk + rank;
     ti.k_len = s_off[ti.g + 1] - s_off[ti.g];
   }
@@ -909,6 +910,13 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   f0 = f1 = f2 = mc;  // (state blocks move as 1-D bulk copies; the maps are unused)
   if (!ok) return fail("gemm: cuTensorMapEncodeTiled failed (alignment/stride?)");
   const int grid = sm_count();
+  if (p.mode == GEMM_KDIM && p.band == 0) {  // (measurement knob: KDIM raster band)
+    static const int band_env = [] {
+      const char* v = std::getenv("TED_GEMM_BAND");
+      return v ? std::atoi(v) : 0;
+    }();
+    const_cast<GemmParams&>(p).band = band_env;
+  }
   if (p.mode == GEMM_ROWS && p.push_peers != nullptr) {  // push return over NVLink
     if (o.b_mn && p.epi == EPI_BIAS)
       return launch_t<false, true, EPI_BIAS, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);

@@ -77,6 +77,7 @@ struct GemmParams {
   const int* row_src = nullptr;
   int push_T = 1, push_slot = 0;
   int64_t push_slot_stride = 0;
+  int band = 0;  // KDIM raster: row blocks (tile pairs) per band (0: the default)
 };
 
 struct GemmOperands {
