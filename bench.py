@@ -392,17 +392,34 @@ def run_reference(args, w, rank, world):
 
 
 def nvlink_bytes(gpu: int):
-    """(tx, rx) NVLink data bytes of this GPU so far (NVML throughput counters, all links),
-    or None when NVML does not expose them."""
+    """(tx, rx) NVLink data bytes of this GPU so far, summed over its links: NVML's
+    throughput counters, else `nvidia-smi nvlink -gt d` (KiB per link); None when neither
+    is exposed."""
     try:
         import pynvml as N
         N.nvmlInit()
         hd = N.nvmlDeviceGetHandleByIndex(gpu)
         vals = N.nvmlDeviceGetFieldValues(hd, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
                                                N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
-        if any(v.nvmlReturn != 0 for v in vals):
-            return None
-        return tuple(int(v.value.ullVal) * 1024 for v in vals)  # KiB counters
+        if all(v.nvmlReturn == 0 for v in vals):
+            return tuple(int(v.value.ullVal) * 1024 for v in vals)  # KiB counters
+    except Exception:
+        pass
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu)],
+                             capture_output=True, text=True, timeout=20).stdout
+        tx = rx = 0
+        seen = False
+        for line in out.splitlines():
+            low = line.lower()
+            num = [t for t in line.replace(":", " ").split() if t.isdigit()]
+            if "tx" in low and num:
+                tx += int(num[-1]) * 1024
+                seen = True
+            elif "rx" in low and num:
+                rx += int(num[-1]) * 1024
+                seen = True
+        return (tx, rx) if seen else None
     except Exception:
         return None
 
