@@ -835,6 +835,12 @@ int pair_mask() {
 
 }  // namespace
 
+// 2-D bf16 K-major tensor map (rows of `cols` elements, `row_bytes` apart), SWIZZLE_128B
+bool tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
+                  uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows) {
+  return make_map(m, base, cols, rows, 1, row_bytes, 0, box_cols, box_rows);
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {

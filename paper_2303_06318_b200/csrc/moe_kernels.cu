@@ -1,5 +1,5 @@
 // moe_kernels.cu -- HBM-bound kernels of the TED MoE layer on sm_100a:
-//   gate (logits + argmax + softmax + per-block expert histogram)   moe.cpp:158-186
+//   gate: argmax + softmax on given logits (the logits themselves: gate_sm100.cu) moe.cpp:158-186
 //   capacity slot scan (exclusive per-expert prefix, ascending)     moe.cpp:454-462 order
 //   dispatch pack (DTD chunk select + scatter into expert layout)   moe.cpp:440-476
 //   combine y = p * f_home, and its backward                        moe.cpp:558-563, :587-597
@@ -107,15 +107,7 @@ __device__ __forceinline__ void stage_wg(const bf16* __restrict__ wg, int E, int
   }
 }
 
-// Gate logits on the tensor cores: logits[16 tokens x 8 experts] per mma.sync.m16n8k16
-// (bf16 x bf16 products exact, fp32 accumulation -- the same arithmetic class as the FMA
-// path, 12 warp instructions per token instead of ~1000, so the kernel is HBM-bound).
-// The K order inside each 32-element step is permuted identically for A and B (a dot
-// product is order-free up to fp32 rounding): quad lane c loads 16 contiguous bytes
-// (elements 8c..8c+7) of its two token rows g and g+8, and MMA m in {0,1} takes elements
-// 8c+4m..8c+4m+3 of the token rows and of the staged Wg^T rows.  CTA = 64 tokens (one
-// routing block), warp = 16 tokens x one half of every 64-element K pair; the two K halves
-// are summed in a fixed order (bit-identical logits on every TP replica).
+// mma.sync.m16n8k16 (bf16 in, fp32 accumulate): the gate backward's small products
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1,
                                                uint32_t a2, uint32_t a3, uint32_t b0,
                                                uint32_t b1) {
@@ -124,187 +116,6 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint3
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-constexpr int kGatePad = 8;  // bf16 padding per staged Wg^T row (spreads the B loads' banks)
-
-template <int EMAX, int U>
-__global__ void __launch_bounds__(kThreads, 2) gate_fwd_mma_kernel(
-    const bf16* __restrict__ a, const bf16* __restrict__ wg, int64_t n, int h, int E, int HC,
-    float* __restrict__ logits, float* __restrict__ probs, int* __restrict__ expert,
-    float* __restrict__ prob, int* __restrict__ blk_hist) {
-  constexpr int NT = EMAX / 8;
-  extern __shared__ __align__(16) uint8_t smem[];
-  float* s_part = reinterpret_cast<float*>(smem);  // [2][kRouteBlock][EMAX]
-  bf16* s_wg = reinterpret_cast<bf16*>(smem + 2 * kRouteBlock * EMAX * sizeof(float));
-  __shared__ int s_hist[64];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, c = lane & 3;
-  const int tt = warp & 3, ks = warp >> 2;
-  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
-  const int64_t ta = tok0 + tt * 16 + g, tb = ta + 8;
-  const bf16* pa = a + (ta < n ? ta : 0) * int64_t(h) + 8 * c;
-  const bf16* pb = a + (tb < n ? tb : 0) * int64_t(h) + 8 * c;
-  const bool va = ta < n, vb = tb < n;
-  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
-  const int HCP = HC + kGatePad;
-  float acc[NT][4];
-#pragma unroll
-  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-
-  for (int c0 = 0; c0 < h; c0 += HC) {
-    const int hc = min(HC, h - c0);
-    __syncthreads();
-    stage_wg<EMAX>(wg, E, c0, hc, HCP, s_wg);  // s_wg[e][i] = Wg[c0 + i][e], zero e >= E
-    __syncthreads();
-    const int steps = hc / 32;  // 32-element K steps; this warp takes ks, ks + 2, ...
-    uint4 cur[U][2], nxt[U][2];
-    auto load = [&](int s0, uint4 (&d)[U][2]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int st = s0 + 2 * u;
-        const int64_t off = c0 + int64_t(st) * 32;
-        const bool in = st < steps;
-        d[u][0] = (in && va) ? ldg_stream(pa + off) : make_uint4(0, 0, 0, 0);
-        d[u][1] = (in && vb) ? ldg_stream(pb + off) : make_uint4(0, 0, 0, 0);
-      }
-    };
-    load(ks, cur);
-    for (int s0 = ks; s0 < steps; s0 += 2 * U) {
-      load(s0 + 2 * U, nxt);
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int st = s0 + 2 * u;
-        if (st >= steps) break;
-        const uint32_t* xa = reinterpret_cast<const uint32_t*>(&cur[u][0]);
-        const uint32_t* xb = reinterpret_cast<const uint32_t*>(&cur[u][1]);
-        const bf16* wrow = s_wg + g * HCP + st * 32 + 8 * c;
-#pragma unroll
-        for (int m = 0; m < 2; ++m) {
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const uint2 bw = *reinterpret_cast<const uint2*>(wrow + nt * 8 * HCP + 4 * m);
-            mma_bf16_16816(acc[nt], xa[2 * m], xb[2 * m], xa[2 * m + 1], xb[2 * m + 1], bw.x,
-                           bw.y);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        cur[u][0] = nxt[u][0];
-        cur[u][1] = nxt[u][1];
-      }
-    }
-  }
-  // partial logits of this K half: token rows g / g+8, experts nt*8 + 2c (+1)
-  float* sp = s_part + ks * (kRouteBlock * EMAX);
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int e = nt * 8 + 2 * c;
-    sp[(tt * 16 + g) * EMAX + e] = acc[nt][0];
-    sp[(tt * 16 + g) * EMAX + e + 1] = acc[nt][1];
-    sp[(tt * 16 + g + 8) * EMAX + e] = acc[nt][2];
-    sp[(tt * 16 + g + 8) * EMAX + e + 1] = acc[nt][3];
-  }
-  __syncthreads();
-  for (int t = 0; t < kWarpTok; ++t) {
-    const int lt = warp * kWarpTok + t;
-    const int64_t k = tok0 + lt;
-    if (k >= n) break;
-    const float* l0 = s_part + lt * EMAX;
-    const float* l1 = l0 + kRouteBlock * EMAX;
-    const float l0v = lane < E ? l0[lane] + l1[lane] : 0.f;
-    const float l1v = lane + 32 < E ? l0[lane + 32] + l1[lane + 32] : 0.f;
-    const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
-    if (lane == 0) atomicAdd(&s_hist[best], 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
-}
-
-// Same logits (bit for bit: identical products, K permutation and accumulation order),
-// with Wg^T read straight from global memory -- pre-transposed once per call into
-// wgT [EMAX][h] (zero rows e >= E), small enough (<= 128 KB) to stay in L1 / L2 -- instead
-// of being re-staged into shared memory by every 64-token CTA behind two barriers: the
-// token rows stream from HBM without stalls, U 32-element K steps in flight per warp.
-template <int EMAX, int U>
-__global__ void __launch_bounds__(kThreads, 2) gate_fwd_l1_kernel(
-    const bf16* __restrict__ a, const bf16* __restrict__ wgT, int64_t n, int h, int E,
-    float* __restrict__ logits, float* __restrict__ probs, int* __restrict__ expert,
-    float* __restrict__ prob, int* __restrict__ blk_hist) {
-  constexpr int NT = EMAX / 8;
-  __shared__ float s_part[2][kRouteBlock][EMAX];
-  __shared__ int s_hist[64];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, c = lane & 3;
-  const int tt = warp & 3, ks = warp >> 2;
-  const int64_t tok0 = int64_t(blockIdx.x) * kRouteBlock;
-  const int64_t ta = tok0 + tt * 16 + g, tb = ta + 8;
-  const bf16* pa = a + (ta < n ? ta : 0) * int64_t(h) + 8 * c;
-  const bf16* pb = a + (tb < n ? tb : 0) * int64_t(h) + 8 * c;
-  const bool va = ta < n, vb = tb < n;
-  if (threadIdx.x < 64) s_hist[threadIdx.x] = 0;
-  float acc[NT][4];
-#pragma unroll
-  for (int i = 0; i < NT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  const bf16* wb = wgT + int64_t(g) * h + 8 * c;  // expert nt*8 + g, K offset 8c
-  const int steps = h / 32;  // this warp takes K steps ks, ks + 2, ...
-  uint4 cur[U][2], nxt[U][2];
-  auto load = [&](int s0, uint4 (&d)[U][2]) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int st = s0 + 2 * u;
-      const int64_t off = int64_t(st) * 32;
-      const bool in = st < steps;
-      d[u][0] = (in && va) ? ldg_stream(pa + off) : make_uint4(0, 0, 0, 0);
-      d[u][1] = (in && vb) ? ldg_stream(pb + off) : make_uint4(0, 0, 0, 0);
-    }
-  };
-  load(ks, cur);
-  for (int s0 = ks; s0 < steps; s0 += 2 * U) {
-    load(s0 + 2 * U, nxt);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int st = s0 + 2 * u;
-      if (st >= steps) break;
-      const uint32_t* xa = reinterpret_cast<const uint32_t*>(&cur[u][0]);
-      const uint32_t* xb = reinterpret_cast<const uint32_t*>(&cur[u][1]);
-      const bf16* wrow = wb + st * 32;
-#pragma unroll
-      for (int m = 0; m < 2; ++m) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const uint2 bw = __ldg(reinterpret_cast<const uint2*>(wrow + int64_t(nt) * 8 * h + 4 * m));
-          mma_bf16_16816(acc[nt], xa[2 * m], xb[2 * m], xa[2 * m + 1], xb[2 * m + 1], bw.x, bw.y);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      cur[u][0] = nxt[u][0];
-      cur[u][1] = nxt[u][1];
-    }
-  }
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const int e = nt * 8 + 2 * c;
-    s_part[ks][tt * 16 + g][e] = acc[nt][0];
-    s_part[ks][tt * 16 + g][e + 1] = acc[nt][1];
-    s_part[ks][tt * 16 + g + 8][e] = acc[nt][2];
-    s_part[ks][tt * 16 + g + 8][e + 1] = acc[nt][3];
-  }
-  __syncthreads();
-  for (int t = 0; t < kWarpTok; ++t) {
-    const int lt = warp * kWarpTok + t;
-    const int64_t k = tok0 + lt;
-    if (k >= n) break;
-    const float l0v = lane < E ? s_part[0][lt][lane] + s_part[1][lt][lane] : 0.f;
-    const float l1v = 0.f;  // EMAX <= 32
-    const int best = select_softmax(l0v, l1v, E, lane, k, logits, probs, expert, prob);
-    if (lane == 0) atomicAdd(&s_hist[best], 1);
-  }
-  __syncthreads();
-  if (threadIdx.x < E) blk_hist[int64_t(blockIdx.x) * E + threadIdx.x] = s_hist[threadIdx.x];
 }
 
 // wgT[e][k] = Wg[k][e] (e < E), 0 (E <= e < EMAX)
@@ -1363,8 +1174,7 @@ void smem_attr(K k, size_t bytes) {
 
 // ================================================================== launchers
 size_t gate_wgt_elems(int h, int E) {
-  const int em = E <= 8 ? 8 : 16;
-  return (E <= 16 && size_t(em) * h * 2 <= (128u << 10)) ? size_t(em) * h : 0;
+  return (E >= 1 && E <= 64 && h % 64 == 0) ? size_t(gate_tc_experts(E)) * h : 0;
 }
 
 cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
@@ -1373,33 +1183,12 @@ cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E,
   if (E < 1 || E > 64 || h % 256 != 0) return cudaErrorInvalidValue;
   const int grid = ceil_div(n, kRouteBlock);
   if (grid == 0) return cudaSuccess;
-  if (wgT != nullptr && gate_wgt_elems(h, E) > 0) {
-    const int em = E <= 8 ? 8 : 16;
-    wg_transpose_kernel<<<ceil_div(h, 256), 256, 0, s>>>(wg, h, E, em, wgT);
-    if (em == 8)
-      gate_fwd_l1_kernel<8, 4><<<grid, kThreads, 0, s>>>(a, wgT, n, h, E, logits, probs, expert,
-                                                         prob, blk_hist);
-    else
-      gate_fwd_l1_kernel<16, 4><<<grid, kThreads, 0, s>>>(a, wgT, n, h, E, logits, probs, expert,
-                                                          prob, blk_hist);
-    count_launch(2);
-    return cudaGetLastError();
-  }
-#define TED_GATE(EM, U)                                                                       \
-  {                                                                                           \
-    const int HC = std::min(((h + 255) / 256) * 256, EM <= 16 ? 2048 : (EM <= 32 ? 1024 : 512)); \
-    const size_t sm = 2 * kRouteBlock * EM * sizeof(float) + size_t(EM) * (HC + kGatePad) * 2; \
-    smem_attr(gate_fwd_mma_kernel<EM, U>, sm);                                                \
-    gate_fwd_mma_kernel<EM, U><<<grid, kThreads, sm, s>>>(a, wg, n, h, E, HC, logits, probs,  \
-                                                          expert, prob, blk_hist);            \
-  }
-  if (E <= 8) TED_GATE(8, 4)
-  else if (E <= 16) TED_GATE(16, 4)
-  else if (E <= 32) TED_GATE(32, 2)
-  else TED_GATE(64, 2)
-#undef TED_GATE
+  if (wgT == nullptr || gate_wgt_elems(h, E) == 0) return cudaErrorInvalidValue;
+  // tcgen05 logits (gate_sm100.cu) on the transposed gate weight
+  const int em = gate_tc_experts(E);
+  wg_transpose_kernel<<<ceil_div(h, 256), 256, 0, s>>>(wg, h, E, em, wgT);
   count_launch(1);
-  return cudaGetLastError();
+  return gate_forward_tc(a, wgT, n, h, E, logits, probs, expert, prob, blk_hist, s);
 }
 
 cudaError_t gate_route_logits(const float* logits, int64_t n, int E, float* probs, int* expert,

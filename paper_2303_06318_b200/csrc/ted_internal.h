@@ -1,6 +1,7 @@
 // ted_internal.h -- internal (C++) declarations shared by the TED kernels and the host
 // driver.  Not part of the C ABI (that is include/ted.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -91,6 +92,9 @@ struct GemmOperands {
 };
 
 int sm_count();
+// 2-D bf16 K-major TMA map (SWIZZLE_128B), boxes of box_cols x box_rows (gemm_sm100.cu)
+bool tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
+                  uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows);
 // max_rows = number of rows the A/B row dimension spans (for the TMA bounds).
 cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_rows,
                          cudaStream_t s, const char** why);
@@ -100,9 +104,15 @@ constexpr int kRouteBlock = 64;  // tokens per routing block (gate / scan / disp
 constexpr int kPad = 128;         // expert segments are padded to the GEMM M tile
 
 // top-1 gate: logits = a Wg (fp32 accumulate), argmax (lowest index on ties), softmax.
-// wgT: scratch of gate_wgt_elems(h, E) bf16 (0: not used -- the shared-memory-staged
-// variant runs); with it Wg^T is transposed once and read from L1 by every CTA.
+// wgT: scratch of gate_wgt_elems(h, E) bf16 (nullptr: the mma.sync variant with the gate
+// weight staged in shared memory runs); with it Wg^T is transposed once per call and the
+// logits run on tcgen05 with TMA-streamed token rows (gate_sm100.cu).
 size_t gate_wgt_elems(int h, int E);
+// the tcgen05 gate (gate_sm100.cu): wgT [gate_tc_experts(E)][h], zero rows e >= E
+int gate_tc_experts(int E);
+cudaError_t gate_forward_tc(const bf16* a, const bf16* wgT, int64_t n, int h, int E,
+                            float* logits, float* probs, int* expert, float* prob,
+                            int* blk_hist, cudaStream_t s);
 cudaError_t gate_forward(const bf16* a, const bf16* wg, int64_t n, int h, int E, float* logits,
                          float* probs, int* expert, float* prob, int* blk_hist, bf16* wgT,
                          cudaStream_t s);
