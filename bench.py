@@ -116,6 +116,54 @@ def rooflines(w, stage_avg_ms, stats, T, P, D, world):
     return roofline, {"roofline_gemm": roof_tc}
 
 
+def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
+    """A parity check at the benched configuration (one GPU), after the timed steps: one
+    more forward on the same tokens, then, in fp64 numpy on the layer's current bf16
+    parameters (MoeRank's MoE branch, moe.cpp:435-563, restated here -- bench.py does not
+    run the test oracle on this path): the routing of EVERY token must equal the argmax of
+    the GPU's own fp32 logits (lowest index on ties), and y of `tokens` sampled kept tokens
+    must match p * (gelu(a W1_e + b1_e) W2_e + b2_e) within rel-L2 2e-2 (bf16 storage of
+    X, Z, H, F; fp32 accumulation)."""
+    import numpy as np
+    import torch
+    y = torch.empty_like(a)
+    L.forward(a, y)
+    torch.cuda.synchronize()
+    r = L.routing()
+    lg = r["logits"]
+    exp_route = np.argmax(lg, axis=1)  # numpy argmax: first maximum = lowest index
+    routing_ok = bool(np.array_equal(exp_route, r["expert"]))
+    h, f = w["hidden"], 4 * w["hidden"]
+    kept = np.nonzero(r["pos_home"] >= 0)[0]
+    rng = np.random.default_rng(seed)
+    pick = rng.choice(kept, size=min(tokens, len(kept)), replace=False)
+    av = a.float().cpu().numpy().astype(np.float64)
+    yv = y.float().cpu().numpy().astype(np.float64)
+
+    def bf16(x):
+        return torch.from_numpy(np.asarray(x, np.float32)).bfloat16().float().numpy().astype(np.float64)
+    cache, num, den = {}, 0.0, 0.0
+    for k in sorted(pick, key=lambda k: r["expert"][k]):
+        e = int(r["expert"][k])
+        if e not in cache:
+            cache.clear()
+            cache[e] = {nm: L.get_param(f"layer0.expert{e}.{nm}").astype(np.float64)
+                        for nm in ("w1", "b1", "w2", "b2")}
+        W = cache[e]
+        z = av[k] @ W["w1"].reshape(h, f) + W["b1"]  # (the epilogue applies GELU before rounding)
+        g = bf16(0.5 * z * (1 + np.tanh(0.7978845608028654 * (z + 0.044715 * z ** 3))))
+        fo = bf16(g @ W["w2"].reshape(f, h) + W["b2"])
+        ref = r["prob"][k] * fo
+        num += float(np.sum((yv[k] - ref) ** 2))
+        den += float(np.sum(ref ** 2))
+    rel = (num / max(den, 1e-300)) ** 0.5
+    return {"routing_bit_exact_all_tokens": routing_ok, "y_rel_l2_sampled": rel,
+            "tokens_sampled": int(len(pick)), "tolerance": 2e-2,
+            "pass": bool(routing_ok and rel < 2e-2),
+            "check": "routing of all tokens vs argmax of the GPU logits; y of sampled kept "
+                     "tokens vs fp64 numpy on the layer's bf16 parameters"}
+
+
 def quick_layer_bench(w, steps: int, warmup: int):
     """ms/step of one more single-GPU workload in the same process (graph-replayed step,
     CUDA events), plus its per-stage times from an eager timed pass."""
@@ -507,6 +555,7 @@ def run_ours(args, w, rank, world, local_rank, dist):
     ms = max_over_ranks(ms)
     stats = L.stats()
     loss = L.loss()
+    parity = sampled_parity(L, a, w, T, P) if world == 1 and not args.no_parity else None
 
     # e2e through the public API: every step's tokens are copied from pinned host memory
     # (on a copy stream into one of two device buffers, so step i+1's H2D runs under step
@@ -671,6 +720,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
         "clocks": clk.summary(),
         "switches": ted_switches(),
     }
+    if parity is not None:
+        line["parity"] = parity
     if dtd_cmp is not None:
         line["dtd_compare"] = dtd_cmp
     if world > 1:
@@ -784,6 +835,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2, help="c4: layers of the stack")
     ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] side line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled parity check")
     ap.add_argument("--no-dtd-compare", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
