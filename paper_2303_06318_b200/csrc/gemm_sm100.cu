@@ -132,8 +132,9 @@ __device__ __forceinline__ void raster(int local, int mt, int nt, int& m_blk, in
   m_blk = band * kb + (idx - n_blk * rows);
 }
 
-// PAIR: t numbers 256-row tile pairs; this CTA takes row block 2 m + rank
-template <bool PAIR = false>
+// PAIR: t numbers 256-row tile pairs; this CTA takes row block 2 m + rank.
+// MCA (ROWS): t numbers row-tile x column-block pairs; this CTA takes column block 2 n + rank
+template <bool PAIR = false, bool MCA = false>
 __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_off,
                                             const int* s_tstart, int total, int t, TileInfo& ti,
                                             int rank = 0) {
@@ -144,7 +145,9 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
     while (g + 1 < p.groups && s_tstart[g + 1] <= t) ++g;
     ti.g = g;
     const int blocks = (s_off[g + 1] - s_off[g]) / BM;
-    raster(t - s_tstart[g], PAIR ? (blocks + 1) / 2 : blocks, nt, ti.m_blk, ti.n_blk);
+    raster(t - s_tstart[g], PAIR ? (blocks + 1) / 2 : blocks, MCA ? nt / 2 : nt, ti.m_blk,
+           ti.n_blk);
+    if (MCA) ti.n_blk = 2 * ti.n_blk + rank;
     if (PAIR) {
       ti.pair_ghost = 2 * ti.m_blk + 1 >= blocks;
       ti.m_blk = 2 * ti.m_blk + rank;
@@ -193,7 +196,7 @@ __device__ __forceinline__ uint4* blk_chunk(uint8_t* blk, int r, int j) {
   return reinterpret_cast<uint4*>(blk + r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
 }
 
-template <bool A_MN, bool B_MN, int EPI, bool PAIR, bool PUSH = false>
+template <bool A_MN, bool B_MN, int EPI, bool PAIR, bool PUSH = false, bool MCA = false>
 __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
@@ -206,6 +209,10 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
   static_assert(!PAIR || A_MN == B_MN || !A_MN, "pair: KDIM (A, B MN-major) or ROWS (A K-major)");
   static_assert(!PUSH || (!A_MN && !PAIR && (EPI == EPI_STORE || EPI == EPI_BIAS)),
                 "push: single-CTA ROWS GEMMs with the store / bias epilogue");
+  // MCA: a 1x2 cluster over adjacent column blocks of one row tile; each CTA loads half of
+  // the shared A tile and multicasts it to both (a sixth less L2 -> shared-memory traffic)
+  static_assert(!MCA || (!A_MN && !PAIR && !PUSH), "multicast A: single-CTA-MMA ROWS GEMMs");
+  constexpr bool CLU = PAIR || MCA;  // launched as 2-CTA clusters
   constexpr int STAGES = CF::STAGES;
   constexpr int B_LOCAL = CF::B_LOCAL;
   constexpr int EPI_WARPS = CF::EPI_WARPS;
@@ -227,9 +234,9 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // CTA pair: both CTAs walk the same tile sequence; rank 0 issues the MMAs
-  const int rank = PAIR ? int(ptx::cluster_rank()) : 0;
-  const int tile0 = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);
-  const int tstep = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+  const int rank = CLU ? int(ptx::cluster_rank()) : 0;
+  const int tile0 = CLU ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int tstep = CLU ? int(gridDim.x >> 1) : int(gridDim.x);
 
   // group table (device-resident counts: no host sync on the routing result)
   for (int i = threadIdx.x; i <= p.groups; i += blockDim.x) s_off[i] = p.seg_off[i];
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     for (int g = 0; g < p.groups; ++g) {
       s_tstart[g] = acc;
       const int blocks = (s_off[g + 1] - s_off[g]) / BM;
-      if (p.mode == GEMM_ROWS) acc += (PAIR ? (blocks + 1) / 2 : blocks) * nt;
+      if (p.mode == GEMM_ROWS) acc += (PAIR ? (blocks + 1) / 2 : blocks) * (MCA ? nt / 2 : nt);
       else acc += (p.M / (PAIR ? 2 * BM : BM)) * nt;
     }
     s_tstart[p.groups] = acc;
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     if (EPI == EPI_BIAS_GELU || EPI == EPI_DGELU) ptx::prefetch_tmap(&tmAux);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], MCA ? 2 : 1);  // MCA: both CTAs' MMAs read the multicast A
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
@@ -265,6 +272,10 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     if (warp == 2) ptx::tmem_alloc_pair(s_tmem, TMEM_COLS);
     ptx::tc_fence_before();
     ptx::cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  } else if (MCA) {
+    if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // the peer's barriers exist before our multicast signals them
   } else {
     if (warp == 2) ptx::tmem_alloc(s_tmem, TMEM_COLS);
     ptx::tc_fence_before();
@@ -285,7 +296,8 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     TileInfo ti;
     // pair: the completion bytes of both CTAs' loads count on the leader's full barrier
     const uint32_t lead_full = PAIR ? ptx::mapa(&full[0], 0) : 0;
-    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti, rank); t += tstep) {
+    for (int t = tile0; decode_tile<PAIR, MCA>(p, s_off, s_tstart, total, t, ti, rank);
+         t += tstep) {
       const int kb_n = ti.k_len / BK;
       for (int kb = 0; kb < kb_n; ++kb) {
         ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -326,7 +338,11 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
           if (p.mode == GEMM_ROWS) {
             const int row0 = s_off[ti.g] + ti.m_blk * BM;
             const int k0 = kb * BK;
-            ptx::tma_load_3d(a_dst, &tmA, &full[stage], k0, row0, 0);  // A K-major
+            if (MCA)  // my half of the shared A tile, into both CTAs (A K-major, 128 B rows)
+              ptx::tma_load_3d_mc(a_dst + rank * (A_STAGE_BYTES / 2), &tmA, &full[stage], k0,
+                                  row0 + rank * (BM / 2), 0, uint16_t(3));
+            else
+              ptx::tma_load_3d(a_dst, &tmA, &full[stage], k0, row0, 0);  // A K-major
             if (B_MN) {
 #pragma unroll
               for (int i = 0; i < BN / 64; ++i)
@@ -354,7 +370,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 && rank == 0) {
+  } else if (warp == 1 && (!PAIR || rank == 0)) {  // (a CTA pair: the leader issues)
     // ------------------------------------------------------------ MMA issuer
     // The whole warp walks the schedule (every value below is warp-uniform, so it lives in
     // uniform registers) and one elected lane issues: a single-lane loop made the compiler
@@ -373,7 +389,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     TileInfo ti;
-    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti); t += tstep) {
+    for (int t = tile0; decode_tile<PAIR, MCA>(p, s_off, s_tstart, total, t, ti); t += tstep) {
       ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
       ptx::tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
@@ -393,6 +409,7 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
           }
           // frees the smem slot (in both CTAs of a pair) when these MMAs finish
           if (PAIR) ptx::umma_commit_pair(&empty[stage]);
+          else if (MCA) ptx::umma_commit_mc(&empty[stage], uint16_t(3));  // both producers
           else ptx::umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -552,7 +569,8 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     uint32_t acc_phase = 0, zphase = 0;
     TileInfo ti;
     const uint32_t lead_tempty = PAIR ? ptx::mapa(&tempty[0], 0) : 0;
-    for (int t = tile0; decode_tile<PAIR>(p, s_off, s_tstart, total, t, ti, rank); t += tstep) {
+    for (int t = tile0; decode_tile<PAIR, MCA>(p, s_off, s_tstart, total, t, ti, rank);
+         t += tstep) {
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       int row0, gz;
@@ -736,7 +754,11 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     if (PUSH || lane == 0) ptx::bulk_wait0();  // (push: every lane tracks its own rows)
     if (PUSH) __threadfence_system();  // the pushed rows are visible before the plane barrier
   }
-  if (PAIR) {
+  if (MCA) {
+    __syncthreads();
+    ptx::cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+    if (warp == 2) ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  } else if (PAIR) {
     ptx::tc_fence_before();
     ptx::cluster_sync();  // the leader's MMAs read the peer's smem until the last tile
     ptx::tc_fence_after();
@@ -778,12 +800,12 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64
   return r == CUDA_SUCCESS;
 }
 
-template <bool A_MN, bool B_MN, int EPI, bool PAIR = false, bool PUSH = false>
+template <bool A_MN, bool B_MN, int EPI, bool PAIR = false, bool PUSH = false, bool MCA = false>
 cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                      const CUtensorMap& mx, const CUtensorMap& m0, const CUtensorMap& m1,
                      const CUtensorMap& m2, const GemmParams& p, int grid, cudaStream_t s) {
   using CF = Cfg<EPI, PAIR, PUSH>;
-  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI, PAIR, PUSH>;
+  auto k = grouped_gemm_kernel<A_MN, B_MN, EPI, PAIR, PUSH, MCA>;
   static int pair_grid = 0;  // per instantiation: CTAs of the co-resident pairs
   static bool attr_set = false;
   if (!attr_set) {
@@ -792,7 +814,7 @@ cudaError_t launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtenso
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  if (!PAIR) {
+  if (!PAIR && !MCA) {
     k<<<grid, CF::THREADS, CF::SMEM, s>>>(ma, mb, mc, mx, m0, m1, m2, p);
     count_launch(1);
     return cudaGetLastError();
@@ -831,6 +853,18 @@ int pair_mask() {
     return v ? std::atoi(v) : 1;
   }();
   return m;
+}
+
+// ROWS GEMMs as 1x2 clusters sharing (multicasting) the A tile: TED_GEMM_MCA=1.  Off by
+// default: 1.5 % slower forward / dgrad GEMMs at C3 (same-box A/B, 2 reps) -- the A tile is
+// only a third of a stage, and the coupled clusters lose more to synchronisation than the
+// saved L2 reads give back under the power cap.
+bool mca_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("TED_GEMM_MCA");
+    return v && std::strcmp(v, "1") == 0;
+  }();
+  return on;
 }
 
 }  // namespace
@@ -883,8 +917,11 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
   CUtensorMap ma, mb, mc, mx, f0, f1, f2;
   bool ok;
   const auto SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  // ROWS GEMMs on 1x2 clusters multicasting A (not with the push return)
+  const bool mca = p.mode == GEMM_ROWS && p.push_peers == nullptr && !(pair_mask() & 2) &&
+                   mca_on() && (p.N / BN) % 2 == 0;
   if (p.mode == GEMM_ROWS) {
-    ok = make_map(&ma, o.A, p.K, rows, 1, o.lda * 2, 0, BK, BM);
+    ok = make_map(&ma, o.A, p.K, rows, 1, o.lda * 2, 0, BK, mca ? BM / 2 : BM);
     if (o.b_mn)
       ok = ok && make_map(&mb, o.B, p.N, p.K, p.groups, o.ldb * 2, o.b_group_stride * 2, 64, BK);
     else  // a CTA pair stages half of B's columns per CTA
@@ -929,6 +966,20 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
     if (!o.b_mn && p.epi == EPI_STORE)
       return launch_t<false, false, EPI_STORE, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
     return fail("gemm: the push return needs the bias (B MN-major) or store (B K-major) epilogue");
+  }
+  if (mca) {
+    if (o.b_mn) {
+      if (p.epi == EPI_BIAS_GELU)
+        return launch_t<false, true, EPI_BIAS_GELU, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      if (p.epi == EPI_BIAS)
+        return launch_t<false, true, EPI_BIAS, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+      return launch_t<false, true, EPI_STORE, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    }
+    if (p.epi == EPI_DGELU)
+      return launch_t<false, false, EPI_DGELU, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    if (p.epi == EPI_BIAS)
+      return launch_t<false, false, EPI_BIAS, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
+    return launch_t<false, false, EPI_STORE, false, false, true>(ma, mb, mc, mx, f0, f1, f2, p, grid, s);
   }
   if (p.mode == GEMM_ROWS) {
     if (pair_mask() & 2) {  // CTA pairs over 256-row tiles
