@@ -440,9 +440,9 @@ def run_reference(args, w, rank, world):
 
 
 def nvlink_bytes(gpu: int):
-    """(tx, rx) NVLink data bytes of this GPU so far, summed over its links: NVML's
-    throughput counters, else `nvidia-smi nvlink -gt d` (KiB per link); None when neither
-    is exposed."""
+    """(tx, rx) NVLink data bytes of this GPU so far (NVML throughput counters, all links), or
+    None when NVML does not expose them.  Read outside the timed regions (before the barrier
+    that starts them): a slow query on one rank would otherwise skew the ranks' start."""
     try:
         import pynvml as N
         N.nvmlInit()
@@ -450,26 +450,11 @@ def nvlink_bytes(gpu: int):
         vals = N.nvmlDeviceGetFieldValues(hd, [N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
                                                N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX])
         if all(v.nvmlReturn == 0 for v in vals):
-            return tuple(int(v.value.ullVal) * 1024 for v in vals)  # KiB counters
+            out = tuple(int(v.value.ullVal) * 1024 for v in vals)  # KiB counters
+            return out if any(out) else None
     except Exception:
         pass
-    try:
-        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu)],
-                             capture_output=True, text=True, timeout=20).stdout
-        tx = rx = 0
-        seen = False
-        for line in out.splitlines():
-            low = line.lower()
-            num = [t for t in line.replace(":", " ").split() if t.isdigit()]
-            if "tx" in low and num:
-                tx += int(num[-1]) * 1024
-                seen = True
-            elif "rx" in low and num:
-                rx += int(num[-1]) * 1024
-                seen = True
-        return (tx, rx) if seen else None
-    except Exception:
-        return None
+    return None
 
 
 def ted_switches():
@@ -524,10 +509,10 @@ def run_ours(args, w, rank, world, local_rank, dist):
     for _ in range(args.warmup):
         L.step(a, y, da)
     torch.cuda.synchronize()
+    nv0 = nvlink_bytes(local_rank) if world > 1 else None
     barrier()
     torch.cuda.synchronize()
     launches0 = ted.kernel_launches()
-    nv0 = nvlink_bytes(local_rank) if world > 1 else None
     with ClockSampler(local_rank) as clk:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -616,10 +601,10 @@ def run_ours(args, w, rank, world, local_rank, dist):
             for _ in range(3):
                 Lx.step(a, y, da)
             torch.cuda.synchronize()
-            barrier()
             nv0 = nvlink_bytes(local_rank)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             Lx.ledger(reset=True)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             for _ in range(kx):
                 Lx.step(a, y, da)
