@@ -76,6 +76,18 @@ __device__ __forceinline__ float4 ld_state(const float* p, uint64_t pol) {
                : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ float4 ld_state_plain(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_state_plain(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_state(float* p, float4 v, uint64_t pol) {
   asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::
                    "l"(p),
@@ -296,6 +308,10 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     TileInfo ti;
     // pair: the completion bytes of both CTAs' loads count on the leader's full barrier
     const uint32_t lead_full = PAIR ? ptx::mapa(&full[0], 0) : 0;
+    // AdamW wgrad: operand loads marked evict-last (the 26 B/parameter state stream would
+    // otherwise push the re-read operand tiles out of L2)
+    const bool op_hint = EPI == EPI_ADAM && p.operand_hint != 0;
+    const uint64_t op_pol = op_hint ? ptx::evict_last_policy() : 0;
     for (int t = tile0; decode_tile<PAIR, MCA>(p, s_off, s_tstart, total, t, ti, rank);
          t += tstep) {
       const int kb_n = ti.k_len / BK;
@@ -312,13 +328,25 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
             const int ncol = ti.n_blk * BN + rank * (BN / 2);  // this CTA's half of B's columns
             if (A_MN) {  // KDIM
               const int krow = s_off[ti.g] + kb * BK;
+              if (op_hint) {  // operands stay in L2 while the AdamW state streams through
 #pragma unroll
-              for (int i = 0; i < BM / 64; ++i)
-                ptx::tma_load_3d_pair(a_dst + i * (64 * BK * 2), &tmA, fb,
-                                      ti.m_blk * BM + i * 64, krow, 0);
+                for (int i = 0; i < BM / 64; ++i)
+                  ptx::tma_load_3d_pair_hint(a_dst + i * (64 * BK * 2), &tmA, fb,
+                                             ti.m_blk * BM + i * 64, krow, 0, op_pol);
 #pragma unroll
-              for (int i = 0; i < BN / 128; ++i)
-                ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb, ncol + i * 64, krow, 0);
+                for (int i = 0; i < BN / 128; ++i)
+                  ptx::tma_load_3d_pair_hint(b_dst + i * (64 * BK * 2), &tmB, fb, ncol + i * 64,
+                                             krow, 0, op_pol);
+              } else {
+#pragma unroll
+                for (int i = 0; i < BM / 64; ++i)
+                  ptx::tma_load_3d_pair(a_dst + i * (64 * BK * 2), &tmA, fb,
+                                        ti.m_blk * BM + i * 64, krow, 0);
+#pragma unroll
+                for (int i = 0; i < BN / 128; ++i)
+                  ptx::tma_load_3d_pair(b_dst + i * (64 * BK * 2), &tmB, fb, ncol + i * 64,
+                                        krow, 0);
+              }
             } else {  // ROWS
               const int k0 = kb * BK;
               if (!ti.ghost)
@@ -354,13 +382,23 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
           } else {
             const int krow = s_off[ti.g] + kb * BK;
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              ptx::tma_load_3d(a_dst + i * (64 * BK * 2), &tmA, &full[stage],
-                               ti.m_blk * BM + i * 64, krow, 0);
+            for (int i = 0; i < BM / 64; ++i) {
+              if (op_hint)
+                ptx::tma_load_3d_hint(a_dst + i * (64 * BK * 2), &tmA, &full[stage],
+                                      ti.m_blk * BM + i * 64, krow, 0, op_pol);
+              else
+                ptx::tma_load_3d(a_dst + i * (64 * BK * 2), &tmA, &full[stage],
+                                 ti.m_blk * BM + i * 64, krow, 0);
+            }
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              ptx::tma_load_3d(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
-                               ti.n_blk * BN + i * 64, krow, 0);
+            for (int i = 0; i < BN / 64; ++i) {
+              if (op_hint)
+                ptx::tma_load_3d_hint(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
+                                      ti.n_blk * BN + i * 64, krow, 0, op_pol);
+              else
+                ptx::tma_load_3d(b_dst + i * (64 * BK * 2), &tmB, &full[stage],
+                                 ti.n_blk * BN + i * 64, krow, 0);
+            }
           }
         }
         __syncwarp();
@@ -455,9 +493,15 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
     };
     float4 ring[RING][3];
     auto issue = [&](float4 (&r)[3], int64_t o) {
-      r[0] = ld_state(p.adam_master + o, pol);
-      r[1] = ld_state(p.adam_m1 + o, pol);
-      r[2] = ld_state(p.adam_m2 + o, pol);
+      if (p.state_policy & 1) {  // (measurement knob) no L2 eviction hint on the loads
+        r[0] = ld_state_plain(p.adam_master + o);
+        r[1] = ld_state_plain(p.adam_m1 + o);
+        r[2] = ld_state_plain(p.adam_m2 + o);
+      } else {
+        r[0] = ld_state(p.adam_master + o, pol);
+        r[1] = ld_state(p.adam_m1 + o, pol);
+        r[2] = ld_state(p.adam_m2 + o, pol);
+      }
     };
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -517,9 +561,15 @@ __global__ void __launch_bounds__(Cfg<EPI, PAIR, PUSH>::THREADS, 1)
           gw[(c % 4) * 2 + 1] = pack_bf16(v[vb + 2], v[vb + 3]);
         }
         const int64_t o = cur + c * 128;
-        st_state(p.adam_master + o, st[0], pol);
-        st_state(p.adam_m1 + o, st[1], pol);
-        st_state(p.adam_m2 + o, st[2], pol);
+        if (p.state_policy & 2) {  // (measurement knob) no L2 eviction hint on the stores
+          st_state_plain(p.adam_master + o, st[0]);
+          st_state_plain(p.adam_m1 + o, st[1]);
+          st_state_plain(p.adam_m2 + o, st[2]);
+        } else {
+          st_state(p.adam_master + o, st[0], pol);
+          st_state(p.adam_m1 + o, st[1], pol);
+          st_state(p.adam_m2 + o, st[2], pol);
+        }
         pw[(c % 4) * 2] = pack_bf16(mq[0], mq[1]);
         pw[(c % 4) * 2 + 1] = pack_bf16(mq[2], mq[3]);
         if (c % 4 == 3) {
@@ -959,6 +1009,18 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
       return v ? std::atoi(v) : 0;
     }();
     const_cast<GemmParams&>(p).band = band_env;
+  }
+  if (p.mode == GEMM_KDIM) {  // (measurement knobs: L2 hints of the AdamW wgrad streams)
+    static const int pol_env = [] {
+      const char* v = std::getenv("TED_STATE_POLICY");
+      return v ? std::atoi(v) : 0;
+    }();
+    static const int op_env = [] {  // default on: 1.2 % faster fused wgrad (same box)
+      const char* v = std::getenv("TED_OPERAND_HINT");
+      return v ? std::atoi(v) : 1;
+    }();
+    const_cast<GemmParams&>(p).state_policy = pol_env;
+    const_cast<GemmParams&>(p).operand_hint = op_env;
   }
   if (p.mode == GEMM_ROWS && p.push_peers != nullptr) {  // push return over NVLink
     if (o.b_mn && p.epi == EPI_BIAS)

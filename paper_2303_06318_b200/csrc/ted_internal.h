@@ -79,6 +79,8 @@ struct GemmParams {
   int push_T = 1, push_slot = 0;
   int64_t push_slot_stride = 0;
   int band = 0;  // KDIM raster: row blocks (tile pairs) per band (0: the default)
+  int state_policy = 0;  // AdamW state L2 hints: bit 0 plain loads, bit 1 plain stores
+  int operand_hint = 0;  // AdamW wgrad: operand TMA loads with an L2 evict-last policy
 };
 
 struct GemmOperands {
