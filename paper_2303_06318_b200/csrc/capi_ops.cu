@@ -358,7 +358,7 @@ int ted_dispatch_forward(const uint16_t* a, const int32_t* expert, int64_t n, in
     need(E >= 1 && E <= 64, "dispatch: experts must be in [1, 64]");
     need(h >= 8 && h % 8 == 0, "dispatch: hidden must be a positive multiple of 8");
     need(n >= 0, "dispatch: negative token count");
-    need(expert && pos && x_asm && seg_off && kept_counts, "dispatch: null output");
+    need(x_asm && seg_off && kept_counts && (n == 0 || (expert && pos)), "dispatch: null argument");
     device_ok();
     cudaStream_t s = S(stream);
     const int64_t cap = capacity <= 0 ? std::max<int64_t>(n, 1) : capacity;

@@ -101,3 +101,38 @@ def test_operator_config_errors_are_status_2():
     w1 = torch.zeros(1, 200, 800, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(ted.InvalidConfigError):
         ted.expert_ffn_forward(x, seg, w1, w1[:, 0], w1.transpose(1, 2), w1[:, :, 0])
+
+
+def test_operator_edge_cases():
+    """Empty and tiny inputs (the reference's tests cover empty shards and single tokens):
+    no tokens, one token, one expert, every token dropped (capacity 1 with all tokens on one
+    expert)."""
+    import paper_2303_06318_b200 as ted
+    h, E = 256, 4
+    # one token, one expert
+    a = torch.randn(1, h, device="cuda").bfloat16()
+    e = torch.zeros(1, device="cuda", dtype=torch.int32)
+    x, pos, seg, kept, slot = ted.dispatch_forward(a, e, 1)
+    torch.cuda.synchronize()
+    assert pos.item() == 0 and kept.item() == 1 and seg.tolist() == [0, 128]
+    assert torch.equal(x[0], a[0]) and torch.count_nonzero(x[1:128]) == 0
+    # 64 tokens on expert 2 with capacity 1: one kept, the rest dropped (pos -1, zero y)
+    a = torch.randn(64, h, device="cuda").bfloat16()
+    e = torch.full((64,), 2, device="cuda", dtype=torch.int32)
+    x, pos, seg, kept, slot = ted.dispatch_forward(a, e, E, cap=1)
+    torch.cuda.synchronize()
+    assert kept.tolist() == [0, 0, 1, 0] and int((pos >= 0).sum()) == 1 and pos[0].item() == 0
+    assert slot.tolist() == list(range(64))
+    prob = torch.rand(64, device="cuda")
+    y = ted.combine_forward(x, pos, prob)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(y[1:]) == 0
+    da = ted.dispatch_backward(x, pos, 64)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(da[1:]) == 0 and torch.equal(da[0], x[0])
+    # no tokens: nothing to do, no error
+    a0 = torch.empty(0, h, device="cuda").bfloat16()
+    e0 = torch.empty(0, device="cuda", dtype=torch.int32)
+    x0, pos0, seg0, kept0, _ = ted.dispatch_forward(a0, e0, E)
+    torch.cuda.synchronize()
+    assert kept0.tolist() == [0] * E and seg0.tolist() == [0] * (E + 1)
