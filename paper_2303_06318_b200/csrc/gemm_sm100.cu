@@ -942,8 +942,9 @@ int sm_count() {
 //   ROWS / B K-major : B_g [N][K] at B + g*b_group_stride
 //   KDIM / A MN-major: A [rows_total][M];   B MN-major: B [rows_total][N]
 //   C (and aux): ROWS [rows_total][N] (ldc / ld_aux);  KDIM C_g [M][N] at C + g*c_group_stride
-cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_rows,
+cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p_in, int max_rows,
                          cudaStream_t s, const char** why) {
+  GemmParams p = p_in;  // (the launch knobs below fill in defaults)
   auto fail = [&](const char* w) {
     if (why) *why = w;
     return cudaErrorInvalidValue;
@@ -1008,7 +1009,7 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
       const char* v = std::getenv("TED_GEMM_BAND");
       return v ? std::atoi(v) : 0;
     }();
-    const_cast<GemmParams&>(p).band = band_env;
+    p.band = band_env;
   }
   if (p.mode == GEMM_KDIM) {  // (measurement knobs: L2 hints of the AdamW wgrad streams)
     static const int pol_env = [] {
@@ -1019,8 +1020,8 @@ cudaError_t grouped_gemm(const GemmOperands& o, const GemmParams& p, int max_row
       const char* v = std::getenv("TED_OPERAND_HINT");
       return v ? std::atoi(v) : 1;
     }();
-    const_cast<GemmParams&>(p).state_policy = pol_env;
-    const_cast<GemmParams&>(p).operand_hint = op_env;
+    p.state_policy = pol_env;
+    p.operand_hint = op_env;
   }
   if (p.mode == GEMM_ROWS && p.push_peers != nullptr) {  // push return over NVLink
     if (o.b_mn && p.epi == EPI_BIAS)
