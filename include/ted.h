@@ -255,6 +255,9 @@ int ted_layer_step(ted_layer* L, const uint16_t* a_dev, uint16_t* y_dev, uint16_
                    void* stream);
 /* Local loss of the last forward (sum(y^2) / (2 N_global)); synchronises the stream. */
 int ted_layer_loss(ted_layer* L, double* loss, void* stream);
+/* The same value copied stream-ordered into caller-pinned host memory without waiting (a
+ * training loop reads step i's loss after enqueuing step i + 1 and an event wait). */
+int ted_layer_loss_async(ted_layer* L, double* loss_pinned, void* stream);
 /* Failure detection (TrainerOptions::collective_timeout, moe.hpp:96; Fabric's TimeoutError,
  * fabric.cpp:65-96).  A plane member that does not reach an NVLink barrier within `seconds`
  * (default 120; 0 = wait forever) is recorded by the device in a host-mapped word -- no

@@ -144,6 +144,7 @@ _sig("ted_layer_optimizer_step", _i32, [_vp, _vp])
 _sig("ted_layer_step", _i32, [_vp, _vp, _vp, _vp, _vp])
 _sig("ted_layer_loss", _i32, [_vp, C.POINTER(_dbl), _vp])
 _sig("ted_layer_set_timeout", _i32, [_vp, _dbl])
+_sig("ted_layer_loss_async", _i32, [_vp, _vp, _vp])
 _sig("ted_layer_ledger", _i32, [_vp, _vp, _i32])
 _sig("ted_model_ledger", _i32, [_vp, _vp, _i32])
 _sig("ted_ops_reserve", _i32, [C.c_size_t, _vp])
@@ -191,7 +192,8 @@ EXPORTED = [
     "ted_gate_backward", "ted_grouped_gemm", "ted_adam_step", "ted_placement_verdict", "ted_layer_create",
     "ted_layer_destroy", "ted_nccl_unique_id", "ted_layer_set_param", "ted_layer_get_param",
     "ted_layer_get_grad", "ted_layer_keep_grads", "ted_layer_init_params", "ted_layer_forward", "ted_layer_backward",
-    "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_set_timeout",
+    "ted_layer_optimizer_step", "ted_layer_step", "ted_layer_loss", "ted_layer_loss_async",
+    "ted_layer_set_timeout",
     "ted_layer_get_stats",
     "ted_layer_get_routing", "ted_layer_timing", "ted_layer_timing_read", "ted_kernel_launches",
     "ted_set_device", "ted_model_create", "ted_model_destroy", "ted_model_set_param",
@@ -603,6 +605,12 @@ class MoeLayer:
     def ledger(self, reset: bool = False) -> dict:
         """This rank's CommLedger entries {"<phase>.<op>": {calls, payload_bytes}}."""
         return _ledger(_lib.ted_layer_ledger, self._h, reset)
+
+    def loss_async(self, dst_pinned, stream=None):
+        """Copy the last forward's loss into element 0 of a pinned float64 host tensor,
+        stream-ordered, without waiting."""
+        _check(_lib.ted_layer_loss_async(self._h, C.c_void_p(dst_pinned.data_ptr()),
+                                         _stream(stream)))
 
     def set_timeout(self, seconds: float):
         """collective_timeout (moe.hpp:96): a stalled peer raises TedRuntimeError

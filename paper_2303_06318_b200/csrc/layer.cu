@@ -1786,6 +1786,15 @@ int ted_layer_keep_grads(ted_layer* L, int keep) {
   });
 }
 
+int ted_layer_loss_async(ted_layer* L, double* loss_pinned, void* stream) {
+  return guard([&] {
+    require(L && loss_pinned, "null argument");
+    check_fault(L);
+    CU(cudaMemcpyAsync(loss_pinned, L->loss.p, sizeof(double), cudaMemcpyDeviceToHost,
+                       S(stream)));
+  });
+}
+
 int ted_layer_loss(ted_layer* L, double* loss, void* stream) {
   return guard([&] {
     require(L && loss, "null argument");
