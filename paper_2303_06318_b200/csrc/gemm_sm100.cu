@@ -111,7 +111,10 @@ struct Cfg {
   static constexpr int NOUT = EPI == EPI_BIAS_GELU ? 2 : 1;  // staged outputs per block
   static constexpr int B_LOCAL = PAIR ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;  // this CTA's B
   static constexpr int STAGE_LOCAL = A_STAGE_BYTES + B_LOCAL;
-  static constexpr int STAGES = PAIR ? (EPI == EPI_ADAM ? 5 : 6) : 4;
+  // (the AdamW pair kernel runs 4 stages: 7-10 % faster than 5 or 6 at C3, same-box A/B --
+  // a shallower operand prefetch competes less with the state stream; the forward / dgrad
+  // GEMMs lose 12 % with 3)
+  static constexpr int STAGES = PAIR ? (EPI == EPI_ADAM ? 4 : 6) : 4;
   // AdamW: the parameter half block and (keep-gradients mode) the gradient half block
   static constexpr int PUSH_COLS = 64;  // columns per staged push round (128 B rows)
   static constexpr size_t PER_WARP = PUSH ? 32 * PUSH_COLS * 2
@@ -170,7 +173,11 @@ __device__ __forceinline__ bool decode_tile(const GemmParams& p, const int* s_of
     const int mt = p.M / (PAIR ? 2 * BM : BM);
     const int per = mt * nt;
     ti.g = t / per;
-    raster(t % per, mt, nt, ti.m_blk, ti.n_blk, p.band > 0 ? p.band : kBand);
+    // CTA pairs with the AdamW epilogue: bands of 8 pair rows (2048 rows of A) when the
+    // matrix is taller than 16 -- the A band stays in L2 against the state stream (wgrad2 at
+    // C3 7.23 -> 6.66 ms, wgrad1 unchanged; measured with TED_GEMM_BAND)
+    const int band = p.band > 0 ? p.band : (PAIR && mt > 16 ? 8 : kBand);
+    raster(t % per, mt, nt, ti.m_blk, ti.n_blk, band);
     if (PAIR) ti.m_blk = 2 * ti.m_blk + rank;
     ti.k_len = s_off[ti.g + 1] - s_off[ti.g];
   }
