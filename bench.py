@@ -118,13 +118,18 @@ def rooflines(w, stage_avg_ms, stats, T, P, D, world):
 
 
 def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
-    """A parity check at the benched configuration (one GPU), after the timed steps: one
-    more forward on the same tokens, then, in fp64 numpy on the layer's current bf16
-    parameters (MoeRank's MoE branch, moe.cpp:435-563, restated here -- bench.py does not
-    run the test oracle on this path): the routing of EVERY token must equal the argmax of
-    the GPU's own fp32 logits (lowest index on ties), and y of `tokens` sampled kept tokens
-    must match p * (gelu(a W1_e + b1_e) W2_e + b2_e) within rel-L2 2e-2 (bf16 storage of
-    X, Z, H, F; fp32 accumulation)."""
+    """A parity check at the benched configuration (one GPU): one forward on the benched
+    tokens, then, in fp64 numpy on the layer's current bf16 parameters (MoeRank's MoE
+    branch, moe.cpp:435-563, restated here -- bench.py does not run the test oracle on this
+    path): the routing of EVERY token must equal the argmax of the GPU's own fp32 logits
+    (lowest index on ties), and y of `tokens` sampled kept tokens must match
+    p * (gelu(a W1_e + b1_e) W2_e + b2_e) (bf16 storage of X, Z, H, F; fp32 accumulation).
+
+    Two error figures: `y_rel_l2_sampled` = ||y - ref|| / ||ref||, and `y_err_vs_terms` =
+    ||y - ref|| / ||p (|H| |W2_e| + |b2_e|)||, the error against the magnitude of the terms
+    summed into y.  Training on one fixed batch drives y (the objective is sum(y^2)/2N)
+    towards zero by cancellation, so after many steps ||ref|| shrinks while the rounding
+    error of the terms does not: `condition` = ||terms|| / ||ref|| says by how much."""
     import numpy as np
     import torch
     y = torch.empty_like(a)
@@ -143,7 +148,7 @@ def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
 
     def bf16(x):
         return torch.from_numpy(np.asarray(x, np.float32)).bfloat16().float().numpy().astype(np.float64)
-    cache, num, den = {}, 0.0, 0.0
+    cache, num, den, scl = {}, 0.0, 0.0, 0.0
     for k in sorted(pick, key=lambda k: r["expert"][k]):
         e = int(r["expert"][k])
         if e not in cache:
@@ -155,14 +160,28 @@ def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
         g = bf16(0.5 * z * (1 + np.tanh(0.7978845608028654 * (z + 0.044715 * z ** 3))))
         fo = bf16(g @ W["w2"].reshape(f, h) + W["b2"])
         ref = r["prob"][k] * fo
+        terms = r["prob"][k] * (np.abs(g) @ np.abs(W["w2"].reshape(f, h)) + np.abs(W["b2"]))
         num += float(np.sum((yv[k] - ref) ** 2))
         den += float(np.sum(ref ** 2))
+        scl += float(np.sum(terms ** 2))
     rel = (num / max(den, 1e-300)) ** 0.5
     return {"routing_bit_exact_all_tokens": routing_ok, "y_rel_l2_sampled": rel,
-            "tokens_sampled": int(len(pick)), "tolerance": 2e-2,
-            "pass": bool(routing_ok and rel < 2e-2),
+            "y_err_vs_terms": (num / max(scl, 1e-300)) ** 0.5,
+            "condition": (scl / max(den, 1e-300)) ** 0.5, "tokens_sampled": int(len(pick))}
+
+
+def parity_verdict(before, after):
+    """`before`: the check on the initialised parameters (ahead of the warm-up steps), pass
+    = routing bit-exact and y rel-L2 <= 2e-2; `after`: the same check once the timed steps
+    have trained the parameters, pass = routing bit-exact and the error against the term
+    magnitudes <= 2e-2 (its plain rel-L2 is reported, scaled by the cancellation
+    `condition`)."""
+    ok_b = bool(before["routing_bit_exact_all_tokens"] and before["y_rel_l2_sampled"] < 2e-2)
+    ok_a = bool(after["routing_bit_exact_all_tokens"] and after["y_err_vs_terms"] < 2e-2)
+    return {"before_steps": before, "after_steps": after, "tolerance": 2e-2, "pass": ok_b and ok_a,
             "check": "routing of all tokens vs argmax of the GPU logits; y of sampled kept "
-                     "tokens vs fp64 numpy on the layer's bf16 parameters"}
+                     "tokens vs fp64 numpy on the layer's bf16 parameters, on the initialised "
+                     "parameters (rel-L2) and after the timed steps (error vs term magnitude)"}
 
 
 def quick_layer_bench(w, steps: int, warmup: int):
@@ -507,6 +526,8 @@ def run_ours(args, w, rank, world, local_rank, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    do_parity = world == 1 and not args.no_parity
+    parity0 = sampled_parity(L, a, w, T, P) if do_parity else None
     for _ in range(args.warmup):
         L.step(a, y, da)
     torch.cuda.synchronize()
@@ -541,7 +562,7 @@ def run_ours(args, w, rank, world, local_rank, dist):
     ms = max_over_ranks(ms)
     stats = L.stats()
     loss = L.loss()
-    parity = sampled_parity(L, a, w, T, P) if world == 1 and not args.no_parity else None
+    parity = parity_verdict(parity0, sampled_parity(L, a, w, T, P)) if do_parity else None
 
     # e2e through the public API: every step's tokens are copied from pinned host memory
     # (on a copy stream into one of two device buffers, so step i+1's H2D runs under step

@@ -563,107 +563,134 @@ __global__ void __launch_bounds__(kThreads) gate_bwd_dx_kernel(const RowSrc R,
   }
 }
 
+// da = sum of the dX replicas + dl Wg^T on mma.sync.  Work unit = 128 tokens x CW hidden
+// columns (CW = 512, or 256 when h % 512 != 0); persistent CTAs stride over the units, so a
+// call is ~7 units per CTA slot instead of 1.7 waves of whole-row CTAs.  Per unit the CTA
+// stages Wg's CW columns once in shared memory, already in the m16n8k16 B-fragment order
+// (one conflict-free 8-byte LDS per lane per n-tile), and each warp streams 16 tokens x CW
+// columns: dl as bf16 hi + lo A fragments (two MMAs: the product keeps ~16 mantissa bits of
+// dl, fp32 accumulation), the dX rows (NS replicas) prefetched D steps of 32 columns ahead.
 template <int KS, int NS, int D>
 __global__ void __launch_bounds__(kThreads, 2) gate_bwd_dx_mma_kernel(const RowSrc R,
                                                                    const float* __restrict__ dl,
                                                                    const bf16* __restrict__ wg,
                                                                    int64_t n, int h, int E,
+                                                                   int CW,
                                                                    bf16* __restrict__ da) {
+  extern __shared__ __align__(16) uint2 s_b[];  // [CW/32 steps][4 n-tiles][KS][32 lanes]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
-  const int tt = warp & 3, half = warp >> 2;
-  const int64_t kr[2] = {int64_t(blockIdx.x) * kRouteBlock + tt * 16 + g,
-                         int64_t(blockIdx.x) * kRouteBlock + tt * 16 + g + 8};
-  uint32_t ahi[KS][4], alo[KS][4];
-#pragma unroll
-  for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = q & 1, pq = q >> 1;  // a0: (row g, k 2c), a1: (g+8, 2c), a2: (g, 2c+8) ...
-      const int e0 = 16 * ks + 2 * c + 8 * pq;
-      const int64_t k = kr[r];
-      const float v0 = (k < n && e0 < E) ? dl[k * E + e0] : 0.f;
-      const float v1 = (k < n && e0 + 1 < E) ? dl[k * E + e0 + 1] : 0.f;
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
-      const float2 hf = __bfloat1622float2(hi);
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
-      ahi[ks][q] = *reinterpret_cast<const uint32_t*>(&hi);
-      alo[ks][q] = *reinterpret_cast<const uint32_t*>(&lo);
-    }
-  // dX rows of this lane's two tokens, replicas 0..NS-1 prefetched D steps (of 32 columns)
-  // ahead -- on more than one GPU these are NVLink loads from the TP replicas' buffers
+  const int nchunk = h / CW, steps = CW / 32;
+  const int64_t ntb = (n + 127) / 128;
+  const int64_t units = ntb * nchunk;
   const int nsum = R.nsum < 1 ? 1 : R.nsum;
-  const bf16* rows[2][NS];
+  int staged = -1;  // the column chunk whose fragments are in shared memory
+  for (int64_t un = blockIdx.x; un < units; un += gridDim.x) {
+    const int64_t tb = un / nchunk;
+    const int cbeg = int(un % nchunk) * CW;
+    if (cbeg != staged) {  // (with a grid that is a multiple of nchunk: once per CTA)
+    __syncthreads();  // the previous unit's fragments are no longer read
+    // B fragment of (step st, n-tile nt, ks) for lane (g', c'): output column
+    // cbeg + 32 st + 8 (g' >> 1) + 2 nt + (g' & 1), experts 16 ks + 2 c' + {0, 1} and + 8
+#pragma unroll 4
+    for (int i = threadIdx.x; i < steps * 4 * KS * 32; i += kThreads) {
+      const int ln = i & 31, ks = (i >> 5) % KS, nt = (i / (32 * KS)) & 3, st = i / (128 * KS);
+      const int gg = ln >> 2, cc = ln & 3;
+      const bf16* wrow = wg + int64_t(cbeg + 32 * st + 8 * (gg >> 1) + 2 * nt + (gg & 1)) * E;
+      uint32_t b[2];
 #pragma unroll
-  for (int r = 0; r < 2; ++r)
+      for (int pq = 0; pq < 2; ++pq) {
+        const int e0 = 16 * ks + 2 * cc + 8 * pq;
+        __nv_bfloat162 wv;
+        wv.x = e0 < E ? wrow[e0] : __float2bfloat16(0.f);
+        wv.y = e0 + 1 < E ? wrow[e0 + 1] : __float2bfloat16(0.f);
+        b[pq] = *reinterpret_cast<const uint32_t*>(&wv);
+      }
+      s_b[i] = make_uint2(b[0], b[1]);
+    }
+    __syncthreads();
+    staged = cbeg;
+    }
+    const int64_t kr[2] = {tb * 128 + warp * 16 + g, tb * 128 + warp * 16 + g + 8};
+    if (tb * 128 + warp * 16 >= n) continue;  // (every warp passed this unit's barriers)
+    uint32_t ahi[KS][4], alo[KS][4];
 #pragma unroll
-    for (int rep = 0; rep < NS; ++rep)
-      rows[r][rep] = (kr[r] < n && rep < nsum) ? src_row(R, kr[r], h, rep) : nullptr;
-  const int hh = h / 2;
-  const int cbeg = half * hh, cend = (half + 1) * hh;
-  uint4 X[D][2][NS];
-  auto load_x = [&](int col0, uint4 (&x)[2][NS]) {
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = q & 1, pq = q >> 1;  // a0: (row g, k 2c), a1: (g+8, 2c), a2: (g, 2c+8) ...
+        const int e0 = 16 * ks + 2 * c + 8 * pq;
+        const int64_t k = kr[r];
+        const float v0 = (k < n && e0 < E) ? dl[k * E + e0] : 0.f;
+        const float v1 = (k < n && e0 + 1 < E) ? dl[k * E + e0 + 1] : 0.f;
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+        const float2 hf = __bfloat1622float2(hi);
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+        ahi[ks][q] = *reinterpret_cast<const uint32_t*>(&hi);
+        alo[ks][q] = *reinterpret_cast<const uint32_t*>(&lo);
+      }
+    // dX rows of this lane's two tokens, replicas 0..NS-1 -- on more than one GPU these are
+    // NVLink loads from the TP replicas' buffers or the local receive slots of the push
+    const bf16* rows[2][NS];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
       for (int rep = 0; rep < NS; ++rep)
-        x[r][rep] = (rows[r][rep] && col0 < cend) ? ldg_stream(rows[r][rep] + col0 + 8 * c)
-                                                  : make_uint4(0, 0, 0, 0);
-  };
+        rows[r][rep] = (kr[r] < n && rep < nsum) ? src_row(R, kr[r], h, rep) : nullptr;
+    const int cend = cbeg + CW;
+    uint4 X[D][2][NS];
+    auto load_x = [&](int col0, uint4 (&x)[2][NS]) {
 #pragma unroll
-  for (int u = 0; u < D; ++u) load_x(cbeg + 32 * u, X[u]);
-  for (int cb = cbeg; cb < cend; cb += 32 * D) {
+      for (int r = 0; r < 2; ++r)
 #pragma unroll
-    for (int u = 0; u < D; ++u) {
-      const int col0 = cb + 32 * u;
-      float acc[4][4];
+        for (int rep = 0; rep < NS; ++rep)
+          x[r][rep] = (rows[r][rep] && col0 < cend) ? ldg_stream(rows[r][rep] + col0 + 8 * c)
+                                                    : make_uint4(0, 0, 0, 0);
+    };
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
-        // B column g of this n-tile is output column col0 + 8 (g >> 1) + 2 nt + (g & 1)
-        const bf16* wrow = wg + int64_t(col0 + 8 * (g >> 1) + 2 * nt + (g & 1)) * E;
+    for (int u = 0; u < D; ++u) load_x(cbeg + 32 * u, X[u]);
+    for (int cb = cbeg; cb < cend; cb += 32 * D) {
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          uint32_t b[2];
-#pragma unroll
-          for (int pq = 0; pq < 2; ++pq) {
-            const int e0 = 16 * ks + 2 * c + 8 * pq;
-            const bf16 w0 = e0 < E ? wrow[e0] : __float2bfloat16(0.f);
-            const bf16 w1 = e0 + 1 < E ? wrow[e0 + 1] : __float2bfloat16(0.f);
-            __nv_bfloat162 wv;
-            wv.x = w0;
-            wv.y = w1;
-            b[pq] = *reinterpret_cast<const uint32_t*>(&wv);
-          }
-          mma_bf16_16816(acc[nt], ahi[ks][0], ahi[ks][1], ahi[ks][2], ahi[ks][3], b[0], b[1]);
-          mma_bf16_16816(acc[nt], alo[ks][0], alo[ks][1], alo[ks][2], alo[ks][3], b[0], b[1]);
-        }
-      }
-      // lane (g, c): row r's columns col0 + 8c .. +7 = acc[0..3][2r], acc[0..3][2r + 1]
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (kr[r] >= n) continue;
-        float o[8], x[8];
+      for (int u = 0; u < D; ++u) {
+        const int col0 = cb + 32 * u;
+        const uint2* sb = s_b + ((col0 - cbeg) / 32) * (4 * KS * 32) + lane;
+        float acc[4][4];
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
-          o[2 * nt] = acc[nt][2 * r];
-          o[2 * nt + 1] = acc[nt][2 * r + 1];
-        }
+          acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
 #pragma unroll
-        for (int rep = 0; rep < NS; ++rep) {  // TP partial sums (parallel_linear.cpp:19)
-          unpack8(X[u][r][rep], x);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) o[q] += x[q];
+          for (int ks = 0; ks < KS; ++ks) {
+            const uint2 b = sb[(nt * KS + ks) * 32];
+            mma_bf16_16816(acc[nt], ahi[ks][0], ahi[ks][1], ahi[ks][2], ahi[ks][3], b.x, b.y);
+            mma_bf16_16816(acc[nt], alo[ks][0], alo[ks][1], alo[ks][2], alo[ks][3], b.x, b.y);
+          }
         }
-        if (rows[r][0] != nullptr)
-          for (int rep = NS; rep < nsum; ++rep) {  // TP > NS: the remaining replicas
-            unpack8(ldg_stream(src_row(R, kr[r], h, rep) + col0 + 8 * c), x);
+        // lane (g, c): row r's columns col0 + 8c .. +7 = acc[0..3][2r], acc[0..3][2r + 1]
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (kr[r] >= n) continue;
+          float o[8], x[8];
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            o[2 * nt] = acc[nt][2 * r];
+            o[2 * nt + 1] = acc[nt][2 * r + 1];
+          }
+#pragma unroll
+          for (int rep = 0; rep < NS; ++rep) {  // TP partial sums (parallel_linear.cpp:19)
+            unpack8(X[u][r][rep], x);
 #pragma unroll
             for (int q = 0; q < 8; ++q) o[q] += x[q];
           }
-        *reinterpret_cast<uint4*>(da + kr[r] * h + col0 + 8 * c) = pack8(o);
+          if (rows[r][0] != nullptr)
+            for (int rep = NS; rep < nsum; ++rep) {  // TP > NS: the remaining replicas
+              unpack8(ldg_stream(src_row(R, kr[r], h, rep) + col0 + 8 * c), x);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] += x[q];
+            }
+          *reinterpret_cast<uint4*>(da + kr[r] * h + col0 + 8 * c) = pack8(o);
+        }
+        load_x(col0 + 32 * D, X[u]);  // refill this ring slot D steps ahead
       }
-      load_x(col0 + 32 * D, X[u]);  // refill this ring slot D steps ahead
     }
   }
 }
@@ -750,7 +777,7 @@ __global__ void __launch_bounds__(128) gate_bwd_dw_kernel(const bf16* __restrict
 // byte-permutes them into the A fragments: M-tile mt's rows g / g+8 are hidden columns
 // 8g + 2mt / 8g + 2mt + 1 (a permutation of M undone when writing).  dlogits (fp32) enter
 // as bf16 hi + lo (two MMAs, ~2^-17 relative); fp32 accumulation; one partial per chunk.
-template <int NT>
+template <int NT, int D>
 __global__ void __launch_bounds__(128) gate_bwd_dw_mma_kernel(const bf16* __restrict__ a,
                                                               const float* __restrict__ dl,
                                                               int64_t n, int h, int E, int tok,
@@ -766,53 +793,64 @@ __global__ void __launch_bounds__(128) gate_bwd_dw_mma_kernel(const bf16* __rest
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0.f;
   const int tr[4] = {2 * c, 2 * c + 1, 2 * c + 8, 2 * c + 9};  // this lane's token rows
-  auto load = [&](int64_t k0, uint4 (&x)[4]) {
+  // a ring of D 16-token steps in flight per warp: the token rows (64 columns = 128 B per
+  // row) and the dlogits the step's B fragments are made of, both loaded D steps ahead
+  // (D = 1 with 4 CTAs per SM measured fastest: 2 and 4 with fewer CTAs were 1.3-2x slower)
+  uint4 X[D][4];
+  float DL[D][NT][4];
+  auto load = [&](int64_t k0, uint4 (&x)[4], float (&d)[NT][4]) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int64_t t = k0 + tr[i];
       x[i] = t < k_end ? ldg_stream(a + t * h + hb + 8 * g) : make_uint4(0, 0, 0, 0);
     }
-  };
-  uint4 xc[4], xn[4];
-  load(k_beg, xc);
-  for (int64_t k0 = k_beg; k0 < k_end; k0 += 16) {
-    if (k0 + 16 < k_end) load(k0 + 16, xn);
-    // B fragments: dlogits of tokens (2c, 2c+1) and (2c+8, 2c+9) for expert nt*8 + g
-    uint32_t bhi[NT][2], blo[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
       const int e = nt * 8 + g;
 #pragma unroll
-      for (int pq = 0; pq < 2; ++pq) {
-        const int64_t t0 = k0 + tr[2 * pq], t1 = k0 + tr[2 * pq + 1];
-        const float v0 = (t0 < k_end && e < E) ? dl[t0 * E + e] : 0.f;
-        const float v1 = (t1 < k_end && e < E) ? dl[t1 * E + e] : 0.f;
-        const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
-        const float2 hf = __bfloat1622float2(hi);
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
-        bhi[nt][pq] = *reinterpret_cast<const uint32_t*>(&hi);
-        blo[nt][pq] = *reinterpret_cast<const uint32_t*>(&lo);
+      for (int i = 0; i < 4; ++i) {
+        const int64_t t = k0 + tr[i];
+        d[nt][i] = (t < k_end && e < E) ? dl[t * E + e] : 0.f;
       }
     }
-    const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&xc[0]);
-    const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&xc[1]);
-    const uint32_t* w2 = reinterpret_cast<const uint32_t*>(&xc[2]);
-    const uint32_t* w3 = reinterpret_cast<const uint32_t*>(&xc[3]);
+  };
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      // row g: hidden column 8g + 2mt (low halves), row g + 8: 8g + 2mt + 1 (high halves)
-      const uint32_t a0 = __byte_perm(w0[mt], w1[mt], 0x5410);
-      const uint32_t a1 = __byte_perm(w0[mt], w1[mt], 0x7632);
-      const uint32_t a2 = __byte_perm(w2[mt], w3[mt], 0x5410);
-      const uint32_t a3 = __byte_perm(w2[mt], w3[mt], 0x7632);
+  for (int u = 0; u < D; ++u) load(k_beg + 16 * u, X[u], DL[u]);
+  for (int64_t kb = k_beg; kb < k_end; kb += 16 * D) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, bhi[nt][0], bhi[nt][1]);
-        mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, blo[nt][0], blo[nt][1]);
+    for (int u = 0; u < D; ++u) {
+      // B fragments: dlogits of tokens (2c, 2c+1) and (2c+8, 2c+9) for expert nt*8 + g
+      uint32_t bhi[NT][2], blo[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int pq = 0; pq < 2; ++pq) {
+          const float v0 = DL[u][nt][2 * pq], v1 = DL[u][nt][2 * pq + 1];
+          const __nv_bfloat162 hi = __floats2bfloat162_rn(v0, v1);
+          const float2 hf = __bfloat1622float2(hi);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(v0 - hf.x, v1 - hf.y);
+          bhi[nt][pq] = *reinterpret_cast<const uint32_t*>(&hi);
+          blo[nt][pq] = *reinterpret_cast<const uint32_t*>(&lo);
+        }
+      const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&X[u][0]);
+      const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&X[u][1]);
+      const uint32_t* w2 = reinterpret_cast<const uint32_t*>(&X[u][2]);
+      const uint32_t* w3 = reinterpret_cast<const uint32_t*>(&X[u][3]);
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        // row g: hidden column 8g + 2mt (low halves), row g + 8: 8g + 2mt + 1 (high halves)
+        const uint32_t a0 = __byte_perm(w0[mt], w1[mt], 0x5410);
+        const uint32_t a1 = __byte_perm(w0[mt], w1[mt], 0x7632);
+        const uint32_t a2 = __byte_perm(w2[mt], w3[mt], 0x5410);
+        const uint32_t a3 = __byte_perm(w2[mt], w3[mt], 0x7632);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, bhi[nt][0], bhi[nt][1]);
+          mma_bf16_16816(acc[mt][nt], a0, a1, a2, a3, blo[nt][0], blo[nt][1]);
+        }
       }
+      load(kb + 16 * (u + D), X[u], DL[u]);  // refill this ring slot D steps ahead
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) xc[i] = xn[i];
   }
   float* out = part + int64_t(blockIdx.x) * h * E;
 #pragma unroll
@@ -1279,12 +1317,24 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
     else if (E <= 32) TED_GBX(32)
     else TED_GBX(64)
 #undef TED_GBX
-  } else if (E <= 16) {
-    gate_bwd_dx_mma_kernel<1, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
-  } else if (E <= 32) {
-    gate_bwd_dx_mma_kernel<2, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
   } else {
-    gate_bwd_dx_mma_kernel<4, 1, 4><<<grid, kThreads, 0, s>>>(src, dlogits, wg, n, h, E, da);
+    const int CW = h % 512 == 0 ? 512 : 256;
+    const int KS = E <= 16 ? 1 : (E <= 32 ? 2 : 4);
+    const size_t sm = size_t(CW / 32) * 4 * KS * 32 * sizeof(uint2);
+    const int64_t units = ceil_div(n, 128) * (h / CW);
+    // a grid that is a multiple of the chunk count keeps every CTA on one column chunk
+    const int nch = h / CW, slots = 2 * sm_count();
+    const int g2 = int(std::min<int64_t>(units, slots >= nch ? slots / nch * nch : slots));
+#define TED_GDX(KSV)                                                                           \
+  {                                                                                            \
+    smem_attr(gate_bwd_dx_mma_kernel<KSV, 1, 4>, sm);                                         \
+    gate_bwd_dx_mma_kernel<KSV, 1, 4><<<g2, kThreads, sm, s>>>(src, dlogits, wg, n, h, E, CW,  \
+                                                               da);                            \
+  }
+    if (KS == 1) TED_GDX(1)
+    else if (KS == 2) TED_GDX(2)
+    else TED_GDX(4)
+#undef TED_GDX
   }
   count_launch(1);
   return cudaGetLastError();
@@ -1316,9 +1366,9 @@ cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n,
   }
   if (E <= 32 && h % 64 == 0) {
     const dim3 grid(nb, ceil_div(h, 256));
-    if (E <= 8) gate_bwd_dw_mma_kernel<1><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
-    else if (E <= 16) gate_bwd_dw_mma_kernel<2><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
-    else gate_bwd_dw_mma_kernel<4><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+    if (E <= 8) gate_bwd_dw_mma_kernel<1, 1><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+    else if (E <= 16) gate_bwd_dw_mma_kernel<2, 1><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
+    else gate_bwd_dw_mma_kernel<4, 1><<<grid, 128, 0, s>>>(a, dlogits, n, h, E, tok, part);
   } else if (E <= 8) {
     gate_bwd_dw_kernel<8, 8><<<dim3(nb, ceil_div(h, 128 * 8)), 128, 0, s>>>(a, dlogits, n, h, E,
                                                                           tok, part);
