@@ -1304,7 +1304,7 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
   if (grid == 0) return cudaSuccess;
   // NS replicas of each dX row prefetched D steps ahead (1 = single GPU / reduced rows,
   // 2 = the TP-2 partial sums of the peer-memory exchange)
-  if (src.nsum >= 2) {  // NVLink pulls of TP partials: the row-streaming variant
+  if (src.nsum >= 2 && src.peers != nullptr) {  // NVLink pulls of TP partials: row streaming
 #define TED_GBX(EM)                                                                            \
   {                                                                                            \
     const int HC = gate_hc<EM>(h);                                                             \
@@ -1325,15 +1325,21 @@ cudaError_t gate_backward_input(const RowSrc& src, const float* dlogits, const b
     // a grid that is a multiple of the chunk count keeps every CTA on one column chunk
     const int nch = h / CW, slots = 2 * sm_count();
     const int g2 = int(std::min<int64_t>(units, slots >= nch ? slots / nch * nch : slots));
-#define TED_GDX(KSV)                                                                           \
+    // local rows: one replica (1 GPU, EP-only), or the TP partials the GEMM epilogue pushed
+    // into this rank's receive slots (NS = 2, a 2-step ring to stay within 128 registers)
+#define TED_GDX(KSV, NSV, DV)                                                                  \
   {                                                                                            \
-    smem_attr(gate_bwd_dx_mma_kernel<KSV, 1, 4>, sm);                                         \
-    gate_bwd_dx_mma_kernel<KSV, 1, 4><<<g2, kThreads, sm, s>>>(src, dlogits, wg, n, h, E, CW,  \
-                                                               da);                            \
+    smem_attr(gate_bwd_dx_mma_kernel<KSV, NSV, DV>, sm);                                      \
+    gate_bwd_dx_mma_kernel<KSV, NSV, DV><<<g2, kThreads, sm, s>>>(src, dlogits, wg, n, h, E,   \
+                                                                  CW, da);                     \
   }
-    if (KS == 1) TED_GDX(1)
-    else if (KS == 2) TED_GDX(2)
-    else TED_GDX(4)
+    if (src.nsum >= 2) {
+      if (KS == 1) TED_GDX(1, 2, 2)
+      else if (KS == 2) TED_GDX(2, 2, 2)
+      else TED_GDX(4, 2, 2)
+    } else if (KS == 1) TED_GDX(1, 1, 4)
+    else if (KS == 2) TED_GDX(2, 1, 4)
+    else TED_GDX(4, 1, 4)
 #undef TED_GDX
   }
   count_launch(1);
