@@ -20,7 +20,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-TOL = 2e-2
+# worst rel-L2 over y, da, every expert grad, dWg and the loss: measured 3.3e-3 - 3.8e-3 on
+# 2 GPUs (TP partials and the DP gradient sum travel as bf16); the bar is ~2.5x that
+TOL = 1e-2
 
 
 def rel(x, ref):

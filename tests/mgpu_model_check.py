@@ -93,7 +93,7 @@ def main():
     if rank == 0:
         tot = np.sum([np.array(l) for (tt, l) in allv if tt == 0], axis=0)
         ref = golden_losses(layers, h, E, n, seed, shards)
-        np.testing.assert_allclose(tot, ref, rtol=2e-2)
+        np.testing.assert_allclose(tot, ref, rtol=1e-2)  # measured <= 3.0e-3 on 2 GPUs
         print("MGPU-OK " + json.dumps({"losses": tot.tolist(), "ref": ref.tolist()}), flush=True)
     dist.barrier()
     dist.destroy_process_group()

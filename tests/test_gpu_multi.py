@@ -37,6 +37,12 @@ def _run(nproc, *args, env=None, script="mgpu_layer_check.py", timeout=600):
             break
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "MGPU-OK" in r.stdout, r.stdout[-4000:]
+    rep = os.environ.get("TED_MGPU_REPORT")  # collect the parity reports (worst_rel, ledger)
+    if rep:
+        with open(rep, "a") as f:
+            for line in r.stdout.splitlines():
+                if line.startswith("MGPU-OK "):
+                    f.write(line[8:] + "\n")
     return r.stdout
 
 

@@ -1,5 +1,6 @@
-"""One C2 MoE-layer training step after 3 warm-up steps (for ncu captures: run with
-TED_GRAPH=0 so every kernel is a plain launch)."""
+"""MoE-layer training steps (default C2); the last one inside cudaProfilerStart/Stop so
+`ncu --profile-from-start off` captures exactly one step (run with TED_GRAPH=0 so every
+kernel is a plain launch)."""
 import sys
 
 import torch
@@ -15,8 +16,13 @@ g = torch.Generator(device="cuda")
 g.manual_seed(1000)
 a = torch.randn(n, h, device="cuda", generator=g).bfloat16()
 y, da = torch.empty_like(a), torch.empty_like(a)
-for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 4):
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+for i in range(steps):
+    if i == steps - 1:  # ncu --profile-from-start off: only the last step is captured
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
     L.step(a, y, da)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", L.loss())
 L.close()
