@@ -755,6 +755,7 @@ int ted_model_set_param(ted_model* M, const char* name, const float* full) {
     std::vector<uint16_t> b(shard.size());
     for (size_t i = 0; i < b.size(); ++i) b[i] = f2bf(shard[i]);
     Family& F = M->fam;
+    CU(cudaDeviceSynchronize());  // a step in flight on a non-blocking stream may still write
     CU(cudaMemcpy(F.param.p + dl.off, b.data(), b.size() * 2, cudaMemcpyHostToDevice));
     const int64_t lo = std::max(dl.off, F.begin),
                   hi = std::min(dl.off + int64_t(b.size()), F.end);
@@ -812,6 +813,7 @@ int ted_model_keep_grads(ted_model* M, int keep) {
 int ted_model_init_params(ted_model* M, uint64_t seed) {
   return guard([&] {
     require(M != nullptr, "null model");
+    CU(cudaDeviceSynchronize());  // after any step still in flight
     for (int l = 0; l < M->layers; ++l) {
       for (const char* blk : {"attn", "ffn"}) {
         if (std::strcmp(blk, "ffn") == 0 && l % 2 == 0) continue;
