@@ -16,7 +16,7 @@ serial equivalence, test_moe.cpp:288-330) are checked where they are cheap and e
   * the full-size grouped GEMMs (fwd, dgrad, wgrad shapes) against torch fp32;
   * the fused AdamW-in-wgrad step against the unfused optimizer path, and the kept
     gradients of the fused step against the unfused backward, bit for bit.
-Tolerances as tests/test_gpu_layer.py: rel-L2 <= 2e-2 for bf16-stored activations and
+Tolerances as tests/test_gpu_layer.py: rel-L2 <= 1e-2 for bf16-stored activations and
 gradients, logits 1e-5, fused vs unfused parameters 1e-3 (the same bf16-rounded gradient
 and the same update expression: in practice identical)."""
 import numpy as np
@@ -28,7 +28,7 @@ torch = pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from tests._util import from_dev, rel_l2, to_dev_bf16  # noqa: E402
 
-TOL = 2e-2
+TOL = 1e-2  # measured worst 4.5e-3 over the 1-GPU parity suite (tools: TED_TOL_REPORT)
 N_TOK, H, E, CF = 32768, 4096, 16, 1.25
 F = 4 * H
 

@@ -4,7 +4,7 @@ Mirrors the reference's own tests: SerialEquivalence (test_moe.cpp:288-330, here
 oracle is the serial model), Gate KAT, dispatch/placement bookkeeping, and the
 synthetic objective loss = sum(y^2)/(2N) with dy = y/N (moe.cpp:379-391).
 Tolerances (stated here, the reference is fp64-only): routing bit-exact given the GPU's
-fp32 logits; outputs / gradients rel-L2 <= 2e-2 (bf16 storage of X, Z, H, Fe, dFe, dZ
+fp32 logits; outputs / gradients rel-L2 <= 1e-2 (bf16 storage of X, Z, H, Fe, dFe, dZ
 and of every gradient, fp32 accumulation)."""
 import numpy as np
 import pytest
@@ -15,7 +15,7 @@ torch = pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from tests._util import rel_l2, to_dev_bf16, from_dev  # noqa: E402
 
-TOL = 2e-2
+TOL = 1e-2  # measured worst 4.5e-3 over the 1-GPU parity suite (tools: TED_TOL_REPORT)
 
 
 def _make(n, h, E, cf, seed):

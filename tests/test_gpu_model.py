@@ -1,6 +1,6 @@
 """The whole model (layer stack: attention stand-in + MoE / dense FFN, ted_model_*) on one
 GPU against the reference's own SerialModel losses over 3 training steps (forward, loss,
-backward, AdamW) on identical seeded parameters and batch.  Tolerance: 2e-2 relative per
+backward, AdamW) on identical seeded parameters and batch.  Tolerance: 1e-2 relative per
 step (bf16 storage of activations, weights and gradients; the reference is fp64)."""
 import numpy as np
 import pytest
@@ -9,8 +9,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 from tests._stack import golden_losses, stack_batch, stack_params  # noqa: E402
+from tests._util import record  # noqa: E402
 
-TOL = 2e-2
+TOL = 1e-2  # relative per step; see record() / TED_TOL_REPORT for the measured values
 
 
 @pytest.mark.parametrize("layers,h,E,n,seed", [(2, 256, 4, 128, 1), (4, 256, 4, 128, 5),
@@ -30,6 +31,7 @@ def test_stack_matches_reference_serial_model(layers, h, E, n, seed):
         M.step(batch)
         losses.append(M.loss())
     ref = golden_losses(layers, h, E, n, seed, 1)
+    record(float(np.max(np.abs(np.array(losses) - ref) / np.abs(ref))))
     np.testing.assert_allclose(losses, ref, rtol=TOL)
     M.close()
 

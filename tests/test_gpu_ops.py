@@ -2,7 +2,7 @@
 ted_dispatch_forward -> ted_expert_ffn_forward -> ted_combine_forward, and back through
 ted_combine_backward -> ted_expert_ffn_backward -> ted_gate_backward_dlogits) against the
 fp64 oracle, the way SerialModel::forward_layer / backward_layer compose the reference's
-free functions (moe.cpp:989-1064).  Same tolerances as the layer tests (rel-L2 <= 2e-2)."""
+free functions (moe.cpp:989-1064).  Same tolerances as the layer tests (rel-L2 <= 1e-2)."""
 import numpy as np
 import pytest
 
@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 from oracle import oracle as O  # noqa: E402
 from tests._util import from_dev, rel_l2, to_dev_bf16  # noqa: E402
 
-TOL = 2e-2
+TOL = 1e-2  # measured worst 4.5e-3 over the 1-GPU parity suite (tools: TED_TOL_REPORT)
 
 
 @pytest.mark.parametrize("n,h,E,cf,seed", [(1024, 256, 4, 0.0, 1), (1024, 256, 4, 1.25, 11),
