@@ -127,9 +127,8 @@ def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
 
     Two error figures: `y_rel_l2_sampled` = ||y - ref|| / ||ref||, and `y_err_vs_terms` =
     ||y - ref|| / ||p (|H| |W2_e| + |b2_e|)||, the error against the magnitude of the terms
-    summed into y.  Training on one fixed batch drives y (the objective is sum(y^2)/2N)
-    towards zero by cancellation, so after many steps ||ref|| shrinks while the rounding
-    error of the terms does not: `condition` = ||terms|| / ||ref|| says by how much."""
+    summed into y; `condition` = ||terms|| / ||ref|| (about sqrt(ffn) for random weights;
+    thousands on the batch the layer was trained on, where y cancels)."""
     import numpy as np
     import torch
     y = torch.empty_like(a)
@@ -171,17 +170,17 @@ def sampled_parity(L, a, w, T, P, tokens=8, seed=0):
 
 
 def parity_verdict(before, after):
-    """`before`: the check on the initialised parameters (ahead of the warm-up steps), pass
-    = routing bit-exact and y rel-L2 <= 2e-2; `after`: the same check once the timed steps
-    have trained the parameters, pass = routing bit-exact and the error against the term
-    magnitudes <= 2e-2 (its plain rel-L2 is reported, scaled by the cancellation
-    `condition`)."""
-    ok_b = bool(before["routing_bit_exact_all_tokens"] and before["y_rel_l2_sampled"] < 2e-2)
-    ok_a = bool(after["routing_bit_exact_all_tokens"] and after["y_err_vs_terms"] < 2e-2)
-    return {"before_steps": before, "after_steps": after, "tolerance": 2e-2, "pass": ok_b and ok_a,
+    """`before`: the check on the initialised parameters and the benched tokens (ahead of the
+    warm-up steps); `after`: the same check once the timed steps have trained the
+    parameters, on a fresh batch of tokens (training on one fixed batch cancels y on that
+    batch -- the objective is sum(y^2)/2N -- which only inflates the relative error there:
+    see `condition`).  Pass = routing bit-exact and y rel-L2 <= 1e-2, both times."""
+    ok = all(r["routing_bit_exact_all_tokens"] and r["y_rel_l2_sampled"] < 1e-2
+             for r in (before, after))
+    return {"before_steps": before, "after_steps": after, "tolerance": 1e-2, "pass": bool(ok),
             "check": "routing of all tokens vs argmax of the GPU logits; y of sampled kept "
-                     "tokens vs fp64 numpy on the layer's bf16 parameters, on the initialised "
-                     "parameters (rel-L2) and after the timed steps (error vs term magnitude)"}
+                     "tokens vs fp64 numpy on the layer's bf16 parameters (rel-L2), on the "
+                     "initialised parameters and, after the timed steps, on fresh tokens"}
 
 
 def quick_layer_bench(w, steps: int, warmup: int):
@@ -562,7 +561,13 @@ def run_ours(args, w, rank, world, local_rank, dist):
     ms = max_over_ranks(ms)
     stats = L.stats()
     loss = L.loss()
-    parity = parity_verdict(parity0, sampled_parity(L, a, w, T, P)) if do_parity else None
+    parity = None
+    if do_parity:
+        g2 = torch.Generator(device="cuda")
+        g2.manual_seed(7777)
+        a_new = torch.randn(n, w["hidden"], device="cuda", generator=g2).bfloat16()
+        parity = parity_verdict(parity0, sampled_parity(L, a_new, w, T, P))
+        del a_new
 
     # e2e through the public API: every step's tokens are copied from pinned host memory
     # (on a copy stream into one of two device buffers, so step i+1's H2D runs under step
