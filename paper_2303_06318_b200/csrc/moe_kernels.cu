@@ -337,7 +337,7 @@ __global__ void zero_pad_kernel(bf16* buf, int64_t ld, int h, const int* seg_off
 }
 
 // ------------------------------------------------------------------ combine
-__global__ void __launch_bounds__(kThreads) combine_fwd_kernel(const bf16* __restrict__ fhome,
+__global__ void __launch_bounds__(kThreads, 4) combine_fwd_kernel(const bf16* __restrict__ fhome,
                                                                const int* __restrict__ pos_home,
                                                                const float* __restrict__ prob,
                                                                int64_t n, int h,
