@@ -910,6 +910,80 @@ __global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restri
   }
 }
 
+// The same reduction four columns per thread (float4 loads: 4x the bytes in flight per load
+// instruction) with the identical per-column summation order as sum_partials_kernel, so
+// the results are bit-identical.  Needs M, stride and w multiples of 4, part 16 B aligned.
+__global__ void __launch_bounds__(256) sum_partials4_kernel(const float* __restrict__ part,
+                                                            int64_t stride, int64_t M,
+                                                            int ns_const,
+                                                            const int* __restrict__ seg_off,
+                                                            int w, int rows_per_split,
+                                                            bf16* __restrict__ out,
+                                                            int64_t out_stride) {
+  __shared__ float4 s_acc[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = (int64_t(blockIdx.x) * 32 + lane) * 4;  // columns m .. m+3, one group
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (m < M) {
+    int ns = ns_const;
+    if (seg_off) {
+      const int g = int(m / w);
+      ns = (seg_off[g + 1] - seg_off[g] + rows_per_split - 1) / rows_per_split;
+    }
+    float4 a4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a4[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto add = [](float4& x, const float4 y) {
+      x.x += y.x;
+      x.y += y.y;
+      x.z += y.z;
+      x.w += y.w;
+    };
+    int sidx = warp;
+    for (; sidx + 24 < ns; sidx += 32) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = *reinterpret_cast<const float4*>(part + int64_t(sidx + 8 * u) * stride + m);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) add(a4[u], v[u]);
+    }
+    for (; sidx < ns; sidx += 8)
+      add(a4[0], *reinterpret_cast<const float4*>(part + int64_t(sidx) * stride + m));
+    acc.x = (a4[0].x + a4[1].x) + (a4[2].x + a4[3].x);
+    acc.y = (a4[0].y + a4[1].y) + (a4[2].y + a4[3].y);
+    acc.z = (a4[0].z + a4[1].z) + (a4[2].z + a4[3].z);
+    acc.w = (a4[0].w + a4[1].w) + (a4[2].w + a4[3].w);
+  }
+  s_acc[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && m < M) {
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 v = s_acc[q][lane];
+      t[0] += v.x;
+      t[1] += v.y;
+      t[2] += v.z;
+      t[3] += v.w;
+    }
+    bf16* o = out + (m / w) * out_stride + (m % w);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] = __float2bfloat16(t[c]);
+  }
+}
+
+void sum_partials(const float* part, int64_t stride, int64_t M, int ns_const, const int* seg_off,
+                  int w, int rows_per_split, bf16* out, int64_t out_stride, cudaStream_t s) {
+  if (M % 4 == 0 && stride % 4 == 0 && w % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(part) & 15) == 0)
+    sum_partials4_kernel<<<unsigned((M + 127) / 128), 256, 0, s>>>(part, stride, M, ns_const, seg_off, w,
+                                                         rows_per_split, out, out_stride);
+  else
+    sum_partials_kernel<<<unsigned((M + 31) / 32), 256, 0, s>>>(part, stride, M, ns_const, seg_off, w,
+                                                        rows_per_split, out, out_stride);
+}
+
 // ------------------------------------------------------------------ bias-grad column sums
 constexpr int kColRows = 32;  // rows per partial
 
@@ -1389,7 +1463,7 @@ cudaError_t gate_backward_weight(const bf16* a, const float* dlogits, int64_t n,
                                                                        tok, part);
   }
   const int64_t M = int64_t(h) * E;
-  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, nb, nullptr, int(M), 1, dwg, 0);
+  sum_partials(part, M, M, nb, nullptr, int(M), 1, dwg, 0, s);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -1406,8 +1480,7 @@ cudaError_t colsum_groups(const bf16* D, int64_t ld, int w, const int* seg_off, 
   dim3 grid(ceil_div(w / 8, 128), G * rsplits);
   colsum_part_kernel<<<grid, 128, 0, s>>>(D, ld, w, seg_off, G, rsplits, part);
   const int64_t M = int64_t(G) * w;
-  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, 0, seg_off, w, kColRows, out,
-                                                      out_stride);
+  sum_partials(part, M, M, 0, seg_off, w, kColRows, out, out_stride, s);
   count_launch(2);
   return cudaGetLastError();
 }
@@ -1416,8 +1489,7 @@ cudaError_t colsum_finish(const float* part, int w, const int* seg_off, int G, b
                           int64_t out_stride, cudaStream_t s) {
   if (w % 8 != 0 || G < 1) return cudaErrorInvalidValue;
   const int64_t M = int64_t(G) * w;
-  sum_partials_kernel<<<ceil_div(M, 32), 256, 0, s>>>(part, M, M, 0, seg_off, w, kColRows, out,
-                                                      out_stride);
+  sum_partials(part, M, M, 0, seg_off, w, kColRows, out, out_stride, s);
   count_launch(1);
   return cudaGetLastError();
 }
